@@ -1,0 +1,120 @@
+// ref_shim.cpp -- C ABI over the UNMODIFIED reference implementation.
+// TEST / BASELINE INFRASTRUCTURE ONLY.
+//
+// Compiled against /root/reference/proj/include where it lies (nothing is
+// copied) into oracle/_ref/libref_logtrawl.so by oracle/Makefile.  Used to
+// pin the C restatement (oracle/pfac_oracle.c) and as the CPU baseline
+// ("kind": "reference") in bench.py: the timed call is the reference's own
+// measure() harness (bench.hpp:64-113) over pfac_scan + verify_hits.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "logtrawl/bench.hpp"
+#include "logtrawl/kmp.hpp"
+#include "logtrawl/pipeline.hpp"
+
+using namespace logtrawl;
+
+namespace {
+struct ref_hit {
+  uint64_t offset;
+  uint32_t pattern_id, matched_len;
+};
+struct ref_alert {
+  uint64_t offset;
+  uint32_t rule_id, pattern_len;
+  uint64_t line;
+};
+
+RuleSet rules_of(const uint8_t* bytes, const uint64_t* off, uint32_t k) {
+  RuleSet r;
+  for (uint32_t i = 0; i < k; ++i) {
+    Pattern p;
+    p.id = i;
+    p.name = "r" + std::to_string(i);
+    p.bytes.assign((const char*)bytes + off[i], off[i + 1] - off[i]);
+    r.max_len = std::max(r.max_len, p.bytes.size());
+    r.patterns.push_back(std::move(p));
+  }
+  return r;
+}
+}  // namespace
+
+extern "C" {
+
+// truncate_prefixes -> build_failureless_trie -> pfac_scan -> verify_hits
+int ref_pfac_scan_verify(const uint8_t* text, uint64_t n, const uint8_t* bytes,
+                         const uint64_t* off, uint32_t k, uint64_t L, int compact,
+                         unsigned workers, int with_lines, ref_hit** hits_out,
+                         uint64_t* n_hits, ref_alert** alerts_out, uint64_t* n_alerts) {
+  try {
+    RuleSet r = rules_of(bytes, off, k);
+    std::string_view tv((const char*)text, n);
+    PrefixSet ps = truncate_prefixes(r, L);
+    Automaton trie = build_failureless_trie(ps, compact ? Backend::compact : Backend::dense);
+    auto hits = pfac_scan(tv, trie, {.workers = workers});
+    LineIndex idx(tv);
+    auto alerts = verify_hits(tv, hits, ps, r, with_lines ? &idx : nullptr);
+    *hits_out = (ref_hit*)malloc(sizeof(ref_hit) * (hits.size() + 1));
+    for (size_t i = 0; i < hits.size(); ++i)
+      (*hits_out)[i] = {hits[i].offset, hits[i].pattern_id, hits[i].matched_len};
+    *n_hits = hits.size();
+    *alerts_out = (ref_alert*)malloc(sizeof(ref_alert) * (alerts.size() + 1));
+    for (size_t i = 0; i < alerts.size(); ++i)
+      (*alerts_out)[i] = {alerts[i].offset, alerts[i].rule_id, alerts[i].pattern_len,
+                          alerts[i].line};
+    *n_alerts = alerts.size();
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (const CapacityError&) {
+    return 2;
+  } catch (const std::logic_error&) {
+    return 3;
+  } catch (...) {
+    return 4;
+  }
+}
+
+// The reference benchmark harness (bench.hpp:64-113): prebuilds the trie,
+// one untimed warm-up, then `runs` timed pfac_scan + verify_hits (or
+// kmp_multi).  engine: 0 kmp, 1 pfac_dense, 2 pfac_compact.
+int ref_measure(const uint8_t* text, uint64_t n, const uint8_t* bytes, const uint64_t* off,
+                uint32_t k, uint64_t L, int engine, unsigned workers, uint64_t runs,
+                double* mean_seconds, double* throughput_bps) {
+  try {
+    RuleSet r = rules_of(bytes, off, k);
+    EngineConfig cfg;
+    cfg.engine = engine == 0 ? EngineKind::kmp
+                             : (engine == 1 ? EngineKind::pfac_dense : EngineKind::pfac_compact);
+    cfg.prefix_len = L;
+    cfg.workers = workers;
+    ThroughputReport rep = measure(cfg, std::string_view((const char*)text, n), r, runs);
+    *mean_seconds = rep.mean_seconds;
+    *throughput_bps = rep.throughput_bps;
+    return 0;
+  } catch (...) {
+    return 4;
+  }
+}
+
+int ref_kmp_search(const uint8_t* text, uint64_t n, const uint8_t* p, uint32_t m,
+                   uint64_t** offs, uint64_t* n_offs, uint64_t* comparisons) {
+  Pattern pt{0, "p", std::string((const char*)p, m)};
+  FailureTable ft = build_failure_table(pt);
+  uint64_t cmp = 0;
+  auto v = kmp_search(std::string_view((const char*)text, n), pt, ft, &cmp);
+  *offs = (uint64_t*)malloc(sizeof(uint64_t) * (v.size() + 1));
+  for (size_t i = 0; i < v.size(); ++i) (*offs)[i] = v[i];
+  *n_offs = v.size();
+  *comparisons = cmp;
+  return 0;
+}
+
+unsigned ref_default_workers(void) { return default_workers(); }
+
+void ref_free(void* p) { free(p); }
+}
