@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""PFAC log-scan throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl glop|reference] [--config pfac|kmp]
+
+Workload (configs[2] / configs[3] of BASELINE.json): synthetic RFC 5424 syslog,
+8e9 bytes per GPU (weak scaling; 64e9 at 8 GPUs), 1,000 8-byte patterns
+(half reference random_rules, half incident vocabulary), prefix L = 8.
+A step = one pass of the hot path over the GPU's shard: device PFAC scan +
+stage-2 verify + per-pattern counts (+ the NCCL count all-reduce at N > 1).
+`value` has the text already in HBM; `e2e` goes through the public pipeline
+call with the text in pinned HOST memory (H2D + scan + verify + D2H of alerts
+inside the timed region).  The 8 GB shard is larger than L2, so no flush.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PFAC log-scan Gbps at 1/2/4/8 B200 vs pattern count; % of HBM roofline"
+KMP_METRIC = "KMP log-scan Gbps (single pattern 'Failed password'), 1 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["glop", "reference"], default="glop")
+    ap.add_argument("--config", choices=["pfac", "kmp"], default="pfac")
+    ap.add_argument("--bytes-per-gpu", type=float, default=8e9)
+    ap.add_argument("--patterns", type=int, default=1000)
+    ap.add_argument("--prefix-len", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--rules-seed", type=int, default=606)
+    ap.add_argument("--kernel", choices=["auto", "filtered", "direct"], default="auto")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline work")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kind: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        return s.get(kind, {}).get("dram_bytes_per_launch"), s.get(kind, {}).get("bytes_per_launch")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def cpu_baseline_pfac(text_host, pats, L, target_s):
+    """The reference pfac_scan + verify_hits (oracle/_ref, all host threads)
+    on a bounded sample of the same workload; falls back to the C port."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as O
+
+    ref = O.ref()
+    kind = "reference" if ref is not None else "port"
+    timer = O.ref_time_pfac if ref is not None else (lambda t, p, l, w, r: O.port_time_pfac(t, p, l, w, r))
+    probe = min(len(text_host), 64 << 20)
+    secs, _ = timer(text_host[:probe], pats, L, 0, 1)
+    per_byte = max(secs[0], 1e-6) / probe
+    runs = 3
+    sample = int(min(len(text_host), max(probe, target_s / runs / per_byte)))
+    secs, na = timer(text_host[:sample], pats, L, 1, runs)
+    mean = statistics.mean(secs)
+    cores = int(ref.ref_default_workers()) if ref is not None else 1
+    return {"value": round(8 * sample / mean / 1e9, 3), "unit": "Gbps", "cores": cores, "kind": kind,
+            "sample": f"first {sample} bytes of the GPU-0 shard, same {len(pats)} rules, L={L}; pfac_scan + "
+                      f"verify_hits, {runs} timed runs after 1 warm-up, mean {mean:.3f} s/run, "
+                      f"{'workers=hardware_concurrency' if kind == 'reference' else 'single thread'}"}
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+
+    import oracle_ffi as O
+    from paper_1704_02278_b200 import glop
+
+    ref = O.ref()
+    kind = "reference" if ref is not None else "port"
+    budget = 120.0  # seconds for warmup + steps
+    if args.config == "kmp":
+        p = b"Failed password"
+        probe = glop.gen_syslog_host(64 << 20, args.seed)
+        secs, _ = (O.ref_time_kmp(probe, p, 0, 1) if ref is not None else ([time.perf_counter()], 0))
+        per_byte = max(secs[0], 1e-6) / probe.size
+        sample = int(min(args.bytes_per_gpu, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
+        text = glop.gen_syslog_host(sample, args.seed)
+        secs, nm = O.ref_time_kmp(text, p, args.warmup, args.steps)
+        cores, metric = 1, KMP_METRIC
+        config = {"workload": "configs[1]: KMP 'Failed password' over synthetic RFC 5424 syslog",
+                  "bytes": int(args.bytes_per_gpu), "sample_bytes": sample}
+        desc = f"kmp_multi (kmp.hpp:74) single-threaded by design on the first {sample} bytes"
+    else:
+        pats, _ = glop.gen_rules(args.patterns, args.rules_seed)
+        probe = glop.gen_syslog_host(64 << 20, args.seed)
+        timer = O.ref_time_pfac if ref is not None else (lambda t, q, l, w, r: O.port_time_pfac(t, q, l, w, r))
+        secs, _ = timer(probe, pats, args.prefix_len, 0, 1)
+        per_byte = max(secs[0], 1e-6) / probe.size
+        sample = int(min(args.bytes_per_gpu, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
+        text = glop.gen_syslog_host(sample, args.seed)
+        secs, na = timer(text, pats, args.prefix_len, args.warmup, args.steps)
+        cores = int(ref.ref_default_workers()) if ref is not None else 1
+        metric = METRIC
+        config = workload_config(args, 1)
+        config["sample_bytes"] = sample
+        desc = (f"reference pfac_scan + verify_hits (oracle/_ref built from /root/reference), workers={cores}, "
+                f"on the first {sample} bytes of the same corpus and rules")
+    mean = statistics.mean(secs)
+    value = 8 * sample / mean / 1e9
+    line = {"impl": "reference", "metric": metric, "value": round(value, 3), "unit": "Gbps", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic RFC 5424 syslog (csrc/corpus.h)", "config": config,
+            "cpu_baseline": {"value": round(value, 3), "unit": "Gbps", "cores": cores, "kind": kind, "sample": desc},
+            "e2e": {"value": round(value, 3), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world):
+    return {"workload": "configs[2]/[3]: PFAC, %d patterns (8-byte prefixes), %.0f GB synthetic RFC 5424 syslog "
+                        "per GPU" % (args.patterns, args.bytes_per_gpu / 1e9),
+            "bytes_per_gpu": int(args.bytes_per_gpu), "total_bytes": int(args.bytes_per_gpu) * world,
+            "patterns": args.patterns, "prefix_len": args.prefix_len, "corpus_seed": args.seed,
+            "rules_seed": args.rules_seed, "kernel": args.kernel,
+            "parallelism": f"shard{world} (contiguous log shards, 7-byte halo)",
+            "l2": "inputs larger than L2 (>= 8 GB per GPU), no flush needed"}
+
+
+# --------------------------------------------------------------------- glop arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1704_02278_b200 import glop
+    from paper_1704_02278_b200.shards import plan_shards
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = glop.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    S = int(args.bytes_per_gpu)
+    total = S * world
+    kernel = {"auto": glop.PFAC_AUTO, "filtered": glop.PFAC_FILTERED, "direct": glop.PFAC_DIRECT}[args.kernel]
+
+    if args.config == "kmp":
+        return bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks)
+
+    pats, _ = glop.gen_rules(args.patterns, args.rules_seed)
+    trie = ctx.upload(glop.build_failureless_trie(pats, args.prefix_len))
+    rules = ctx.upload_rules(pats, args.prefix_len)
+    info = trie.info
+    halo = max(info.max_depth, max(len(p) for p in pats)) - 1
+    sh = plan_shards(total, world, halo)[rank]
+    d_text = torch.empty(sh.read + 64, dtype=torch.uint8, device="cuda")
+    ctx.gen_syslog_device(d_text.data_ptr(), sh.read, args.seed, begin=sh.lo)
+    ctx.synchronize()
+    cap = max(1 << 20, S // 256)
+    d_hits = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
+    d_alerts = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
+    d_counts = torch.zeros(args.patterns, dtype=torch.int64, device="cuda")
+
+    def step():
+        with torch.cuda.stream(stream):
+            d_counts.zero_()
+        nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), sh.read, d_hits.data_ptr(), cap, own=sh.own,
+                                  base=sh.lo, kernel=kernel)
+        na = ctx.verify_hits_device(rules, d_text.data_ptr(), sh.read, d_hits.data_ptr(), nh, d_alerts.data_ptr(),
+                                    d_counts.data_ptr(), base=sh.lo)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(d_counts)
+        return nh, na
+
+    for _ in range(max(args.warmup, 3)):
+        nh, na = step()
+    ctx.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        l0 = ctx.launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        kms = []
+        for _ in range(args.steps):
+            nh, na = step()
+            kms.append(ctx.last_kernel_ms())
+        ev1.record(stream)
+        ctx.synchronize()
+        barrier()
+        launches = ctx.launches - l0
+        ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        kernel_ms = max_over_ranks(statistics.mean(kms))
+        total_alerts = int(d_counts.sum().item())
+
+        e2e = None
+        if not args.no_e2e:
+            e2e = run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, torch, dist)
+    clocks = sampler.summary()
+
+    value = 8 * total / (ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    achieved = sh.own / (kernel_ms / 1e3) / 1e9  # GB/s of the dominant kernel
+    traffic, _ = ncu_traffic("pfac_tile_kernel")
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "Gbps", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic RFC 5424 syslog generated on device (csrc/corpus.h), seeded",
+            "config": workload_config(args, world),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "pfac_tile_kernel", "kernel_ms": round(kernel_ms, 4),
+                         "algorithmic_bytes_per_launch": sh.own,
+                         "step_share": round(kernel_ms / ms, 3)},
+            "gpu_launches": launches, "clocks": clocks,
+            "results": {"stage1_hits_per_gpu_step": int(nh), "alerts_per_step": total_alerts,
+                        "trie": {"states": info.state_count, "classes": info.classes, "q": info.q,
+                                 "stride": info.stride, "table_bytes": int(info.table_bytes),
+                                 "table_in_smem": bool(info.table_in_smem)}}}
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample = min(sh.own, 2 << 30)
+        host = d_text[:sample].cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline_pfac(host, pats, args.prefix_len, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, torch, dist):
+    """Same metric through the public pipeline call with the shard in pinned
+    host memory: H2D copy + scan + verify + D2H alerts/counts every step."""
+    host = ctx.host_alloc(sh.read)
+    try:
+        ctx.memcpy(host, d_text.data_ptr(), sh.read, 2)
+        ctx.synchronize()
+        steps = args.e2e_steps or args.steps
+        alerts, counts, s1 = ctx.run_pfac_pipeline(trie, rules, host, sh.read, False, own=sh.own, base=sh.lo)
+        barrier()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(steps):
+            alerts, counts, s1 = ctx.run_pfac_pipeline(trie, rules, host, sh.read, False, own=sh.own, base=sh.lo)
+            if world > 1:
+                c = torch.from_numpy(counts.astype("int64")).cuda()
+                dist.all_reduce(c)
+            d2h = alerts.nbytes + counts.nbytes
+        barrier()
+        dt = max_over_ranks((time.perf_counter() - t0) / steps)
+    finally:
+        ctx.host_free(host)
+    return {"value": round(8 * sh.own * world / dt / 1e9, 2), "unit": "Gbps", "h2d_bytes_per_step": sh.read,
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 3),
+            "api": "glop_run_pfac_pipeline_shard (pinned host text)"}
+
+
+def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
+    import torch
+
+    from paper_1704_02278_b200 import glop
+
+    S = int(min(args.bytes_per_gpu, 1e9)) if args.bytes_per_gpu == 8e9 else int(args.bytes_per_gpu)
+    p = b"Failed password"
+    d_text = torch.empty(S + 64, dtype=torch.uint8, device="cuda")
+    ctx.gen_syslog_device(d_text.data_ptr(), S, args.seed, begin=rank * S)
+    ctx.synchronize()
+    cap = 1 << 24
+    d_out = torch.empty(cap * 8, dtype=torch.uint8, device="cuda")
+    for _ in range(max(args.warmup, 3)):
+        nm, cmp_ = ctx.kmp_search_device(p, d_text.data_ptr(), S, d_out.data_ptr(), cap, base=rank * S)
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        l0 = ctx.launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        kms = []
+        for _ in range(args.steps):
+            nm, cmp_ = ctx.kmp_search_device(p, d_text.data_ptr(), S, d_out.data_ptr(), cap, base=rank * S)
+            kms.append(ctx.last_kernel_ms())
+        ev1.record(stream)
+        ctx.synchronize()
+        barrier()
+        launches = ctx.launches - l0
+        ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        kernel_ms = max_over_ranks(statistics.mean(kms))
+    peak, peak_src = peaks()
+    achieved = S / (kernel_ms / 1e3) / 1e9
+    line = {"metric": KMP_METRIC, "value": round(8 * S * world / (ms / 1e3) / 1e9, 2), "unit": "Gbps",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic RFC 5424 syslog generated on device", "config": {
+                "workload": "configs[1]: KMP single pattern 'Failed password' over 1 GB synthetic syslog",
+                "bytes_per_gpu": S, "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("kmp_tile_kernel")[0],
+                         "peak_source": peak_src, "kernel": "kmp_tile_kernel", "kernel_ms": round(kernel_ms, 4)},
+            "gpu_launches": launches, "clocks": sampler.summary(), "results": {"matches": int(nm),
+                                                                              "comparisons": int(cmp_)}}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_ffi as O
+
+        sample = min(S, 256 << 20)
+        host = d_text[:sample].cpu().numpy()
+        if O.ref() is not None:
+            secs, _ = O.ref_time_kmp(host, p, 1, 3)
+            line["cpu_baseline"] = {"value": round(8 * sample / statistics.mean(secs) / 1e9, 3), "unit": "Gbps",
+                                    "cores": 1, "kind": "reference",
+                                    "sample": f"kmp_multi on the first {sample} bytes, single thread by design"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

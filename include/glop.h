@@ -1,0 +1,233 @@
+/*
+ * glop.h -- C ABI of the B200-native GLoP matching path (libglop.so).
+ *
+ * This is the drop-in boundary underneath the reference's C++ API
+ * (namespace logtrawl, /root/reference/proj/include/logtrawl/*.hpp).  The C++
+ * headers in include/logtrawl/ keep the reference signatures and call these
+ * entry points; every entry point below names the reference interface it
+ * replaces.  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Conventions
+ *  - Every function returns a glop_status; on failure glop_last_error()
+ *    returns a thread-local message.  The C++ shim maps codes onto the
+ *    reference's exception types (see include/logtrawl/detail/abi.hpp).
+ *  - "host" pointers may be pageable or pinned; "device" pointers are CUDA
+ *    device pointers on the context's device.
+ *  - Arrays returned through `T** out` are library-owned host memory, released
+ *    with glop_free().
+ *  - A glop_ctx owns one CUDA stream plus scratch; calls on one context are
+ *    serialised, calls on different contexts run concurrently.  A glop_trie /
+ *    glop_rules is immutable after upload and may be shared by contexts on the
+ *    same device (automaton.hpp "immutable value, shareable").
+ *  - There is no CPU fallback: without a usable sm_100 device, calls fail with
+ *    GLOP_ECUDA.
+ */
+#ifndef GLOP_H_
+#define GLOP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GLOP_OK = 0,
+  GLOP_EINVAL = 1,    /* reference: std::invalid_argument              */
+  GLOP_ECAPACITY = 2, /* reference: logtrawl::CapacityError            */
+  GLOP_ELOGIC = 3,    /* reference: std::logic_error (verify.hpp:76-77) */
+  GLOP_ECUDA = 4,     /* device / driver failure (std::runtime_error)   */
+  GLOP_ENOMEM = 5     /* allocation failure (std::bad_alloc)            */
+} glop_status;
+
+/* Layout-identical to logtrawl::Hit (scan.hpp:31-41) on LP64: 16 bytes. */
+typedef struct {
+  uint64_t offset;
+  uint32_t pattern_id;
+  uint32_t matched_len;
+} glop_hit;
+
+/* Layout-identical to logtrawl::AutomatonOutput (automaton.hpp:43-49). */
+typedef struct {
+  uint32_t pattern_id;
+  uint32_t matched_len;
+} glop_output;
+
+/* Verified match (verify.hpp:19-28 Alert without the name string / line). */
+typedef struct {
+  uint64_t offset;
+  uint32_t rule_id;
+  uint32_t pattern_len;
+} glop_alert;
+
+typedef struct glop_ctx glop_ctx;
+typedef struct glop_trie glop_trie;
+typedef struct glop_rules glop_rules;
+
+/* PFAC kernel selection.  AUTO picks the q-gram-filtered kernel (the
+ * GPU analogue of the reference's RootJump, scan.hpp:81-108); DIRECT is
+ * the literal one-thread-per-byte walk (scan.hpp:113-170).  Both are exact
+ * and return identical results. */
+typedef enum { GLOP_PFAC_AUTO = 0, GLOP_PFAC_FILTERED = 1, GLOP_PFAC_DIRECT = 2 } glop_pfac_kernel;
+
+const char* glop_last_error(void);
+const char* glop_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+glop_status glop_ctx_create(int device, glop_ctx** out);
+glop_status glop_ctx_destroy(glop_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t as void*), for callers that want to
+ * order their own work (events, NCCL) against library calls. */
+void* glop_ctx_stream(glop_ctx* ctx);
+glop_status glop_ctx_synchronize(glop_ctx* ctx);
+
+/* ---- automaton ------------------------------------------------------------
+ * Replaces the consumer side of build_failureless_trie (automaton.hpp:283-291):
+ * takes the reference's own dense representation -- Q x 256 int32 goto table
+ * with -1 = no edge (automaton.hpp:57), CSR outputs out_offsets[Q+1] /
+ * out_flat (automaton.hpp:78-79) -- and flattens it once into the device
+ * layout: byte->class map, alphabet-compressed transition table (u16 entries
+ * when Q < 32768), per-pattern lengths and the q-gram filter tables.
+ * Fails with GLOP_EINVAL if the input is not a failureless trie (an edge to
+ * the root, a state with two parents, an unreachable state). */
+glop_status glop_trie_upload(glop_ctx* ctx, const int32_t* dense_table, uint32_t state_count,
+                             const uint32_t* out_offsets, const glop_output* out_flat,
+                             glop_trie** out);
+glop_status glop_trie_destroy(glop_trie* trie);
+/* Introspection for tests: state count, alphabet classes, min/max output
+ * depth, filter q-gram length and stride, table bytes, whether the table is
+ * staged in shared memory by the filtered kernel. */
+typedef struct {
+  uint32_t state_count, classes, min_depth, max_depth, q, stride, entry_bytes, table_in_smem;
+  uint64_t table_bytes;
+} glop_trie_info;
+glop_status glop_trie_get_info(const glop_trie* trie, glop_trie_info* info);
+
+/* ---- PFAC scan ------------------------------------------------------------
+ * Replaces pfac_scan (scan.hpp:177-202): every start position of `text`
+ * walks the failureless trie; a Hit is emitted for every output of every
+ * visited state; the result is sorted by (offset, pattern_id).
+ * glop_pfac_scan: host-facing; `text_on_device` says where text lives; the
+ * result is a library-owned host array (glop_free). */
+glop_status glop_pfac_scan(glop_ctx* ctx, const glop_trie* trie, const uint8_t* text, uint64_t n,
+                           int text_on_device, glop_hit** hits, uint64_t* n_hits);
+
+/* Device-resident form for shards and pipelines: reads text[0, n) (device),
+ * reports only starts in [0, own) (own <= n; the bytes [own, n) are the halo),
+ * adds `base` to every reported offset, and writes the sorted hits to
+ * out[0, min(cap, total)).  *n_hits is the total; if it exceeds cap the call
+ * returns GLOP_ECAPACITY and the caller retries with a larger buffer. */
+glop_status glop_pfac_scan_device(glop_ctx* ctx, const glop_trie* trie, const uint8_t* d_text,
+                                  uint64_t n, uint64_t own, uint64_t base, glop_pfac_kernel kernel,
+                                  glop_hit* d_out, uint64_t cap, uint64_t* n_hits);
+
+/* ---- end-to-end PFAC pipeline --------------------------------------------
+ * The device half of run_engine_scan's PFAC branch (pipeline.hpp:86-97):
+ * text (host or device) -> pfac_scan -> verify_hits -> alerts + per-pattern
+ * counts, one host->device copy of the text and one device->host copy of the
+ * alerts.  `counts` (optional, host, n_patterns u64) receives the alert
+ * histogram; `stage1_hits` the pre-verification hit count. */
+glop_status glop_run_pfac_pipeline(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules,
+                                   const uint8_t* text, uint64_t n, int text_on_device,
+                                   glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                                   uint64_t* stage1_hits);
+/* Shard form: text covers global offsets [base, base+n); only starts in
+ * [base, base+own) are reported. */
+glop_status glop_run_pfac_pipeline_shard(glop_ctx* ctx, const glop_trie* trie,
+                                         const glop_rules* rules, const uint8_t* text, uint64_t n,
+                                         uint64_t own, uint64_t base, int text_on_device,
+                                         glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                                         uint64_t* stage1_hits);
+
+/* ---- measurement ----------------------------------------------------------
+ * Device time of the most recent PFAC / KMP scan kernel on this context,
+ * from CUDA events recorded on the context stream around the launch. */
+glop_status glop_last_kernel_ms(glop_ctx* ctx, float* ms);
+/* Number of kernels this context has launched so far. */
+uint64_t glop_ctx_launch_count(glop_ctx* ctx);
+
+/* ---- stage-2 verification ------------------------------------------------
+ * Patterns for verify_hits (verify.hpp:69-105): bytes of pattern i are
+ * bytes[off[i], off[i+1]), its id is i (rules.hpp:24-33). */
+glop_status glop_rules_upload(glop_ctx* ctx, const uint8_t* bytes, const uint64_t* off,
+                              uint32_t n_patterns, uint64_t prefix_len, glop_rules** out);
+glop_status glop_rules_destroy(glop_rules* rules);
+
+/* verify_hits: keeps hits whose pattern suffix matches (patterns no longer
+ * than prefix_len are auto-verified; a pattern running past the end of text
+ * is rejected); alerts sorted by (offset, rule_id).  GLOP_ELOGIC if a hit
+ * extends past the end of text or names an unknown pattern (verify.hpp:76-77,
+ * rules.patterns.at()).  Host-facing; alerts are a library-owned host array.
+ * `counts` (optional, host, n_patterns entries) receives the per-pattern
+ * alert histogram. */
+glop_status glop_verify_hits(glop_ctx* ctx, const glop_rules* rules, const uint8_t* text,
+                             uint64_t n, int text_on_device, const glop_hit* hits, uint64_t n_hits,
+                             int hits_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                             uint64_t* counts);
+
+/* Device-resident verify: hits/text/out/counts are device pointers; d_text
+ * holds global offsets [base, base+n) (base = 0 for a whole text; a shard's
+ * first owned offset otherwise -- hits carry global offsets).  counts
+ * (n_patterns u64, may be NULL) is ACCUMULATED into.  out must hold n_hits. */
+glop_status glop_verify_hits_device(glop_ctx* ctx, const glop_rules* rules, const uint8_t* d_text,
+                                    uint64_t n, uint64_t base, const glop_hit* d_hits,
+                                    uint64_t n_hits, glop_alert* d_out, uint64_t* n_alerts,
+                                    uint64_t* d_counts);
+
+/* ---- KMP ------------------------------------------------------------------
+ * Replaces kmp_search (kmp.hpp:41-69): all start offsets (ascending,
+ * overlapping included) of pattern p; `failure` is the reference failure
+ * table (kmp.hpp:25-36), m entries.  `comparisons` (optional) is incremented
+ * by exactly the number of byte comparisons the sequential algorithm makes.
+ * Runs chunk-parallel with an (m-1)-byte warm-up overlap per chunk. */
+glop_status glop_kmp_search(glop_ctx* ctx, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                            const uint8_t* text, uint64_t n, int text_on_device, uint64_t** offsets,
+                            uint64_t* n_offsets, uint64_t* comparisons);
+glop_status glop_kmp_search_device(glop_ctx* ctx, const uint8_t* p, uint32_t m,
+                                   const uint32_t* failure, const uint8_t* d_text, uint64_t n,
+                                   uint64_t own, uint64_t base, uint64_t* d_out, uint64_t cap,
+                                   uint64_t* n_offsets, uint64_t* comparisons);
+
+/* ---- memory helpers -------------------------------------------------------- */
+void glop_free(void* p);
+glop_status glop_device_alloc(glop_ctx* ctx, uint64_t bytes, void** out);
+glop_status glop_device_free(glop_ctx* ctx, void* p);
+glop_status glop_host_alloc(uint64_t bytes, void** out); /* pinned */
+glop_status glop_host_free(void* p);
+glop_status glop_memcpy(glop_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
+/* kind: 1 = host->device, 2 = device->host, 3 = device->device (stream-ordered) */
+
+/* ---- host-side automaton construction (drop-in C++ code, exported for
+ * FFI callers such as the Python test/bench harness) ------------------------
+ * truncate_prefixes (rules.hpp:190-208) + build_failureless_trie
+ * (automaton.hpp:283-291) exactly as include/logtrawl/ implements them; the
+ * result is the reference's dense form, ready for glop_trie_upload.  Arrays
+ * are library-owned (glop_free).  GLOP_EINVAL for prefix_len < 1,
+ * GLOP_ECAPACITY when the trie would exceed max_states. */
+glop_status glop_build_failureless_trie(const uint8_t* bytes, const uint64_t* off, uint32_t n_patterns,
+                                        uint64_t prefix_len, uint64_t max_states, int32_t** dense_table,
+                                        uint32_t* state_count, uint32_t** out_offsets,
+                                        glop_output** out_flat);
+
+/* ---- synthetic workloads (bench / tests; not the matching path) ------------ */
+/* Bytes [begin, begin+n) of synthetic RFC 5424 corpus `seed`
+ * (paper_1704_02278_b200/csrc/corpus.h); device and host forms are
+ * byte-identical. */
+glop_status glop_gen_syslog_device(glop_ctx* ctx, uint8_t* d_out, uint64_t begin, uint64_t n,
+                                   uint64_t seed);
+glop_status glop_gen_syslog_host(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed,
+                                 unsigned threads);
+/* Reference corpus semantics (loggen.hpp:44-57), host only. */
+glop_status glop_gen_reference_log(uint8_t* out, uint64_t size, uint32_t seed, uint64_t line_len);
+/* Synthetic rule set: k patterns of `len` bytes, half with the reference's
+ * random_rules semantics (loggen.hpp:60-78), half sampled from the corpus's
+ * incident vocabulary.  bytes must hold k*len; names are "rand-i"/"vocab-i"
+ * (is_vocab[i] = 1 for vocabulary patterns; may be NULL). */
+glop_status glop_gen_rules(uint32_t k, uint32_t seed, uint32_t len, uint8_t* bytes,
+                           uint8_t* is_vocab);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLOP_H_ */

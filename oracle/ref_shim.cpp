@@ -6,6 +6,7 @@
 // pin the C restatement (oracle/pfac_oracle.c) and as the CPU baseline
 // ("kind": "reference") in bench.py: the timed call is the reference's own
 // measure() harness (bench.hpp:64-113) over pfac_scan + verify_hits.
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -99,6 +100,50 @@ int ref_measure(const uint8_t* text, uint64_t n, const uint8_t* bytes, const uin
   } catch (...) {
     return 4;
   }
+}
+
+// measure()'s timed body (bench.hpp:103-109: pfac_scan + verify_hits with a
+// prebuilt trie) with an explicit warm-up count; per-run wall seconds.
+int ref_time_pfac(const uint8_t* text, uint64_t n, const uint8_t* bytes, const uint64_t* off, uint32_t k,
+                  uint64_t L, int compact, unsigned workers, uint32_t warmup, uint32_t runs,
+                  double* run_seconds, uint64_t* n_alerts) {
+  try {
+    RuleSet r = rules_of(bytes, off, k);
+    std::string_view tv((const char*)text, n);
+    PrefixSet ps = truncate_prefixes(r, L);
+    Automaton trie = build_failureless_trie(ps, compact ? Backend::compact : Backend::dense);
+    ScanConfig sc;
+    sc.workers = workers ? workers : default_workers();
+    size_t na = 0;
+    for (uint32_t i = 0; i < warmup + runs; ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      std::vector<Hit> hits = pfac_scan(tv, trie, sc);
+      na = verify_hits(tv, hits, ps, r).size();
+      auto t1 = std::chrono::steady_clock::now();
+      if (i >= warmup) run_seconds[i - warmup] = std::chrono::duration<double>(t1 - t0).count();
+    }
+    *n_alerts = na;
+    return 0;
+  } catch (...) {
+    return 4;
+  }
+}
+
+// kmp_multi timed the same way (bench.hpp:83-91), single-threaded by design.
+int ref_time_kmp(const uint8_t* text, uint64_t n, const uint8_t* p, uint32_t m, uint32_t warmup, uint32_t runs,
+                 double* run_seconds, uint64_t* n_matches) {
+  RuleSet r;
+  r.patterns.push_back({0, "p", std::string((const char*)p, m)});
+  r.max_len = m;
+  std::vector<FailureTable> tables{build_failure_table(r.patterns[0])};
+  std::string_view tv((const char*)text, n);
+  for (uint32_t i = 0; i < warmup + runs; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    *n_matches = kmp_multi(tv, r, &tables).size();
+    auto t1 = std::chrono::steady_clock::now();
+    if (i >= warmup) run_seconds[i - warmup] = std::chrono::duration<double>(t1 - t0).count();
+  }
+  return 0;
 }
 
 int ref_kmp_search(const uint8_t* text, uint64_t n, const uint8_t* p, uint32_t m,

@@ -131,12 +131,13 @@ struct Rng {
   }
 };
 
-// Bounded byte writer: bytes past `lim` are dropped.
+// Windowed byte writer: only bytes whose block position lies in [lo, hi)
+// are stored (at out[pos - lo]); everything else is generated and dropped.
 struct Writer {
   uint8_t* out;
-  uint32_t pos, lim;
+  uint32_t pos, lo, hi;
   GLOP_HD void put(uint8_t c) {
-    if (pos < lim) out[pos] = c;
+    if (pos >= lo && pos < hi) out[pos - lo] = c;
     ++pos;
   }
   GLOP_HD void dec(uint32_t v) {
@@ -299,17 +300,23 @@ GLOP_HD void emit_line(Writer& w, Rng& r, uint64_t block, uint32_t line, const C
   w.put('\n');
 }
 
-// Fills `len` (<= kBlock) bytes of block `block` into out.  Bytes are the
-// first `len` bytes of the full kBlock-byte block, except that a block cut
-// short by the end of the corpus keeps whatever line fragment is there.
-GLOP_HD void gen_block(uint8_t* out, uint64_t seed, uint64_t block, uint32_t len) {
+// Corpus byte x (for corpus `seed`) is byte x % kBlock of block x / kBlock;
+// every block ends with LF.  gen_block_range writes bytes [lo, hi) of block
+// `block` to out[0, hi - lo).  Lines are produced in order, so stopping at hi
+// never changes earlier bytes.
+GLOP_HD void gen_block_range(uint8_t* out, uint64_t seed, uint64_t block, uint32_t lo,
+                             uint32_t hi) {
   Rng r;
   r.s = mix64(seed * 0x2545f4914f6cdd1dull ^ mix64(block + 0x51ed27ull));
-  Writer w{out, 0, len};
+  Writer w{out, 0, lo, hi};
   const Counts c = counts();
   uint32_t line = 0;
-  while (w.pos < kBlock) emit_line(w, r, block, line++, c);
-  if (len == kBlock) out[kBlock - 1] = '\n';
+  while (w.pos < hi) emit_line(w, r, block, line++, c);
+  if (hi == kBlock) out[kBlock - 1 - lo] = '\n';
+}
+
+GLOP_HD void gen_block(uint8_t* out, uint64_t seed, uint64_t block) {
+  gen_block_range(out, seed, block, 0, kBlock);
 }
 
 }  // namespace glop_corpus

@@ -1,0 +1,1059 @@
+// glop.cu -- host side of libglop.so: the C ABI declared in include/glop.h.
+//
+// Owns device memory, streams and kernel launches; flattens the reference's
+// dense failureless trie (automaton.hpp:51-141) into the device layout once
+// per automaton; orchestrates scan -> per-tile order -> gather, verification
+// and KMP.  No CPU fallback: every matching computation runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "glop.h"
+#include "glop_kernels.cuh"
+#include "logtrawl/automaton.hpp"
+#include "logtrawl/detail/abi.hpp"
+#include "workload.hpp"
+
+using namespace glop;
+
+static_assert(sizeof(glop_hit) == 16, "glop_hit must match logtrawl::Hit");
+static_assert(sizeof(DevHit) == sizeof(glop_hit), "device hit layout");
+static_assert(sizeof(DevAlert) == sizeof(glop_alert), "device alert layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+glop_status fail(glop_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CU(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? GLOP_ENOMEM : GLOP_ECUDA,            \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+#define TRY(expr)                          \
+  do {                                     \
+    glop_status s_ = (expr);               \
+    if (s_ != GLOP_OK) return s_;          \
+  } while (0)
+
+// Growable device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  glop_status ensure(size_t want) {
+    if (want <= bytes) return GLOP_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want, 256);
+    CU(cudaMalloc(&p, b));
+    bytes = b;
+    return GLOP_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct glop_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  DBuf text, staging, out, dir, prefix, misc, keys, keys_alt, cub_tmp;
+  DBuf keep, bcounts, bprefix, alerts, kmp_dfa, kmp_cls;
+  unsigned long long* h_misc = nullptr;  // pinned readback
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
+  bool timed = false;
+  uint64_t launches = 0;
+  std::mutex mu;
+};
+
+struct glop_trie {
+  int device = 0;
+  void* mem = nullptr;
+  DevTrie view{};
+  glop_trie_info info{};
+  bool empty = true;      // no outputs: every scan is empty
+  bool u16 = true;
+  bool smem_filter = false, smem_direct = false;
+  uint32_t max_pid = 0;
+};
+
+struct glop_rules {
+  int device = 0;
+  void* mem = nullptr;
+  DevRules view{};
+  std::vector<uint64_t> lens;
+};
+
+namespace {
+
+constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per CTA on sm_100
+
+struct Dev {
+  explicit Dev(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); dev = d; }
+  ~Dev() { if (prev != dev) cudaSetDevice(prev); }
+  int prev = 0, dev = 0;
+};
+
+size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
+
+glop_status sync_read(glop_ctx* c, const void* d_src, size_t bytes) {
+  CU(cudaMemcpyAsync(c->h_misc, d_src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return GLOP_OK;
+}
+
+// -------------------------------------------------------------- kernel launch
+template <bool F, bool S, typename E>
+glop_status launch_pfac_t(glop_ctx* c, int grid, size_t smem, const DevTrie& tr,
+                          const ScanParams& p) {
+  auto k = pfac_tile_kernel<F, S, E>;
+  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaEventRecord(c->ev0, c->stream));
+  k<<<grid, kThreads, smem, c->stream>>>(tr, p);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(c->ev1, c->stream));
+  c->timed = true;
+  ++c->launches;
+  return GLOP_OK;
+}
+
+glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p) {
+  const bool smem_table = filter ? t->smem_filter : t->smem_direct;
+  const size_t smem = PfacSmem::total(filter, smem_table ? t->view.table_bytes : 0);
+  const int grid = (int)std::min<uint32_t>(p.num_tiles, (uint32_t)c->num_sms);
+  const DevTrie& tr = t->view;
+  if (t->u16) {
+    if (filter) return smem_table ? launch_pfac_t<true, true, uint16_t>(c, grid, smem, tr, p)
+                                  : launch_pfac_t<true, false, uint16_t>(c, grid, smem, tr, p);
+    return smem_table ? launch_pfac_t<false, true, uint16_t>(c, grid, smem, tr, p)
+                      : launch_pfac_t<false, false, uint16_t>(c, grid, smem, tr, p);
+  }
+  if (filter) return smem_table ? launch_pfac_t<true, true, uint32_t>(c, grid, smem, tr, p)
+                                : launch_pfac_t<true, false, uint32_t>(c, grid, smem, tr, p);
+  return smem_table ? launch_pfac_t<false, true, uint32_t>(c, grid, smem, tr, p)
+                    : launch_pfac_t<false, false, uint32_t>(c, grid, smem, tr, p);
+}
+
+glop_status radix_sort_keys(glop_ctx* c, unsigned long long* in, unsigned long long* out,
+                            unsigned long long n) {
+  size_t tmp = 0;
+  CU(cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, n, 0, 64, c->stream));
+  TRY(c->cub_tmp.ensure(tmp));
+  CU(cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, tmp, in, out, n, 0, 64, c->stream));
+  return GLOP_OK;
+}
+
+// PFAC over d_text[0, n): starts [0, own), offsets + base, sorted hits to out.
+glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_text,
+                                  uint64_t n, uint64_t own, uint64_t base, glop_pfac_kernel kind,
+                                  glop_hit* d_out, uint64_t cap, uint64_t* n_hits) {
+  *n_hits = 0;
+  if (own > n) return fail(GLOP_EINVAL, "pfac_scan: own > n");
+  if (own == 0 || t->empty) return GLOP_OK;
+  const bool filter = kind != GLOP_PFAC_DIRECT;
+  const uint32_t num_tiles = (uint32_t)((own + kTile - 1) / kTile);
+  TRY(c->dir.ensure(sizeof(TileDir) * num_tiles));
+  TRY(c->prefix.ensure(sizeof(unsigned long long) * num_tiles));
+  TRY(c->misc.ensure(64));
+  size_t want = std::max<size_t>(1 << 20, own / 512);
+  if (c->staging.bytes < want * sizeof(glop_hit)) TRY(c->staging.ensure(want * sizeof(glop_hit)));
+  auto* g_count = c->misc.as<unsigned long long>();
+  auto* g_flags = reinterpret_cast<unsigned int*>(g_count + 1);
+
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
+    ScanParams p{};
+    p.text = d_text;
+    p.n = n;
+    p.own = own;
+    p.base = base;
+    p.num_tiles = num_tiles;
+    p.mode = 0;
+    p.staging = reinterpret_cast<DevHit*>(c->staging.p);
+    p.staging_cap = c->staging.bytes / sizeof(glop_hit);
+    p.g_count = g_count;
+    p.dir = c->dir.as<TileDir>();
+    p.g_flags = g_flags;
+    TRY(launch_pfac(c, t, filter, p));
+    TRY(sync_read(c, c->misc.p, 16));
+    const unsigned long long total = c->h_misc[0];
+    const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
+    *n_hits = total;
+    if (flags & 1u) {
+      // some tile produced more hits than its shared-memory buffer holds:
+      // exact fallback -- global keys, device radix sort
+      if (t->max_pid >= (1u << 24) || base + n >= (1ull << 40))
+        return fail(GLOP_ECAPACITY, "pfac_scan: hit density fallback limited to 2^24 ids / 2^40 bytes");
+      if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
+      TRY(c->keys.ensure(total * 8));
+      TRY(c->keys_alt.ensure(total * 8));
+      CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
+      p.mode = 1;
+      p.keys = c->keys.as<unsigned long long>();
+      p.keys_cap = total;
+      TRY(launch_pfac(c, t, filter, p));
+      TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), total));
+      c->launches += 2;  // + the mode-1 scan
+      keys_to_hits_kernel<<<std::max<unsigned long long>(1, std::min<unsigned long long>((total + 255) / 256, 4096)), 256, 0,
+                            c->stream>>>(c->keys_alt.as<unsigned long long>(), total, t->view.pid_len,
+                                         reinterpret_cast<DevHit*>(d_out));
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(c->stream));
+      return GLOP_OK;
+    }
+    if (total > p.staging_cap) {  // grow and rerun
+      c->staging.release();
+      TRY(c->staging.ensure(total * sizeof(glop_hit) + (1 << 20)));
+      continue;
+    }
+    if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
+    if (total == 0) return GLOP_OK;
+    ++c->launches;
+    tile_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->dir.as<TileDir>(), num_tiles,
+                                                  c->prefix.as<unsigned long long>());
+    ++c->launches;
+    gather_kernel<DevHit><<<std::min<uint32_t>((num_tiles + 7) / 8, 4 * c->num_sms), 256, 0, c->stream>>>(
+        c->dir.as<TileDir>(), c->prefix.as<unsigned long long>(), num_tiles,
+        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out));
+    CU(cudaGetLastError());
+    return GLOP_OK;
+  }
+  return fail(GLOP_ECUDA, "pfac_scan: staging did not converge");
+}
+
+// KMP DFA (see glop_kernels.cuh): replays kmp.hpp:52-66 for each (state, class).
+void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::vector<uint8_t>& cls,
+                   uint32_t& C, std::vector<uint32_t>& dfa) {
+  cls.assign(256, 0);
+  bool used[256] = {};
+  for (uint32_t i = 0; i < m; ++i) used[p[i]] = true;
+  C = 1;
+  int rep[257];
+  int other = -1;
+  for (int b = 0; b < 256; ++b) {
+    if (used[b]) {
+      rep[C] = b;
+      cls[b] = (uint8_t)C++;
+    } else if (other < 0) {
+      other = b;
+    }
+  }
+  rep[0] = other;  // -1 if all bytes occur (class 0 then unused)
+  dfa.assign((size_t)m * C, 0);
+  for (uint32_t j0 = 0; j0 < m; ++j0)
+    for (uint32_t c = 0; c < C; ++c) {
+      if (rep[c] < 0) continue;
+      const uint8_t b = (uint8_t)rep[c];
+      uint32_t j = j0, cmp = 0, match = 0;
+      for (;;) {
+        ++cmp;
+        if (b == p[j]) {
+          ++j;
+          if (j == m) {
+            match = 1;
+            j = fail_tab[m - 1];
+          }
+          break;
+        } else if (j > 0) {
+          j = fail_tab[j - 1];
+        } else {
+          break;
+        }
+      }
+      dfa[(size_t)j0 * C + c] = j | (match << 13) | (cmp << 14);
+    }
+}
+
+glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab,
+                            const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                            uint64_t* d_out, uint64_t cap, uint64_t* n_offsets,
+                            uint64_t* comparisons) {
+  *n_offsets = 0;
+  if (own > n) return fail(GLOP_EINVAL, "kmp_search: own > n");
+  if (m == 0 || n < m || own == 0) return GLOP_OK;  // kmp.hpp:50
+  if (m >= 8192) return fail(GLOP_EINVAL, "kmp_search: pattern longer than 8191 bytes");
+  for (uint32_t i = 0; i < m; ++i)
+    if (fail_tab[i] > i) return fail(GLOP_EINVAL, "kmp_search: bad failure table");
+  std::vector<uint8_t> cls;
+  std::vector<uint32_t> dfa;
+  uint32_t C = 0;
+  build_kmp_dfa(pat, m, fail_tab, cls, C, dfa);
+  const uint32_t words = (uint32_t)((dfa.size() + 3) & ~size_t(3));
+  dfa.resize(words, 0);
+  TRY(c->kmp_dfa.ensure(words * 4));
+  TRY(c->kmp_cls.ensure(256));
+  CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), words * 4, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->kmp_cls.p, cls.data(), 256, cudaMemcpyHostToDevice, c->stream));
+  const uint32_t num_tiles = (uint32_t)((own + kKmpTile - 1) / kKmpTile);
+  TRY(c->dir.ensure(sizeof(TileDir) * num_tiles));
+  TRY(c->prefix.ensure(sizeof(unsigned long long) * num_tiles));
+  TRY(c->misc.ensure(64));
+  size_t want = std::max<size_t>(1 << 20, own / 1024);
+  if (c->staging.bytes < want * 8) TRY(c->staging.ensure(want * 8));
+  auto* g_count = c->misc.as<unsigned long long>();
+  const bool smem_dfa = KmpSmem::kDfa + (size_t)words * 4 <= kSmemMax;
+  const size_t smem = KmpSmem::kDfa + (smem_dfa ? (size_t)words * 4 : 0);
+  const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+    KmpParams p{};
+    p.text = d_text;
+    p.n = n;
+    p.own = own;
+    p.base = base;
+    p.m = m;
+    p.C = C;
+    p.num_tiles = num_tiles;
+    p.dfa = c->kmp_dfa.as<uint32_t>();
+    p.cls = c->kmp_cls.as<uint8_t>();
+    p.dfa_words = words;
+    p.p0 = pat[0];
+    p.staging = c->staging.as<unsigned long long>();
+    p.staging_cap = c->staging.bytes / 8;
+    p.g_count = g_count;
+    p.dir = c->dir.as<TileDir>();
+    p.g_flags = reinterpret_cast<unsigned int*>(g_count + 1);
+    p.comparisons = g_count + 2;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    if (smem_dfa) {
+      CU(cudaFuncSetAttribute(kmp_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kmp_tile_kernel<true><<<grid, kThreads, smem, c->stream>>>(p);
+    } else {
+      CU(cudaFuncSetAttribute(kmp_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kmp_tile_kernel<false><<<grid, kThreads, smem, c->stream>>>(p);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev1, c->stream));
+    c->timed = true;
+    ++c->launches;
+    TRY(sync_read(c, c->misc.p, 24));
+    const unsigned long long total = c->h_misc[0];
+    const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
+    *n_offsets = total;
+    if (comparisons) *comparisons += c->h_misc[2];
+    if (flags & 1u) {
+      // > kKmpHitCap matches in one tile: exact fallback -- every match as a
+      // global key, then a device radix sort.
+      if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
+      TRY(c->keys.ensure(total * 8));
+      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+      p.mode = 1;
+      p.keys = c->keys.as<unsigned long long>();
+      p.keys_cap = total;
+      p.comparisons = g_count + 3;  // already counted by the first pass
+      if (smem_dfa) kmp_tile_kernel<true><<<grid, kThreads, smem, c->stream>>>(p);
+      else kmp_tile_kernel<false><<<grid, kThreads, smem, c->stream>>>(p);
+      CU(cudaGetLastError());
+      TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), total));
+      CU(cudaStreamSynchronize(c->stream));
+      return GLOP_OK;
+    }
+    if (total > p.staging_cap) {
+      c->staging.release();
+      TRY(c->staging.ensure(total * 8 + (1 << 20)));
+      if (comparisons) *comparisons -= c->h_misc[2];
+      continue;
+    }
+    if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
+    if (total == 0) return GLOP_OK;
+    ++c->launches;
+    tile_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->dir.as<TileDir>(), num_tiles,
+                                                  c->prefix.as<unsigned long long>());
+    ++c->launches;
+    gather_kernel<unsigned long long>
+        <<<std::min<uint32_t>((num_tiles + 7) / 8, 4 * c->num_sms), 256, 0, c->stream>>>(
+            c->dir.as<TileDir>(), c->prefix.as<unsigned long long>(), num_tiles,
+            c->staging.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out));
+    CU(cudaGetLastError());
+    return GLOP_OK;
+  }
+  return fail(GLOP_ECUDA, "kmp_search: staging did not converge");
+}
+
+glop_status to_device_text(glop_ctx* c, const uint8_t* text, uint64_t n, int on_device,
+                           const uint8_t** d_text) {
+  if (on_device || n == 0) {
+    *d_text = text;
+    return GLOP_OK;
+  }
+  TRY(c->text.ensure(n + 64));
+  CU(cudaMemcpyAsync(c->text.p, text, n, cudaMemcpyHostToDevice, c->stream));
+  *d_text = c->text.as<uint8_t>();
+  return GLOP_OK;
+}
+
+glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* d_text, uint64_t n,
+                               uint64_t base, const glop_hit* d_hits, uint64_t n_hits, glop_alert* d_out,
+                               uint64_t* n_alerts, uint64_t* d_counts) {
+  *n_alerts = 0;
+  if (n_hits == 0) return GLOP_OK;
+  const uint32_t nb = (uint32_t)((n_hits + kVerifyBlock - 1) / kVerifyBlock);
+  TRY(c->keep.ensure(n_hits));
+  TRY(c->bcounts.ensure(nb * 4));
+  TRY(c->bprefix.ensure(nb * 8 + 8));
+  TRY(c->misc.ensure(64));
+  CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
+  auto* flags = reinterpret_cast<unsigned int*>(c->misc.as<unsigned long long>() + 1);
+  auto* total = c->misc.as<unsigned long long>();
+  c->launches += 2;
+  verify_flags_kernel<<<nb, kVerifyBlock, 0, c->stream>>>(
+      r->view, d_text, base, n, reinterpret_cast<const DevHit*>(d_hits), n_hits, c->keep.as<uint8_t>(),
+      c->bcounts.as<uint32_t>(), flags);
+  block_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<uint32_t>(), nb,
+                                                 c->bprefix.as<unsigned long long>(), total);
+  CU(cudaGetLastError());
+  TRY(sync_read(c, c->misc.p, 16));
+  const unsigned long long kept = c->h_misc[0];
+  const unsigned fl = (unsigned)(c->h_misc[1] & 0xffffffffu);
+  if (fl & 1u) return fail(GLOP_ELOGIC, "verify_hits: hit extends past end of text");
+  ++c->launches;
+  verify_scatter_kernel<<<nb, kVerifyBlock, 0, c->stream>>>(
+      r->view, reinterpret_cast<const DevHit*>(d_hits), n_hits, c->keep.as<uint8_t>(),
+      c->bprefix.as<unsigned long long>(), reinterpret_cast<DevAlert*>(d_out),
+      reinterpret_cast<unsigned long long*>(d_counts));
+  CU(cudaGetLastError());
+  *n_alerts = kept;
+  if ((fl & 2u) && kept > 1) {
+    // hits were not in (offset, id) order: order the alerts on the device
+    // (verify.hpp:100-103)
+    if (r->view.n_patterns > (1u << 24) || base + n >= (1ull << 40))
+      return fail(GLOP_EINVAL, "verify_hits: unsorted hits need ids < 2^24 and offsets < 2^40");
+    TRY(c->keys.ensure(kept * 8));
+    TRY(c->keys_alt.ensure(kept * 8));
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((kept + 255) / 256, 4096);
+    c->launches += 2;
+    alerts_to_keys_kernel<<<grid, 256, 0, c->stream>>>(reinterpret_cast<DevAlert*>(d_out), kept,
+                                                       c->keys.as<unsigned long long>());
+    TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), kept));
+    keys_to_alerts_kernel<<<grid, 256, 0, c->stream>>>(c->keys_alt.as<unsigned long long>(), kept, r->view,
+                                                       reinterpret_cast<DevAlert*>(d_out));
+    CU(cudaGetLastError());
+  }
+  return GLOP_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+const char* glop_last_error(void) { return g_err.c_str(); }
+const char* glop_version(void) { return "glop-b200 0.1 (sm_100a)"; }
+
+glop_status glop_ctx_create(int device, glop_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  CU(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(GLOP_EINVAL, "glop_ctx_create: bad device");
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(GLOP_ECUDA, std::string("glop: needs an sm_100 device, found ") + prop.name);
+  Dev g(device);
+  auto* c = new glop_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_misc, 64);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *out = c;
+  return GLOP_OK;
+}
+
+glop_status glop_ctx_destroy(glop_ctx* c) {
+  if (!c) return GLOP_OK;
+  Dev g(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
+                  &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
+                  &c->kmp_dfa, &c->kmp_cls})
+    b->release();
+  cudaFreeHost(c->h_misc);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return GLOP_OK;
+}
+
+void* glop_ctx_stream(glop_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+glop_status glop_ctx_synchronize(glop_ctx* c) {
+  Dev g(c->device);
+  CU(cudaStreamSynchronize(c->stream));
+  return GLOP_OK;
+}
+
+glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, const uint32_t* out_off,
+                             const glop_output* out_flat, glop_trie** out) {
+  *out = nullptr;
+  if (!c || !dense || !out_off || Q == 0) return fail(GLOP_EINVAL, "glop_trie_upload: null/empty input");
+  if (Q >= 0x7FFFFFFFu) return fail(GLOP_EINVAL, "glop_trie_upload: too many states");
+  // --- structure: BFS from the root, every non-root state exactly one parent
+  std::vector<uint32_t> depth(Q, 0);
+  std::vector<uint8_t> seen(Q, 0);
+  std::vector<uint32_t> order;
+  order.reserve(Q);
+  order.push_back(0);
+  seen[0] = 1;
+  bool used[256] = {};
+  for (size_t h = 0; h < order.size(); ++h) {
+    const uint32_t s = order[h];
+    for (int b = 0; b < 256; ++b) {
+      const int32_t t = dense[(size_t)s * 256 + b];
+      if (t == -1) continue;
+      if (t <= 0 || (uint32_t)t >= Q || seen[t])
+        return fail(GLOP_EINVAL, "glop_trie_upload: not a failureless trie");
+      seen[t] = 1;
+      depth[t] = depth[s] + 1;
+      used[b] = true;
+      order.push_back((uint32_t)t);
+    }
+  }
+  if (order.size() != Q) return fail(GLOP_EINVAL, "glop_trie_upload: unreachable state");
+  const uint32_t n_out = out_off[Q];
+  if (n_out && !out_flat) return fail(GLOP_EINVAL, "glop_trie_upload: null outputs");
+  uint32_t lmin = 0, lmax = 0, max_pid = 0;
+  std::vector<uint8_t> has_out(Q, 0);
+  for (uint32_t s = 0; s < Q; ++s) {
+    if (out_off[s + 1] < out_off[s]) return fail(GLOP_EINVAL, "glop_trie_upload: bad out_offsets");
+    if (s == 0) continue;  // the walk never emits at the root (scan.hpp:126)
+    if (out_off[s + 1] > out_off[s]) {
+      has_out[s] = 1;
+      lmin = lmin ? std::min(lmin, depth[s]) : depth[s];
+      lmax = std::max(lmax, depth[s]);
+    }
+  }
+  // compact out lists: drop root outputs, keep the CSR for states 1..Q-1
+  std::vector<uint32_t> off2(Q + 1, 0), pid2;
+  for (uint32_t s = 0; s < Q; ++s) {
+    off2[s] = (uint32_t)pid2.size();
+    if (s == 0) continue;
+    for (uint32_t o = out_off[s]; o < out_off[s + 1]; ++o) {
+      pid2.push_back(out_flat[o].pattern_id);
+      max_pid = std::max(max_pid, out_flat[o].pattern_id);
+    }
+  }
+  off2[Q] = (uint32_t)pid2.size();
+  std::vector<uint32_t> pid_len(pid2.empty() ? 1 : (size_t)max_pid + 1, 0xFFFFFFFFu);
+  for (uint32_t s = 1; s < Q; ++s)
+    for (uint32_t o = out_off[s]; o < out_off[s + 1]; ++o) {
+      uint32_t& L = pid_len[out_flat[o].pattern_id];
+      if (L != 0xFFFFFFFFu && L != out_flat[o].matched_len)
+        return fail(GLOP_EINVAL, "glop_trie_upload: pattern id with two lengths");
+      L = out_flat[o].matched_len;
+    }
+  // --- alphabet classes (ascending byte order; class 0 = no edge anywhere)
+  uint8_t cls[256];
+  uint32_t C = 1;
+  for (int b = 0; b < 256; ++b) cls[b] = used[b] ? (uint8_t)C++ : 0;
+  const bool u16 = Q < 0x8000u;
+  const size_t eb = u16 ? 2 : 4;
+  const size_t table_bytes = up16((size_t)Q * C * eb);
+  std::vector<uint8_t> table(table_bytes, 0);
+  for (uint32_t s = 0; s < Q; ++s)
+    for (int b = 0; b < 256; ++b) {
+      const int32_t t = dense[(size_t)s * 256 + b];
+      if (t < 0) continue;
+      const size_t idx = (size_t)s * C + cls[b];
+      if (u16) {
+        uint16_t e = (uint16_t)(t | (has_out[t] ? 0x8000u : 0));
+        memcpy(&table[idx * 2], &e, 2);
+      } else {
+        uint32_t e = (uint32_t)t | (has_out[t] ? 0x80000000u : 0);
+        memcpy(&table[idx * 4], &e, 4);
+      }
+    }
+  // --- filter tables: every root path of length lmin
+  const uint32_t q = lmin ? std::min<uint32_t>(4, lmin) : 1;
+  const uint32_t stride = lmin ? std::min<uint32_t>(lmin - q + 1, 8) : 1;
+  std::vector<uint8_t> dmask(kDmaskBytes, 0);
+  std::vector<uint32_t> bm2(kBm2Bits / 32, 0);
+  if (lmin) {
+    struct Item {
+      uint32_t s, d;
+    };
+    std::vector<Item> stack{{0, 0}};
+    std::vector<uint8_t> path(lmin);
+    // iterative DFS carrying the path bytes
+    std::vector<int> next_b(lmin + 1, 0);
+    std::vector<uint32_t> st(lmin + 1, 0);
+    int d = 0;
+    st[0] = 0;
+    next_b[0] = 0;
+    while (d >= 0) {
+      if ((uint32_t)d == lmin) {
+        for (uint32_t k = 0; k < stride; ++k) {
+          uint32_t g = 0;
+          for (uint32_t x = 0; x < q; ++x) g |= (uint32_t)path[k + x] << (8 * x);
+          dmask[qgram_bucket(g, q)] |= (uint8_t)(1u << k);
+        }
+        unsigned long long key = 0;
+        for (uint32_t x = 0; x < std::min<uint32_t>(lmin, 8); ++x)
+          key |= (unsigned long long)path[x] << (8 * x);
+        const uint32_t bit = prefix_bit(key);
+        bm2[bit >> 5] |= 1u << (bit & 31);
+        --d;
+        continue;
+      }
+      bool pushed = false;
+      while (next_b[d] < 256) {
+        const int b = next_b[d]++;
+        const int32_t t = dense[(size_t)st[d] * 256 + b];
+        if (t < 0) continue;
+        path[d] = (uint8_t)b;
+        st[d + 1] = (uint32_t)t;
+        next_b[d + 1] = 0;
+        ++d;
+        pushed = true;
+        break;
+      }
+      if (!pushed) --d;
+    }
+  }
+  // --- one device allocation
+  const size_t o_cls = 0, o_table = 256, o_off = o_table + table_bytes;
+  const size_t o_pid = o_off + up16((size_t)(Q + 1) * 4);
+  const size_t o_plen = o_pid + up16(std::max<size_t>(pid2.size(), 1) * 4);
+  const size_t o_dmask = o_plen + up16(pid_len.size() * 4);
+  const size_t o_bm2 = o_dmask + kDmaskBytes;
+  const size_t total = o_bm2 + kBm2Bytes;
+  std::vector<uint8_t> host(total, 0);
+  memcpy(&host[o_cls], cls, 256);
+  memcpy(&host[o_table], table.data(), table_bytes);
+  memcpy(&host[o_off], off2.data(), (Q + 1) * 4);
+  if (!pid2.empty()) memcpy(&host[o_pid], pid2.data(), pid2.size() * 4);
+  memcpy(&host[o_plen], pid_len.data(), pid_len.size() * 4);
+  memcpy(&host[o_dmask], dmask.data(), kDmaskBytes);
+  memcpy(&host[o_bm2], bm2.data(), kBm2Bytes);
+  Dev g(c->device);
+  void* mem = nullptr;
+  CU(cudaMalloc(&mem, total));
+  cudaError_t e = cudaMemcpy(mem, host.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(mem);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  auto* t = new glop_trie();
+  t->device = c->device;
+  t->mem = mem;
+  uint8_t* m = static_cast<uint8_t*>(mem);
+  t->view.cls = m + o_cls;
+  t->view.table = m + o_table;
+  t->view.out_off = reinterpret_cast<const uint32_t*>(m + o_off);
+  t->view.out_pid = reinterpret_cast<const uint32_t*>(m + o_pid);
+  t->view.pid_len = reinterpret_cast<const uint32_t*>(m + o_plen);
+  t->view.dmask = m + o_dmask;
+  t->view.bm2 = reinterpret_cast<const uint32_t*>(m + o_bm2);
+  t->view.Q = Q;
+  t->view.C = C;
+  t->view.lmin = lmin;
+  t->view.lmax = lmax;
+  t->view.q = q;
+  t->view.stride = stride;
+  t->view.table_bytes = (uint32_t)std::min<size_t>(table_bytes, 0xFFFFFFFFu);
+  t->empty = pid2.empty();
+  t->u16 = u16;
+  t->max_pid = max_pid;
+  const size_t cap = std::min<size_t>(kSmemMax, c->smem_optin ? c->smem_optin : kSmemMax);
+  t->smem_filter = PfacSmem::total(true, table_bytes) <= cap;
+  t->smem_direct = PfacSmem::total(false, table_bytes) <= cap;
+  t->info = glop_trie_info{Q, C, lmin, lmax, q, stride, (uint32_t)eb, t->smem_filter ? 1u : 0u,
+                           (uint64_t)table_bytes};
+  *out = t;
+  return GLOP_OK;
+}
+
+glop_status glop_trie_destroy(glop_trie* t) {
+  if (!t) return GLOP_OK;
+  Dev g(t->device);
+  cudaFree(t->mem);
+  delete t;
+  return GLOP_OK;
+}
+
+glop_status glop_trie_get_info(const glop_trie* t, glop_trie_info* info) {
+  if (!t || !info) return fail(GLOP_EINVAL, "null");
+  *info = t->info;
+  return GLOP_OK;
+}
+
+glop_status glop_pfac_scan_device(glop_ctx* c, const glop_trie* t, const uint8_t* d_text, uint64_t n,
+                                  uint64_t own, uint64_t base, glop_pfac_kernel kernel, glop_hit* d_out,
+                                  uint64_t cap, uint64_t* n_hits) {
+  if (!c || !t || !n_hits) return fail(GLOP_EINVAL, "glop_pfac_scan_device: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  return pfac_scan_device_impl(c, t, d_text, n, own, base, kernel, d_out, cap, n_hits);
+}
+
+glop_status glop_pfac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n,
+                           int text_on_device, glop_hit** hits, uint64_t* n_hits) {
+  if (!c || !t || !hits || !n_hits) return fail(GLOP_EINVAL, "glop_pfac_scan: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  *hits = nullptr;
+  *n_hits = 0;
+  const uint8_t* d_text = nullptr;
+  TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
+  TRY(c->out.ensure(cap * sizeof(glop_hit)));
+  uint64_t total = 0;
+  glop_status s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
+  if (s == GLOP_ECAPACITY && total > cap) {
+    c->out.release();
+    cap = total;
+    TRY(c->out.ensure(cap * sizeof(glop_hit)));
+    s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
+  }
+  if (s != GLOP_OK) return s;
+  glop_hit* h = static_cast<glop_hit*>(malloc(std::max<uint64_t>(total, 1) * sizeof(glop_hit)));
+  if (!h) return fail(GLOP_ENOMEM, "glop_pfac_scan: host allocation");
+  if (total) {
+    cudaError_t e = cudaMemcpyAsync(h, c->out.p, total * sizeof(glop_hit), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      free(h);
+      return fail(GLOP_ECUDA, cudaGetErrorString(e));
+    }
+  } else {
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  *hits = h;
+  *n_hits = total;
+  return GLOP_OK;
+}
+
+glop_status glop_rules_upload(glop_ctx* c, const uint8_t* bytes, const uint64_t* off, uint32_t k,
+                              uint64_t prefix_len, glop_rules** out) {
+  *out = nullptr;
+  if (!c || !off) return fail(GLOP_EINVAL, "glop_rules_upload: null argument");
+  if (prefix_len < 1) return fail(GLOP_EINVAL, "truncate_prefixes: prefix_len must be >= 1");
+  const uint64_t nb = off[k];
+  for (uint32_t i = 0; i < k; ++i)
+    if (off[i + 1] < off[i]) return fail(GLOP_EINVAL, "glop_rules_upload: bad offsets");
+  Dev g(c->device);
+  const size_t o_off = up16(std::max<uint64_t>(nb, 1));
+  const size_t total = o_off + (size_t)(k + 1) * 8;
+  std::vector<uint8_t> host(total, 0);
+  if (nb) memcpy(host.data(), bytes, nb);
+  memcpy(&host[o_off], off, (size_t)(k + 1) * 8);
+  void* mem = nullptr;
+  CU(cudaMalloc(&mem, total));
+  cudaError_t e = cudaMemcpy(mem, host.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(mem);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  auto* r = new glop_rules();
+  r->device = c->device;
+  r->mem = mem;
+  r->view.bytes = static_cast<uint8_t*>(mem);
+  r->view.off = reinterpret_cast<const unsigned long long*>(static_cast<uint8_t*>(mem) + o_off);
+  r->view.n_patterns = k;
+  r->view.prefix_len = prefix_len;
+  *out = r;
+  return GLOP_OK;
+}
+
+glop_status glop_rules_destroy(glop_rules* r) {
+  if (!r) return GLOP_OK;
+  Dev g(r->device);
+  cudaFree(r->mem);
+  delete r;
+  return GLOP_OK;
+}
+
+glop_status glop_verify_hits_device(glop_ctx* c, const glop_rules* r, const uint8_t* d_text, uint64_t n,
+                                    uint64_t base, const glop_hit* d_hits, uint64_t n_hits, glop_alert* d_out,
+                                    uint64_t* n_alerts, uint64_t* d_counts) {
+  if (!c || !r || !n_alerts) return fail(GLOP_EINVAL, "glop_verify_hits_device: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  return verify_device_impl(c, r, d_text, n, base, d_hits, n_hits, d_out, n_alerts, d_counts);
+}
+
+glop_status glop_verify_hits(glop_ctx* c, const glop_rules* r, const uint8_t* text, uint64_t n,
+                             int text_on_device, const glop_hit* hits, uint64_t n_hits, int hits_on_device,
+                             glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts) {
+  if (!c || !r || !alerts || !n_alerts) return fail(GLOP_EINVAL, "glop_verify_hits: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  *alerts = nullptr;
+  *n_alerts = 0;
+  const uint8_t* d_text = nullptr;
+  TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  const glop_hit* d_hits = hits;
+  if (!hits_on_device && n_hits) {
+    TRY(c->out.ensure(n_hits * sizeof(glop_hit)));
+    CU(cudaMemcpyAsync(c->out.p, hits, n_hits * sizeof(glop_hit), cudaMemcpyHostToDevice, c->stream));
+    d_hits = c->out.as<glop_hit>();
+  }
+  TRY(c->alerts.ensure(std::max<uint64_t>(n_hits, 1) * sizeof(glop_alert) + (size_t)(r->view.n_patterns + 1) * 8));
+  glop_alert* d_alerts = c->alerts.as<glop_alert>();
+  uint64_t* d_counts = nullptr;
+  if (counts) {
+    d_counts = reinterpret_cast<uint64_t*>(d_alerts + std::max<uint64_t>(n_hits, 1));
+    CU(cudaMemsetAsync(d_counts, 0, (size_t)r->view.n_patterns * 8, c->stream));
+  }
+  uint64_t kept = 0;
+  TRY(verify_device_impl(c, r, d_text, n, 0, d_hits, n_hits, d_alerts, &kept, d_counts));
+  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(kept, 1) * sizeof(glop_alert)));
+  if (!a) return fail(GLOP_ENOMEM, "glop_verify_hits: host allocation");
+  cudaError_t e = cudaSuccess;
+  if (kept) e = cudaMemcpyAsync(a, d_alerts, kept * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && counts)
+    e = cudaMemcpyAsync(counts, d_counts, (size_t)r->view.n_patterns * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(a);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *alerts = a;
+  *n_alerts = kept;
+  return GLOP_OK;
+}
+
+glop_status glop_kmp_search_device(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                   const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                   uint64_t* d_out, uint64_t cap, uint64_t* n_offsets,
+                                   uint64_t* comparisons) {
+  if (!c || !n_offsets || (m && (!p || !failure))) return fail(GLOP_EINVAL, "glop_kmp_search_device: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  return kmp_device_impl(c, p, m, failure, d_text, n, own, base, d_out, cap, n_offsets, comparisons);
+}
+
+glop_status glop_kmp_search(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                            const uint8_t* text, uint64_t n, int text_on_device, uint64_t** offsets,
+                            uint64_t* n_offsets, uint64_t* comparisons) {
+  if (!c || !offsets || !n_offsets || (m && (!p || !failure)))
+    return fail(GLOP_EINVAL, "glop_kmp_search: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  *offsets = nullptr;
+  *n_offsets = 0;
+  const uint8_t* d_text = nullptr;
+  if (m && n >= m) TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / 8);
+  TRY(c->out.ensure(cap * 8));
+  uint64_t total = 0, cmp0 = comparisons ? *comparisons : 0;
+  glop_status s = kmp_device_impl(c, p, m, failure, d_text, n, n, 0, c->out.as<uint64_t>(), cap, &total, comparisons);
+  if (s == GLOP_ECAPACITY && total > cap) {
+    c->out.release();
+    cap = total;
+    TRY(c->out.ensure(cap * 8));
+    if (comparisons) *comparisons = cmp0;
+    s = kmp_device_impl(c, p, m, failure, d_text, n, n, 0, c->out.as<uint64_t>(), cap, &total, comparisons);
+  }
+  if (s != GLOP_OK) return s;
+  uint64_t* o = static_cast<uint64_t*>(malloc(std::max<uint64_t>(total, 1) * 8));
+  if (!o) return fail(GLOP_ENOMEM, "glop_kmp_search: host allocation");
+  cudaError_t e = cudaSuccess;
+  if (total) e = cudaMemcpyAsync(o, c->out.p, total * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(o);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *offsets = o;
+  *n_offsets = total;
+  return GLOP_OK;
+}
+
+glop_status glop_build_failureless_trie(const uint8_t* bytes, const uint64_t* off, uint32_t k,
+                                        uint64_t prefix_len, uint64_t max_states, int32_t** dense_table,
+                                        uint32_t* state_count, uint32_t** out_offsets,
+                                        glop_output** out_flat) {
+  try {
+    logtrawl::RuleSet rs;
+    for (uint32_t i = 0; i < k; ++i) {
+      logtrawl::Pattern p;
+      p.id = i;
+      p.bytes.assign(reinterpret_cast<const char*>(bytes) + off[i], off[i + 1] - off[i]);
+      rs.max_len = std::max(rs.max_len, p.bytes.size());
+      rs.patterns.push_back(std::move(p));
+    }
+    const logtrawl::Automaton a = logtrawl::build_failureless_trie(
+        logtrawl::truncate_prefixes(rs, prefix_len), logtrawl::Backend::dense, max_states);
+    const size_t q = a.state_count;
+    auto* d = static_cast<int32_t*>(malloc(q * 256 * 4));
+    auto* o = static_cast<uint32_t*>(malloc((q + 1) * 4));
+    auto* f = static_cast<glop_output*>(malloc(std::max<size_t>(a.out_flat.size(), 1) * sizeof(glop_output)));
+    if (!d || !o || !f) {
+      free(d), free(o), free(f);
+      return fail(GLOP_ENOMEM, "glop_build_failureless_trie: host allocation");
+    }
+    memcpy(d, a.dense_table.data(), q * 256 * 4);
+    memcpy(o, a.out_offsets.data(), (q + 1) * 4);
+    if (!a.out_flat.empty()) memcpy(f, a.out_flat.data(), a.out_flat.size() * sizeof(glop_output));
+    *dense_table = d;
+    *state_count = (uint32_t)q;
+    *out_offsets = o;
+    *out_flat = f;
+    return GLOP_OK;
+  } catch (const logtrawl::CapacityError& e) {
+    return fail(GLOP_ECAPACITY, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(GLOP_EINVAL, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(GLOP_ENOMEM, "glop_build_failureless_trie: out of memory");
+  }
+}
+
+void glop_free(void* p) { free(p); }
+
+glop_status glop_last_kernel_ms(glop_ctx* c, float* ms) {
+  if (!c || !ms) return fail(GLOP_EINVAL, "glop_last_kernel_ms: null argument");
+  if (!c->timed) return fail(GLOP_EINVAL, "glop_last_kernel_ms: no kernel timed yet");
+  Dev g(c->device);
+  CU(cudaEventSynchronize(c->ev1));
+  CU(cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return GLOP_OK;
+}
+
+uint64_t glop_ctx_launch_count(glop_ctx* c) { return c ? c->launches : 0; }
+
+glop_status glop_run_pfac_pipeline(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text,
+                                   uint64_t n, int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                                   uint64_t* counts, uint64_t* stage1_hits) {
+  return glop_run_pfac_pipeline_shard(c, t, r, text, n, n, 0, text_on_device, alerts, n_alerts, counts,
+                                      stage1_hits);
+}
+
+glop_status glop_run_pfac_pipeline_shard(glop_ctx* c, const glop_trie* t, const glop_rules* r,
+                                         const uint8_t* text, uint64_t n, uint64_t own, uint64_t base,
+                                         int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                                         uint64_t* counts, uint64_t* stage1_hits) {
+  if (!c || !t || !r || !alerts || !n_alerts) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  *alerts = nullptr;
+  *n_alerts = 0;
+  const uint8_t* d_text = nullptr;
+  TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
+  TRY(c->out.ensure(cap * sizeof(glop_hit)));
+  uint64_t nh = 0;
+  glop_status s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
+  if (s == GLOP_ECAPACITY && nh > cap) {
+    c->out.release();
+    cap = nh;
+    TRY(c->out.ensure(cap * sizeof(glop_hit)));
+    s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
+  }
+  if (s != GLOP_OK) return s;
+  if (stage1_hits) *stage1_hits = nh;
+  const uint32_t k = r->view.n_patterns;
+  TRY(c->alerts.ensure(std::max<uint64_t>(nh, 1) * sizeof(glop_alert) + (size_t)(k + 1) * 8));
+  glop_alert* d_alerts = c->alerts.as<glop_alert>();
+  uint64_t* d_counts = reinterpret_cast<uint64_t*>(d_alerts + std::max<uint64_t>(nh, 1));
+  CU(cudaMemsetAsync(d_counts, 0, (size_t)k * 8 + 8, c->stream));
+  uint64_t kept = 0;
+  TRY(verify_device_impl(c, r, d_text, n, base, c->out.as<glop_hit>(), nh, d_alerts, &kept, d_counts));
+  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(kept, 1) * sizeof(glop_alert)));
+  if (!a) return fail(GLOP_ENOMEM, "glop_run_pfac_pipeline: host allocation");
+  cudaError_t e = cudaSuccess;
+  if (kept) e = cudaMemcpyAsync(a, d_alerts, kept * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && counts) e = cudaMemcpyAsync(counts, d_counts, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(a);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *alerts = a;
+  *n_alerts = kept;
+  return GLOP_OK;
+}
+
+glop_status glop_device_alloc(glop_ctx* c, uint64_t bytes, void** out) {
+  Dev g(c->device);
+  CU(cudaMalloc(out, std::max<uint64_t>(bytes, 16)));
+  return GLOP_OK;
+}
+glop_status glop_device_free(glop_ctx* c, void* p) {
+  Dev g(c->device);
+  CU(cudaFree(p));
+  return GLOP_OK;
+}
+glop_status glop_host_alloc(uint64_t bytes, void** out) {
+  CU(cudaMallocHost(out, std::max<uint64_t>(bytes, 16)));
+  return GLOP_OK;
+}
+glop_status glop_host_free(void* p) {
+  CU(cudaFreeHost(p));
+  return GLOP_OK;
+}
+glop_status glop_memcpy(glop_ctx* c, void* dst, const void* src, uint64_t bytes, int kind) {
+  Dev g(c->device);
+  cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                               : (kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  CU(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+  return GLOP_OK;
+}
+
+glop_status glop_gen_syslog_device(glop_ctx* c, uint8_t* d_out, uint64_t begin, uint64_t n, uint64_t seed) {
+  if (n == 0) return GLOP_OK;
+  Dev g(c->device);
+  const uint64_t blocks = (begin + n - 1) / glop_corpus::kBlock - begin / glop_corpus::kBlock + 1;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((blocks + 127) / 128, 65535);
+  ++c->launches;
+  gen_syslog_kernel<<<grid, 128, 0, c->stream>>>(d_out, begin, n, seed);
+  CU(cudaGetLastError());
+  return GLOP_OK;
+}
+
+glop_status glop_gen_syslog_host(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads) {
+  glop_workload::gen_syslog(out, begin, n, seed, threads);
+  return GLOP_OK;
+}
+
+glop_status glop_gen_reference_log(uint8_t* out, uint64_t size, uint32_t seed, uint64_t line_len) {
+  if (size == 0 || line_len < 2) return fail(GLOP_EINVAL, "generate_log: bad size/line_len");
+  std::string s = glop_workload::reference_generate_log(size, seed, line_len);
+  memcpy(out, s.data(), size);
+  return GLOP_OK;
+}
+
+glop_status glop_gen_rules(uint32_t k, uint32_t seed, uint32_t len, uint8_t* bytes, uint8_t* is_vocab) {
+  auto rules = glop_workload::synthetic_rules(k, seed, len);
+  for (uint32_t i = 0; i < k; ++i) {
+    memcpy(bytes + (size_t)i * len, rules[i].bytes.data(), len);
+    if (is_vocab) is_vocab[i] = rules[i].name.rfind("vocab-", 0) == 0;
+  }
+  return GLOP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,777 @@
+// glop_kernels.cuh -- sm_100a device code for the GLoP matching path.
+//
+//   pfac_tile_kernel  K1  PFAC scan (scan.hpp:113-202), two variants:
+//                         FILTERED: sampled q-gram filter + 8-byte prefix
+//                         bitmap in shared memory, then the trie walk only for
+//                         survivors (GPU analogue of RootJump, scan.hpp:81-108)
+//                         DIRECT:   one thread per start byte, literal walk
+//   tile_prefix / gather  K2  deterministic (offset, pattern_id) order
+//                         (scan.hpp:197-201) without a global sort
+//   verify_*          K3  stage-2 suffix check (verify.hpp:69-105)
+//   kmp_tile_kernel   K4  chunk-parallel KMP with (m-1)-byte warm-up
+//                         (kmp.hpp:41-69), exact comparison counts
+//   gen_syslog_kernel     synthetic corpus (bench input, not the path)
+//
+// Text is streamed HBM -> shared memory with 1-D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) into a ring of stages; one
+// persistent CTA per SM walks its tiles round-robin.
+#pragma once
+#include <stdint.h>
+
+#include "corpus.h"
+
+namespace glop {
+
+constexpr int kThreads = 512;
+constexpr uint32_t kTile = 16384;           // owned start positions per tile
+constexpr uint32_t kHalo = 64;              // bytes past the tile kept in smem
+constexpr uint32_t kStageBytes = kTile + kHalo + 16;  // +16: alignment slack
+constexpr int kStages = 4;
+constexpr uint32_t kHitCap = 2048;          // per-tile hit keys in smem
+constexpr uint32_t kDmaskBytes = 65536;     // level-1 q-gram d-mask buckets
+constexpr uint32_t kBm2Bits = 1u << 18;     // level-2 prefix bitmap
+constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
+
+struct TileDir {
+  unsigned long long slot;
+  uint32_t count;
+  uint32_t overflow;
+};
+
+struct DevTrie {
+  const uint8_t* cls;       // 256 byte -> class
+  const void* table;        // Q x C entries, 0 = no edge
+  const uint32_t* out_off;  // Q + 1
+  const uint32_t* out_pid;  // flat output pattern ids
+  const uint32_t* pid_len;  // pattern id -> matched_len
+  const uint8_t* dmask;     // kDmaskBytes
+  const uint32_t* bm2;      // kBm2Bits / 32 words
+  uint32_t Q, C, lmin, lmax, q, stride;
+  uint32_t table_bytes;     // padded to 16
+};
+
+struct ScanParams {
+  const uint8_t* text;
+  unsigned long long n, own, base;
+  uint32_t num_tiles;
+  int mode;  // 0: per-tile sorted staging + directory; 1: global keys
+  struct glop_hit_t {
+    unsigned long long offset;
+    uint32_t pid, len;
+  }* staging;
+  unsigned long long staging_cap;
+  unsigned long long* g_count;  // total hits (all tiles)
+  TileDir* dir;
+  unsigned int* g_flags;        // bit0: some tile overflowed its smem buffer
+  unsigned long long* keys;     // mode 1: (offset << 24) | pid
+  unsigned long long keys_cap;
+};
+using DevHit = ScanParams::glop_hit_t;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------ hashing
+// Level-1 bucket of a q-gram packed little-endian (q <= 4).  q <= 2 is exact.
+__host__ __device__ __forceinline__ uint32_t qgram_bucket(uint32_t g, uint32_t q) {
+  return q <= 2 ? g : ((g * 0x9E3779B1u) >> 16);
+}
+// Level-2 bit of an (up to) 8-byte prefix packed little-endian.
+__host__ __device__ __forceinline__ uint32_t prefix_bit(unsigned long long key) {
+  return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 46);
+}
+__host__ __device__ __forceinline__ unsigned long long low_bytes_mask(uint32_t k) {
+  return k >= 8 ? ~0ull : ((1ull << (8 * k)) - 1);
+}
+
+// ------------------------------------------------------------------ tile ring
+// Window of tile t in "aligned" coordinates: A = text - a, a = text & 15.
+// Stage bytes [0, kStageBytes) hold A[t*kTile, t*kTile + kStageBytes) clipped
+// to the text; text position x lives at win[x + a - t*kTile].
+struct Ring {
+  uint8_t* stages;
+  uint64_t* bars;
+  const uint8_t* A;
+  uint32_t a;
+  unsigned long long n;
+
+  __device__ void issue(int stage, uint32_t t) const {  // one thread
+    uint8_t* dst = stages + (size_t)stage * kStageBytes;
+    const unsigned long long lo = (unsigned long long)t * kTile;
+    const unsigned long long hi = lo + kStageBytes;
+    const unsigned long long vlo = lo > a ? lo : a;               // valid data
+    const unsigned long long vhi = hi < a + n ? hi : a + n;
+    unsigned long long tlo = (vlo + 15) & ~15ull, thi = vhi & ~15ull;
+    if (thi < tlo) thi = tlo;
+    for (unsigned long long x = vlo; x < tlo && x < vhi; ++x) dst[x - lo] = A[x];
+    for (unsigned long long x = thi > vlo ? thi : vlo; x < vhi; ++x) dst[x - lo] = A[x];
+    if (thi > tlo) {
+      mbar_arrive_tx(&bars[stage], (uint32_t)(thi - tlo));
+      bulk_g2s(dst + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), &bars[stage]);
+    } else {
+      mbar_arrive(&bars[stage]);
+    }
+  }
+};
+
+// Unaligned little-endian loads from a stage window (idx + 8 < kStageBytes).
+__device__ __forceinline__ uint32_t win_u32(const uint8_t* win, uint32_t idx) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(win + (idx & ~3u));
+  return __funnelshift_r(w[0], w[1], (idx & 3u) * 8);
+}
+__device__ __forceinline__ unsigned long long win_u64(const uint8_t* win, uint32_t idx) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(win + (idx & ~3u));
+  const uint32_t sh = (idx & 3u) * 8;
+  uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+  return (unsigned long long)__funnelshift_r(w0, w1, sh) |
+         ((unsigned long long)__funnelshift_r(w1, w2, sh) << 32);
+}
+
+template <typename Entry>
+struct EntryTraits;
+template <>
+struct EntryTraits<uint16_t> {
+  static constexpr uint32_t kFlag = 0x8000u, kMask = 0x7FFFu;
+};
+template <>
+struct EntryTraits<uint32_t> {
+  static constexpr uint32_t kFlag = 0x80000000u, kMask = 0x7FFFFFFFu;
+};
+
+// ------------------------------------------------------------------ tile sort
+// Ascending bitonic sort of keys[0, P), P a power of two <= kHitCap.
+__device__ __forceinline__ void sort_keys(unsigned long long* keys, uint32_t P) {
+  if (P <= 1) return;
+  const int tid = threadIdx.x;
+  if (P <= 64) {
+    if (tid < 32) {
+      for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t x = tid; x < P; x += 32) {
+            uint32_t y = x ^ j;
+            if (y > x) {
+              unsigned long long u = keys[x], v = keys[y];
+              bool up = (x & k) == 0;
+              if ((u > v) == up) keys[x] = v, keys[y] = u;
+            }
+          }
+          __syncwarp();
+        }
+    }
+    __syncthreads();
+    return;
+  }
+  for (uint32_t k = 2; k <= P; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t x = tid; x < P; x += kThreads) {
+        uint32_t y = x ^ j;
+        if (y > x) {
+          unsigned long long u = keys[x], v = keys[y];
+          bool up = (x & k) == 0;
+          if ((u > v) == up) keys[x] = v, keys[y] = u;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K1 PFAC
+struct PfacSmem {
+  // byte offsets inside dynamic shared memory
+  static constexpr uint32_t kBars = kStages * kStageBytes;
+  static constexpr uint32_t kCls = kBars + kStages * 8;
+  static constexpr uint32_t kMisc = kCls + 256;          // 16 bytes
+  static constexpr uint32_t kKeys = kMisc + 16;          // kHitCap * 8
+  static constexpr uint32_t kEnd = kKeys + kHitCap * 8;  // then filter, then table
+  static __host__ __device__ uint32_t dmask(bool filter) { return kEnd; }
+  static __host__ __device__ uint32_t bm2(bool filter) { return kEnd + (filter ? kDmaskBytes : 0); }
+  static __host__ __device__ uint32_t table(bool filter) {
+    return kEnd + (filter ? kDmaskBytes + kBm2Bytes : 0);
+  }
+  static __host__ __device__ uint32_t total(bool filter, uint32_t table_bytes) {
+    return table(filter) + table_bytes;
+  }
+};
+
+template <bool kFilter, bool kSmemTable, typename Entry>
+__global__ void __launch_bounds__(kThreads, 1) pfac_tile_kernel(const DevTrie tr, const ScanParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  using ET = EntryTraits<Entry>;
+  const int tid = threadIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PfacSmem::kBars);
+  uint8_t* s_cls = smem + PfacSmem::kCls;
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + PfacSmem::kMisc);
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + PfacSmem::kKeys);
+  uint8_t* s_dmask = smem + PfacSmem::dmask(kFilter);
+  uint32_t* s_bm2 = reinterpret_cast<uint32_t*>(smem + PfacSmem::bm2(kFilter));
+  Entry* s_table = reinterpret_cast<Entry*>(smem + PfacSmem::table(kFilter));
+
+  // ---- one-time staging of the automaton into shared memory
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(tr.cls);
+    if (tid < 16) reinterpret_cast<uint4*>(s_cls)[tid] = src[tid];
+    if (kFilter) {
+      const uint4* d = reinterpret_cast<const uint4*>(tr.dmask);
+      for (uint32_t i = tid; i < kDmaskBytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_dmask)[i] = d[i];
+      const uint4* b = reinterpret_cast<const uint4*>(tr.bm2);
+      for (uint32_t i = tid; i < kBm2Bytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_bm2)[i] = b[i];
+    }
+    if (kSmemTable) {
+      const uint4* t = reinterpret_cast<const uint4*>(tr.table);
+      for (uint32_t i = tid; i < tr.table_bytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_table)[i] = t[i];
+    }
+    if (tid == 0) {
+      for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+      s_misc[0] = 0;
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+
+  const Entry* T = kSmemTable ? s_table : reinterpret_cast<const Entry*>(tr.table);
+  Ring ring{smem, bars, p.text - ((uintptr_t)p.text & 15), (uint32_t)((uintptr_t)p.text & 15), p.n};
+  if (tid == 0)
+    for (int k = 0; k < kStages; ++k) {
+      uint32_t t = blockIdx.x + k * gridDim.x;
+      if (t < p.num_tiles) ring.issue(k, t);
+    }
+
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t t = blockIdx.x + k * gridDim.x;
+    if (t >= p.num_tiles) break;
+    const int stage = k % kStages;
+    mbar_wait(&bars[stage], (k / kStages) & 1);
+    const uint8_t* win = ring.stages + (size_t)stage * kStageBytes;
+    const unsigned long long t0 = (unsigned long long)t * kTile;
+    const unsigned long long t1 = t0 + kTile < p.own ? t0 + kTile : p.own;
+    const uint32_t wofs = ring.a;  // win index of text position t0
+
+    // byte of text position x (t0 <= x < n)
+    auto tbyte = [&](unsigned long long x) -> uint32_t {
+      unsigned long long li = x - t0 + wofs;
+      return li < kStageBytes ? win[li] : __ldg(p.text + x);
+    };
+    auto emit = [&](unsigned long long i, uint32_t st) {
+      for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o) {
+        const uint32_t pid = __ldg(tr.out_pid + o);
+        if (p.mode == 0) {
+          uint32_t slot = atomicAdd(&s_misc[0], 1u);
+          if (slot < kHitCap) s_keys[slot] = ((i - t0) << 40) | pid;
+        } else {
+          unsigned long long slot = atomicAdd(p.g_count, 1ull);
+          if (slot < p.keys_cap) p.keys[slot] = ((p.base + i) << 24) | pid;
+        }
+      }
+    };
+    // PFAC walk from start i (scan.hpp:125-169): every visited output state
+    // emits; stop at a missing edge or the end of text.
+    auto walk = [&](unsigned long long i) {
+      uint32_t st = 0;
+      for (unsigned long long j = i; j < p.n; ++j) {
+        const uint32_t c = s_cls[tbyte(j)];
+        const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
+        if (!e) break;
+        st = e & ET::kMask;
+        if (e & ET::kFlag) emit(i, st);
+      }
+    };
+
+    if (kFilter) {
+      // Sampled q-gram filter.  Every occurrence of an entry (length >= lmin)
+      // starting at i covers [i, i+lmin); the sampled position P = the
+      // multiple of `stride` in [i, i+stride) satisfies P - i = d <= lmin - q,
+      // so the q-gram at P is the entry's q-gram at offset d, recorded in
+      // dmask[bucket] bit d.  Candidates i = P - d then pass an 8-byte prefix
+      // bitmap before the exact walk.
+      const uint32_t q = tr.q, S = tr.stride, lmin = tr.lmin;
+      const uint32_t qmask = q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * q)) - 1);
+      const unsigned long long kmask = low_bytes_mask(lmin < 8 ? lmin : 8);
+      const unsigned long long pfirst = ((t0 + S - 1) / S) * S;
+      const unsigned long long pend = t1 + S - 1;  // exclusive
+      const uint32_t M = pend > pfirst ? (uint32_t)((pend - pfirst + S - 1) / S) : 0;
+      for (uint32_t m = tid; m < M; m += kThreads) {
+        const unsigned long long P = pfirst + (unsigned long long)m * S;
+        if (P + q > p.n) continue;
+        const uint32_t g = win_u32(win, (uint32_t)(P - t0) + wofs) & qmask;
+        uint32_t dm = s_dmask[qgram_bucket(g, q)];
+        while (dm) {
+          const uint32_t d = __ffs(dm) - 1;
+          dm &= dm - 1;
+          if (P < t0 + d) continue;
+          const unsigned long long i = P - d;
+          if (i >= t1 || i + lmin > p.n) continue;
+          const unsigned long long key = win_u64(win, (uint32_t)(i - t0) + wofs) & kmask;
+          const uint32_t b = prefix_bit(key);
+          if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) continue;
+          walk(i);
+        }
+      }
+    } else {
+      for (unsigned long long i = t0 + tid; i < t1; i += kThreads) walk(i);
+    }
+    __syncthreads();  // stage consumed; hit keys complete
+    if (tid == 0) {
+      uint32_t tn = t + kStages * gridDim.x;
+      if (tn < p.num_tiles) {
+        fence_proxy_async();
+        ring.issue(stage, tn);
+      }
+    }
+    if (p.mode == 0) {
+      const uint32_t nh = s_misc[0];
+      const bool over = nh > kHitCap;
+      if (!over && nh > 1) {
+        uint32_t P = 1;
+        while (P < nh) P <<= 1;
+        for (uint32_t x = nh + tid; x < P; x += kThreads) s_keys[x] = ~0ull;
+        __syncthreads();
+        sort_keys(s_keys, P);
+      }
+      if (tid == 0) {
+        unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
+        p.dir[t].slot = slot;
+        p.dir[t].count = nh;
+        p.dir[t].overflow = over;
+        if (over) atomicOr(p.g_flags, 1u);
+        s_misc[1] = (uint32_t)slot;
+        s_misc[2] = (uint32_t)(slot >> 32);
+      }
+      __syncthreads();
+      const unsigned long long slot = (unsigned long long)s_misc[1] | ((unsigned long long)s_misc[2] << 32);
+      if (!over && slot + nh <= p.staging_cap) {
+        for (uint32_t h = tid; h < nh; h += kThreads) {
+          const unsigned long long key = s_keys[h];
+          const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
+          DevHit out;
+          out.offset = p.base + t0 + (key >> 40);
+          out.pid = pid;
+          out.len = __ldg(tr.pid_len + pid);
+          p.staging[slot + h] = out;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_misc[0] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+// Exclusive prefix of per-tile counts (single CTA, any number of tiles).
+__global__ void __launch_bounds__(1024) tile_prefix_kernel(const TileDir* dir, uint32_t num_tiles,
+                                                           unsigned long long* prefix) {
+  __shared__ unsigned long long part[1024];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (num_tiles + 1023) / 1024;
+  const uint32_t b = tid * per, e = min(num_tiles, b + per);
+  unsigned long long s = 0;
+  for (uint32_t i = b; i < e; ++i) s += dir[i].count;
+  part[tid] = s;
+  __syncthreads();
+  for (uint32_t off = 1; off < 1024; off <<= 1) {
+    unsigned long long v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  unsigned long long run = part[tid] - s;
+  for (uint32_t i = b; i < e; ++i) {
+    prefix[i] = run;
+    run += dir[i].count;
+  }
+}
+
+// Copies each tile's sorted hits from staging to its final position (one warp
+// per tile).
+template <typename Rec>
+__global__ void gather_kernel(const TileDir* dir, const unsigned long long* prefix, uint32_t num_tiles,
+                              const Rec* staging, Rec* out) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = warp; t < num_tiles; t += nw) {
+    const uint32_t c = dir[t].count;
+    const Rec* src = staging + dir[t].slot;
+    Rec* dst = out + prefix[t];
+    for (uint32_t h = lane; h < c; h += 32) dst[h] = src[h];
+  }
+}
+
+// Global-key fallback: sorted (offset << 24 | pid) keys -> hits.
+__global__ void keys_to_hits_kernel(const unsigned long long* keys, unsigned long long n,
+                                    const uint32_t* pid_len, DevHit* out) {
+  for (unsigned long long h = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; h < n;
+       h += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[h];
+    DevHit r;
+    r.offset = k >> 24;
+    r.pid = (uint32_t)(k & 0xFFFFFF);
+    r.len = pid_len[r.pid];
+    out[h] = r;
+  }
+}
+
+// ------------------------------------------------------------------ K3 verify
+struct DevRules {
+  const uint8_t* bytes;
+  const unsigned long long* off;
+  uint32_t n_patterns;
+  unsigned long long prefix_len;
+};
+
+struct DevAlert {
+  unsigned long long offset;
+  uint32_t rule_id, pattern_len;
+};
+
+constexpr int kVerifyBlock = 1024;
+
+// Pass 1: keep flags, per-block keep counts, error / order flags.
+// text holds global offsets [base, base + n).
+__global__ void __launch_bounds__(kVerifyBlock) verify_flags_kernel(
+    const DevRules r, const uint8_t* text, unsigned long long base, unsigned long long n, const DevHit* hits,
+    unsigned long long n_hits, uint8_t* keep, uint32_t* block_counts, unsigned int* flags) {
+  __shared__ uint32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const unsigned long long h = blockIdx.x * (unsigned long long)kVerifyBlock + threadIdx.x;
+  uint32_t ok = 0;
+  if (h < n_hits) {
+    const DevHit x = hits[h];
+    if (x.offset < base || x.offset + x.len > base + n || x.pid >= r.n_patterns) {  // verify.hpp:76-77, .at()
+      atomicOr(flags, 1u);
+    } else {
+      const unsigned long long pb = r.off[x.pid], plen = r.off[x.pid + 1] - pb;
+      if (plen <= r.prefix_len) {
+        ok = 1;
+      } else if (x.offset + plen > base + n) {
+        ok = 0;
+      } else {
+        ok = 1;
+        for (unsigned long long k = x.len; k < plen; ++k)
+          if (text[x.offset - base + k] != r.bytes[pb + k]) {
+            ok = 0;
+            break;
+          }
+      }
+    }
+    if (h + 1 < n_hits) {
+      const DevHit y = hits[h + 1];
+      if (y.offset < x.offset || (y.offset == x.offset && y.pid < x.pid)) atomicOr(flags, 2u);
+    }
+    keep[h] = (uint8_t)ok;
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(&s_cnt, __popc(bal));
+  __syncthreads();
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = s_cnt;
+}
+
+__global__ void __launch_bounds__(1024) block_prefix_kernel(const uint32_t* counts, uint32_t nb,
+                                                            unsigned long long* prefix,
+                                                            unsigned long long* total) {
+  __shared__ unsigned long long part[1024];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (nb + 1023) / 1024;
+  const uint32_t b = tid * per, e = min(nb, b + per);
+  unsigned long long s = 0;
+  for (uint32_t i = b; i < e; ++i) s += counts[i];
+  part[tid] = s;
+  __syncthreads();
+  for (uint32_t off = 1; off < 1024; off <<= 1) {
+    unsigned long long v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  unsigned long long run = part[tid] - s;
+  for (uint32_t i = b; i < e; ++i) {
+    prefix[i] = run;
+    run += counts[i];
+  }
+  if (tid == 1023) *total = part[1023];
+}
+
+// Pass 2: stable compaction of kept hits into alerts (+ per-pattern counts).
+__global__ void __launch_bounds__(kVerifyBlock) verify_scatter_kernel(
+    const DevRules r, const DevHit* hits, unsigned long long n_hits, const uint8_t* keep,
+    const unsigned long long* block_prefix, DevAlert* out, unsigned long long* counts) {
+  __shared__ uint32_t warp_base[kVerifyBlock / 32];
+  const unsigned long long h = blockIdx.x * (unsigned long long)kVerifyBlock + threadIdx.x;
+  const uint32_t ok = h < n_hits ? keep[h] : 0;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+  if (lane == 0) warp_base[w] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int i = 0; i < kVerifyBlock / 32; ++i) {
+      uint32_t c = warp_base[i];
+      warp_base[i] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (ok) {
+    const DevHit x = hits[h];
+    const unsigned long long dst =
+        block_prefix[blockIdx.x] + warp_base[w] + __popc(bal & ((1u << lane) - 1));
+    DevAlert a;
+    a.offset = x.offset;
+    a.rule_id = x.pid;
+    a.pattern_len = (uint32_t)(r.off[x.pid + 1] - r.off[x.pid]);
+    out[dst] = a;
+    if (counts) atomicAdd(counts + x.pid, 1ull);
+  }
+}
+
+// Unsorted-input path of verify: alerts <-> (offset << 24 | rule) keys.
+__global__ void alerts_to_keys_kernel(const DevAlert* a, unsigned long long n, unsigned long long* keys) {
+  for (unsigned long long h = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; h < n;
+       h += (unsigned long long)gridDim.x * blockDim.x)
+    keys[h] = (a[h].offset << 24) | a[h].rule_id;
+}
+__global__ void keys_to_alerts_kernel(const unsigned long long* keys, unsigned long long n, const DevRules r,
+                                      DevAlert* out) {
+  for (unsigned long long h = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; h < n;
+       h += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[h];
+    DevAlert a;
+    a.offset = k >> 24;
+    a.rule_id = (uint32_t)(k & 0xFFFFFF);
+    a.pattern_len = (uint32_t)(r.off[a.rule_id + 1] - r.off[a.rule_id]);
+    out[h] = a;
+  }
+}
+
+// ------------------------------------------------------------------ K4 KMP
+// DFA entry for (state j, class c): next state (13 bits) | match << 13 |
+// comparisons << 14, replaying the reference loop (kmp.hpp:52-66) exactly.
+constexpr uint32_t kKmpChunk = 132;  // 33 words: lane-private banks
+constexpr uint32_t kKmpTile = kKmpChunk * kThreads;  // 67584 owned bytes
+constexpr uint32_t kKmpPre = 256;    // warm-up bytes kept before the tile
+constexpr uint32_t kKmpStageBytes = kKmpPre + kKmpTile + 16;
+constexpr int kKmpStages = 2;
+constexpr uint32_t kKmpHitCap = 2048;
+
+struct KmpParams {
+  const uint8_t* text;
+  unsigned long long n, own, base;
+  uint32_t m, C, num_tiles;
+  const uint32_t* dfa;  // m x C
+  const uint8_t* cls;   // 256
+  uint32_t dfa_words;   // padded to 4
+  uint32_t first_class; // class of p[0]
+  uint32_t p0;          // p[0]
+  unsigned long long* staging;
+  unsigned long long staging_cap;
+  unsigned long long* g_count;
+  TileDir* dir;
+  unsigned int* g_flags;
+  unsigned long long* comparisons;
+  int mode;                    // 0: per-tile order; 1: global keys (fallback)
+  unsigned long long* keys;    // mode 1: start offsets
+  unsigned long long keys_cap;
+};
+
+struct KmpSmem {
+  static constexpr uint32_t kBars = kKmpStages * kKmpStageBytes;
+  static constexpr uint32_t kCls = kBars + kKmpStages * 8;
+  static constexpr uint32_t kMisc = kCls + 256;
+  static constexpr uint32_t kKeys = kMisc + 16;
+  static constexpr uint32_t kDfa = kKeys + kKmpHitCap * 8;
+};
+
+template <bool kSmemDfa>
+__global__ void __launch_bounds__(kThreads, 1) kmp_tile_kernel(const KmpParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KmpSmem::kBars);
+  uint8_t* s_cls = smem + KmpSmem::kCls;
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + KmpSmem::kMisc);
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + KmpSmem::kKeys);
+  uint32_t* s_dfa = reinterpret_cast<uint32_t*>(smem + KmpSmem::kDfa);
+  if (tid < 16) reinterpret_cast<uint4*>(s_cls)[tid] = reinterpret_cast<const uint4*>(p.cls)[tid];
+  if (kSmemDfa)
+    for (uint32_t i = tid; i < p.dfa_words / 4; i += kThreads)
+      reinterpret_cast<uint4*>(s_dfa)[i] = reinterpret_cast<const uint4*>(p.dfa)[i];
+  if (tid == 0) {
+    for (int s = 0; s < kKmpStages; ++s) mbar_init(&bars[s], 1);
+    s_misc[0] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t* D = kSmemDfa ? s_dfa : p.dfa;
+  const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
+  const uint8_t* A = p.text - a;
+  // stage holds A[t*kKmpTile + a - kKmpPre .. ) rounded down to 16: text
+  // position x lives at win[x - wbase]
+  auto issue = [&](int stage, uint32_t t) {
+    uint8_t* dst = smem + (size_t)stage * kKmpStageBytes;
+    const long long lo_s = (long long)t * kKmpTile + a - kKmpPre;  // A coords, 16-aligned
+    const unsigned long long lo = lo_s < 0 ? 0 : (unsigned long long)lo_s;
+    const unsigned long long dst_off = (unsigned long long)(lo_s < 0 ? -lo_s : 0);
+    const unsigned long long hi = (unsigned long long)(lo_s + kKmpStageBytes);
+    const unsigned long long vlo = lo > a ? lo : a, vhi = hi < a + p.n ? hi : a + p.n;
+    unsigned long long tlo = (vlo + 15) & ~15ull, thi = vhi & ~15ull;
+    if (thi < tlo) thi = tlo;
+    for (unsigned long long x = vlo; x < tlo && x < vhi; ++x) dst[dst_off + x - lo] = A[x];
+    for (unsigned long long x = thi > vlo ? thi : vlo; x < vhi; ++x) dst[dst_off + x - lo] = A[x];
+    if (thi > tlo) {
+      mbar_arrive_tx(&bars[stage], (uint32_t)(thi - tlo));
+      bulk_g2s(dst + dst_off + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), &bars[stage]);
+    } else {
+      mbar_arrive(&bars[stage]);
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < kKmpStages; ++k) {
+      uint32_t t = blockIdx.x + k * gridDim.x;
+      if (t < p.num_tiles) issue(k, t);
+    }
+  unsigned long long cmp_total = 0;
+  const uint32_t p0x4 = p.p0 * 0x01010101u;
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t t = blockIdx.x + k * gridDim.x;
+    if (t >= p.num_tiles) break;
+    const int stage = k % kKmpStages;
+    mbar_wait(&bars[stage], (k / kKmpStages) & 1);
+    const uint8_t* win = smem + (size_t)stage * kKmpStageBytes;
+    const unsigned long long t0 = (unsigned long long)t * kKmpTile;
+    // win index of text position x: x - t0 + kKmpPre
+    const unsigned long long c0 = t0 + (unsigned long long)tid * kKmpChunk;
+    const unsigned long long c1 = min(c0 + kKmpChunk, p.own);
+    if (c0 < c1) {
+      auto tbyte = [&](unsigned long long x) -> uint32_t {
+        long long li = (long long)(x - t0) + kKmpPre;
+        return (li >= 0 && li < (long long)kKmpStageBytes) ? win[li] : __ldg(p.text + x);
+      };
+      // warm-up: (m-1) bytes before the chunk resynchronise the state
+      uint32_t j = 0;
+      unsigned long long x = c0 >= p.m - 1 ? c0 - (p.m - 1) : 0;
+      for (; x < c0; ++x) j = D[j * p.C + s_cls[tbyte(x)]] & 0x1FFFu;
+      unsigned long long cmp = 0;
+      x = c0;
+      while (x < c1) {
+        // state-0 skip: four bytes none of which is p[0] keep state 0, one
+        // comparison each
+        if (j == 0 && x + 4 <= c1 && ((x - t0 + kKmpPre) & 3) == 0 &&
+            (x - t0 + kKmpPre + 4) <= kKmpStageBytes) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(win + (x - t0 + kKmpPre));
+          if (__vcmpeq4(w, p0x4) == 0) {
+            cmp += 4;
+            x += 4;
+            continue;
+          }
+        }
+        const uint32_t e = D[j * p.C + s_cls[tbyte(x)]];
+        cmp += e >> 14;
+        if (e & 0x2000u) {
+          if (p.mode == 0) {
+            const uint32_t slot = atomicAdd(&s_misc[0], 1u);
+            if (slot < kKmpHitCap) s_keys[slot] = x - t0;  // match ends at x
+          } else {
+            const unsigned long long slot = atomicAdd(p.g_count, 1ull);
+            if (slot < p.keys_cap) p.keys[slot] = p.base + x + 1 - p.m;
+          }
+        }
+        j = e & 0x1FFFu;
+        ++x;
+      }
+      cmp_total += cmp;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t tn = t + kKmpStages * gridDim.x;
+      if (tn < p.num_tiles) {
+        fence_proxy_async();
+        issue(stage, tn);
+      }
+    }
+    if (p.mode != 0) {
+      __syncthreads();
+      continue;
+    }
+    const uint32_t nh = s_misc[0];
+    const bool over = nh > kKmpHitCap;
+    if (!over && nh > 1) {
+      uint32_t P = 1;
+      while (P < nh) P <<= 1;
+      for (uint32_t y = nh + tid; y < P; y += kThreads) s_keys[y] = ~0ull;
+      __syncthreads();
+      sort_keys(s_keys, P);
+    }
+    if (tid == 0) {
+      unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
+      p.dir[t].slot = slot;
+      p.dir[t].count = nh;
+      p.dir[t].overflow = over;
+      if (over) atomicOr(p.g_flags, 1u);
+      s_misc[1] = (uint32_t)slot;
+      s_misc[2] = (uint32_t)(slot >> 32);
+    }
+    __syncthreads();
+    const unsigned long long slot = (unsigned long long)s_misc[1] | ((unsigned long long)s_misc[2] << 32);
+    if (!over && slot + nh <= p.staging_cap)
+      for (uint32_t h = tid; h < nh; h += kThreads)
+        p.staging[slot + h] = p.base + t0 + s_keys[h] + 1 - p.m;
+    __syncthreads();
+    if (tid == 0) s_misc[0] = 0;
+    __syncthreads();
+  }
+  // comparisons: warp reduce then one atomic per warp
+  for (int o = 16; o; o >>= 1) cmp_total += __shfl_xor_sync(0xffffffffu, cmp_total, o);
+  if ((tid & 31) == 0 && cmp_total) atomicAdd(p.comparisons, cmp_total);
+}
+
+// ------------------------------------------------------------------ corpus
+__global__ void gen_syslog_kernel(uint8_t* out, unsigned long long begin, unsigned long long n,
+                                  unsigned long long seed) {
+  using glop_corpus::kBlock;
+  const unsigned long long b0 = begin / kBlock, b1 = (begin + n - 1) / kBlock + 1;
+  for (unsigned long long b = b0 + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; b < b1;
+       b += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long s = b * kBlock > begin ? b * kBlock : begin;
+    const unsigned long long e = (b + 1) * kBlock < begin + n ? (b + 1) * kBlock : begin + n;
+    glop_corpus::gen_block_range(out + (s - begin), seed, b, (uint32_t)(s - b * kBlock),
+                                 (uint32_t)(e - b * kBlock));
+  }
+}
+
+}  // namespace glop

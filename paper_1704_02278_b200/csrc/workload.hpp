@@ -29,7 +29,7 @@ inline void gen_syslog(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed,
   auto work = [&](uint64_t lo, uint64_t hi) {
     std::vector<uint8_t> tmp(kBlock);
     for (uint64_t b = lo; b < hi; ++b) {
-      glop_corpus::gen_block(tmp.data(), seed, b, kBlock);
+      glop_corpus::gen_block(tmp.data(), seed, b);
       uint64_t s = std::max(begin, b * kBlock), e = std::min(begin + n, (b + 1) * kBlock);
       memcpy(out + (s - begin), tmp.data() + (s - b * kBlock), e - s);
     }
@@ -77,10 +77,29 @@ inline std::vector<std::string> reference_random_rules(size_t count, size_t len,
 
 // All distinct 8-byte windows of the literal text of the incident templates
 // (weight class <= 'c'), taken after the '^' marker, never spanning a
-// placeholder.  Deterministic order (template order, then position).
+// placeholder, and never occurring in the literal text of a routine
+// (non-incident) template -- so vocabulary rules fire on incident lines only.
+// Deterministic order (template order, then position).
 inline std::vector<std::string> vocab_windows(size_t w = 8) {
   std::vector<std::string> out;
   std::unordered_set<std::string> seen;
+  std::string routine;  // literal text of every routine template
+  for (const char* p = glop_corpus::kTplHost; *p;) {
+    const char* e = p;
+    while (*e && *e != '|') ++e;
+    if (*p > 'c') {
+      for (const char* x = p + 1; x < e; ++x) {
+        if (*x == '{') {
+          routine += '\x01';
+          while (x < e && *x != '}') ++x;
+        } else if (*x != '^') {
+          routine += *x;
+        }
+      }
+      routine += '\x01';
+    }
+    p = *e ? e + 1 : e;
+  }
   const char* p = glop_corpus::kTplHost;
   while (*p) {
     const char* e = p;
@@ -95,6 +114,7 @@ inline std::vector<std::string> vocab_windows(size_t w = 8) {
     auto flush = [&]() {
       for (size_t i = 0; i + w <= seg.size(); ++i) {
         std::string win = seg.substr(i, w);
+        if (routine.find(win) != std::string::npos) continue;
         if (seen.insert(win).second) out.push_back(win);
       }
       seg.clear();

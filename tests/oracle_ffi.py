@@ -79,6 +79,10 @@ def ref():
                                          C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
             _ref.ref_kmp_search.argtypes = [u8p, C.c_uint64, u8p, C.c_uint32, C.POINTER(vp), u64p, u64p]
             _ref.ref_free.argtypes = [vp]
+            _ref.ref_time_pfac.argtypes = [u8p, C.c_uint64, u8p, u64p, C.c_uint32, C.c_uint64, C.c_int, C.c_uint,
+                                           C.c_uint32, C.c_uint32, C.POINTER(C.c_double), u64p]
+            _ref.ref_time_kmp.argtypes = [u8p, C.c_uint64, u8p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.POINTER(C.c_double), u64p]
             _ref.ref_default_workers.restype = C.c_uint
     return _ref
 
@@ -247,3 +251,44 @@ def ref_measure(text, patterns, L, engine=2, workers=0, runs=3):
     if rc:
         raise OracleError(rc)
     return ms.value, bps.value
+
+
+def ref_time_pfac(text, patterns, L, warmup=1, runs=3, workers=0, compact=True):
+    """Reference pfac_scan + verify_hits timed per run (the body of
+    bench.hpp:103-109).  Returns (run_seconds list, n_alerts)."""
+    r = ref()
+    t, n = _text_arr(text)
+    pat, off = pack_patterns(patterns)
+    secs = (C.c_double * max(runs, 1))()
+    na = C.c_uint64()
+    rc = r.ref_time_pfac(t.ctypes.data_as(u8p), n, pat.ctypes.data_as(u8p), off.ctypes.data_as(u64p),
+                         len(patterns), L, 1 if compact else 0, workers, warmup, runs, secs, C.byref(na))
+    if rc:
+        raise OracleError(rc)
+    return list(secs)[:runs], na.value
+
+
+def ref_time_kmp(text, p: bytes, warmup=1, runs=3):
+    r = ref()
+    t, n = _text_arr(text)
+    pa = np.frombuffer(p, dtype=np.uint8).copy()
+    secs = (C.c_double * max(runs, 1))()
+    nm = C.c_uint64()
+    r.ref_time_kmp(t.ctypes.data_as(u8p), n, pa.ctypes.data_as(u8p), len(p), warmup, runs, secs, C.byref(nm))
+    return list(secs)[:runs], nm.value
+
+
+def port_time_pfac(text, patterns, L, warmup=1, runs=3):
+    """The C restatement (oracle/liboracle.so) timed the same way, single
+    thread -- the CPU baseline when oracle/_ref was never built."""
+    import time
+
+    trie = Trie(patterns, L)
+    secs, na = [], 0
+    for i in range(warmup + runs):
+        t0 = time.perf_counter()
+        hits = pfac_scan(text, trie)
+        na = len(verify_hits(text, hits, patterns, L))
+        if i >= warmup:
+            secs.append(time.perf_counter() - t0)
+    return secs, na

@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bit-exact for every hit, alert, offset
+and comparison count.  Run on the B200: pytest -m gpu."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import golden_io as G
+import oracle_ffi as O
+from paper_1704_02278_b200 import glop
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KERNELS = [glop.PFAC_FILTERED, glop.PFAC_DIRECT]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return glop.Context(0)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    assert torch.cuda.is_available(), "-m gpu tests need the B200"
+    return torch
+
+
+def dev_scan(ctx, torch, trie, text: np.ndarray, kernel, own=None, base=0, offset=0):
+    """pfac_scan_device over text[offset:] resident in HBM."""
+    n = text.size - offset
+    d = torch.from_numpy(np.ascontiguousarray(text)).cuda() if text.size else torch.zeros(1, dtype=torch.uint8).cuda()
+    cap = max(1 << 16, 4 * n)
+    out = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
+    nh = ctx.pfac_scan_device(trie, d.data_ptr() + offset, n, out.data_ptr(), cap, own=own, base=base, kernel=kernel)
+    ctx.synchronize()
+    return out[: nh * 16].cpu().numpy().view(glop.HIT_DTYPE).copy()
+
+
+def alerts_as_golden(a, lines=None):
+    out = np.zeros(len(a), dtype=G.ALERT_DTYPE)
+    out["offset"], out["rule_id"], out["pattern_len"] = a["offset"], a["rule_id"], a["pattern_len"]
+    if lines is not None:
+        out["line"] = lines
+    return out
+
+
+def line_numbers(text: np.ndarray, offsets) -> np.ndarray:
+    """LineIndex::line_of (verify.hpp:48-53) for test bookkeeping."""
+    nl = np.flatnonzero(text == 10)
+    return np.searchsorted(nl + 1, np.asarray(offsets, dtype=np.int64), side="right") + 1
+
+
+def run_case(ctx, pats, text, L, kernel):
+    trie = ctx.upload(glop.build_failureless_trie(pats, L))
+    hits = ctx.pfac_scan(trie, text) if kernel is None else dev_scan(ctx, __import__("torch"), trie,
+                                                                     np.frombuffer(text, np.uint8), kernel)
+    rules = ctx.upload_rules(pats, L)
+    alerts = ctx.verify_hits(rules, text, hits)
+    return hits, alerts
+
+
+# ------------------------------------------------------------------ known answers
+def test_known_answers(ctx):
+    """test_scan.cpp:57-78, test_verify.cpp:26-65 via the golden records."""
+    for c in G.load("known_answer") + G.load("loggen_evil") + G.load("scan_workers"):
+        for kernel in (None, *KERNELS):
+            hits, alerts = run_case(ctx, c.patterns, c.text, c.L, kernel)
+            assert G.pack_hits(hits) == G.pack_hits(c.hits)
+            t = np.frombuffer(c.text, np.uint8)
+            lines = line_numbers(t, alerts["offset"]) if c.alerts["line"].any() else None
+            assert G.pack_alerts(alerts_as_golden(alerts, lines)) == G.pack_alerts(c.alerts)
+
+
+def test_errors_map_to_reference_exceptions(ctx):
+    rules = ctx.upload_rules([b"root"], 8)
+    with pytest.raises(glop.LogicError):  # verify.hpp:76-77
+        ctx.verify_hits(rules, b"ab", np.array([(1, 0, 4)], dtype=glop.HIT_DTYPE))
+    a = glop.build_failureless_trie([b"AB"], 8)
+    bad = glop.Automaton(a.dense_table.copy(), a.out_offsets, a.out_flat)
+    bad.dense_table[1, ord("Z")] = 0  # edge back to the root: not a trie
+    with pytest.raises(glop.InvalidArgument):
+        ctx.upload(bad)
+
+
+# ------------------------------------------------------------------ randomized families
+@pytest.mark.parametrize("family,gen", [("acceptance_exactness", G.acceptance_exactness_inputs),
+                                        ("scan_superset", G.scan_superset_inputs)])
+def test_randomized_families(ctx, torch_cuda, family, gen):
+    """acceptance.cpp:42-78 (1000 trials) and test_scan.cpp:157-176: both
+    kernels bit-identical to the reference (hit and alert digests)."""
+    for rec, (pats, text, L, _w) in zip(G.load(family), gen()):
+        assert G.sha(G.pack_inputs(pats, text)) == rec.inputs_sha
+        trie = ctx.upload(glop.build_failureless_trie(pats, L))
+        rules = ctx.upload_rules(pats, L)
+        t = np.frombuffer(text, np.uint8)
+        for kernel in KERNELS:
+            hits = dev_scan(ctx, torch_cuda, trie, t, kernel)
+            assert len(hits) == rec.n_hits and G.sha(G.pack_hits(hits)) == rec.hits_sha, (family, kernel)
+        alerts = ctx.verify_hits(rules, text, hits)
+        assert len(alerts) == rec.n_alerts
+        assert G.sha(G.pack_alerts(alerts_as_golden(alerts))) == rec.alerts_sha
+
+
+def test_kmp_families(ctx):
+    """test_kmp.cpp:58-93, acceptance.cpp:209-229: offsets and the exact
+    sequential comparison count."""
+    recs = G.load("kmp_naive")
+    for rec, (p, text) in zip([r for r in recs if r.inputs_sha], G.kmp_naive_inputs()):
+        offs, cmp_ = ctx.kmp_search(p, text)
+        assert len(offs) == rec.n_offsets and G.sha(offs.astype("<u8").tobytes()) == rec.offsets_sha
+        assert cmp_ == rec.comparisons
+    for rec in [r for r in recs if not r.inputs_sha]:
+        offs, cmp_ = ctx.kmp_search(rec.pattern, rec.text)
+        assert list(offs) == list(rec.offsets) and cmp_ == rec.comparisons
+    for rec, (p, text) in zip(G.load("kmp_bound"), G.kmp_bound_inputs()):
+        offs, cmp_ = ctx.kmp_search(p, text)
+        assert cmp_ == rec.comparisons and len(offs) == rec.n_offsets and cmp_ <= 2 * len(text)
+
+
+# ------------------------------------------------------------------ large texts
+def test_reference_corpus_fixtures(ctx, torch_cuda):
+    """acceptance.cpp:165-206: 10 MB reference corpora (determinism with 50
+    spliced patterns; stage-1 false-positive rate)."""
+    for name in ("determinism", "fp_rate"):
+        (rec,) = G.load(name)
+        if name == "determinism":
+            text = bytearray(glop.gen_reference_log(10_000_000, 1111, 80).tobytes())
+            rng = G.MT19937(1313)
+            for _ in range(50):
+                p = rec.patterns[rng() % len(rec.patterns)]
+                pos = rng() % (len(text) - len(p))
+                text[pos:pos + len(p)] = p
+            text = bytes(text)
+        else:
+            text = glop.gen_reference_log(10_000_000, 909, 80).tobytes()
+        assert G.sha(text) == rec.text_sha
+        t = np.frombuffer(text, np.uint8)
+        trie = ctx.upload(glop.build_failureless_trie(rec.patterns, rec.L))
+        rules = ctx.upload_rules(rec.patterns, rec.L)
+        for kernel in KERNELS:
+            hits = dev_scan(ctx, torch_cuda, trie, t, kernel)
+            assert len(hits) == rec.n_hits
+            alerts = ctx.verify_hits(rules, text, hits)
+            got = alerts_as_golden(alerts, line_numbers(t, alerts["offset"]))
+            assert G.pack_alerts(got) == G.pack_alerts(rec.alerts)
+
+
+def test_syslog_golden(ctx, torch_cuda):
+    """The synthetic RFC 5424 corpus scanned by the reference pipeline."""
+    recs = {r.name: r for r in G.load("syslog")}
+    for name in ("syslog_k10", "syslog_k1000", "syslog_mid"):
+        rec = recs[name]
+        t = glop.gen_syslog_host(rec.n, seed=1, begin=123457 if name == "syslog_mid" else 0)
+        assert G.sha(t.tobytes()) == rec.text_sha
+        trie = ctx.upload(glop.build_failureless_trie(rec.patterns, rec.L))
+        rules = ctx.upload_rules(rec.patterns, rec.L)
+        for kernel in KERNELS:
+            hits = dev_scan(ctx, torch_cuda, trie, t, kernel)
+            assert len(hits) == rec.n_hits
+            alerts = ctx.verify_hits(rules, t, hits)
+            assert G.pack_alerts(alerts_as_golden(alerts, line_numbers(t, alerts["offset"]))) == G.pack_alerts(rec.alerts)
+
+
+def test_device_corpus_equals_host(ctx, torch_cuda):
+    for begin, n in ((0, 1 << 20), (123457, 300001), (4095, 2), (1 << 30, 70000)):
+        d = torch_cuda.empty(n, dtype=torch_cuda.uint8, device="cuda")
+        ctx.gen_syslog_device(d.data_ptr(), n, seed=5, begin=begin)
+        ctx.synchronize()
+        assert np.array_equal(d.cpu().numpy(), glop.gen_syslog_host(n, seed=5, begin=begin))
+
+
+@pytest.mark.parametrize("k", [10, 1000])
+def test_large_syslog_vs_oracle(ctx, torch_cuda, k):
+    """64 MB device-generated syslog: both kernels == oracle, hit for hit."""
+    n = 64 << 20
+    d = torch_cuda.empty(n, dtype=torch_cuda.uint8, device="cuda")
+    ctx.gen_syslog_device(d.data_ptr(), n, seed=42)
+    ctx.synchronize()
+    text = d.cpu().numpy()
+    pats, _ = glop.gen_rules(k, seed=606)
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    ref = O.pfac_scan(text, O.Trie(pats, 8))
+    assert len(ref) > 0
+    for kernel in KERNELS:
+        assert dev_scan(ctx, torch_cuda, trie, text, kernel).tobytes() == ref.tobytes()
+
+
+def test_shards_with_halo_equal_whole(ctx, torch_cuda):
+    """Contiguous shards reporting only owned starts, reading an
+    (lmax-1)-byte halo, concatenate to the whole-text result."""
+    text = glop.gen_syslog_host(8 << 20, seed=3)
+    pats, _ = glop.gen_rules(1000, seed=17)
+    pats += [b"\n<38>1 2026", b"Fa", b"ssh2\n<"]  # short + line-crossing prefixes
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    whole = dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_FILTERED)
+    lmax = trie.info.max_depth
+    for shards in (2, 3, 8):
+        S = -(-text.size // shards)
+        parts = []
+        for g in range(shards):
+            lo, hi = g * S, min((g + 1) * S, text.size)
+            rd = min(hi + lmax - 1, text.size)
+            parts.append(dev_scan(ctx, torch_cuda, trie, text[lo:rd], glop.PFAC_FILTERED, own=hi - lo, base=lo))
+        assert np.concatenate(parts).tobytes() == whole.tobytes()
+
+
+def test_unaligned_text(ctx, torch_cuda):
+    text = glop.gen_syslog_host(1 << 20, seed=8)
+    pats, _ = glop.gen_rules(100, seed=2)
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    for off in (1, 3, 7, 13):
+        ref = O.pfac_scan(text[off:], O.Trie(pats, 8))
+        for kernel in KERNELS:
+            assert dev_scan(ctx, torch_cuda, trie, text, kernel, offset=off).tobytes() == ref.tobytes()
+
+
+def test_hit_dense_fallback(ctx):
+    """More hits than a tile's shared-memory buffer: exact global fallback."""
+    text = b"A" * 100000 + b"B" + b"A" * 5000
+    pats = [b"A", b"AA", b"AAA", b"AB"]
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    ref = O.pfac_scan(text, O.Trie(pats, 8))
+    assert ctx.pfac_scan(trie, text).tobytes() == ref.tobytes()
+    offs, cmp_ = ctx.kmp_search(b"AA", text)
+    r_offs, r_cmp = O.kmp_search(text, b"AA")
+    assert np.array_equal(offs, r_offs) and cmp_ == r_cmp
+
+
+def test_kmp_large(ctx, torch_cuda):
+    n = 32 << 20
+    text = glop.gen_syslog_host(n, seed=21)
+    for p in (b"Failed password", b"session opened for user root", b"x"):
+        offs, cmp_ = ctx.kmp_search(p, text)
+        r_offs, r_cmp = O.kmp_search(text, p)
+        assert np.array_equal(offs, r_offs) and cmp_ == r_cmp
+
+
+def test_verify_unsorted_and_counts(ctx):
+    text = b"xxGETPASSWORDFILExxGETPASSWxx root"
+    pats = [b"GETPASSWORDFILE", b"root"]
+    rules = ctx.upload_rules(pats, 8)
+    hits = np.array([(30, 1, 4), (2, 0, 8), (19, 0, 8)], dtype=glop.HIT_DTYPE)
+    alerts, counts = ctx.verify_hits(rules, text, hits, counts=True)
+    assert [(int(a["offset"]), int(a["rule_id"])) for a in alerts] == [(2, 0), (30, 1)]
+    assert list(counts) == [1, 1]
+
+
+def test_dropin_cpp_binary():
+    """The reference's C++ call sites compiled against include/logtrawl."""
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
+    if not os.path.exists(exe):
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
