@@ -97,10 +97,12 @@ glop_status glop_trie_upload(glop_ctx* ctx, const int32_t* dense_table, uint32_t
 glop_status glop_trie_destroy(glop_trie* trie);
 /* Introspection for tests: state count, alphabet classes, min/max output
  * depth, filter q-gram length and stride, table bytes, whether the table is
- * staged in shared memory by the filtered kernel. */
+ * staged in shared memory by the filtered kernel, the jump-table depth J and
+ * slot count and whether it is staged in shared memory. */
 typedef struct {
   uint32_t state_count, classes, min_depth, max_depth, q, stride, entry_bytes, table_in_smem;
   uint64_t table_bytes;
+  uint32_t jump_depth, jump_in_smem, jump_slots, reserved;
 } glop_trie_info;
 glop_status glop_trie_get_info(const glop_trie* trie, glop_trie_info* info);
 

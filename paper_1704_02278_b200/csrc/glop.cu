@@ -99,7 +99,7 @@ struct glop_trie {
   glop_trie_info info{};
   bool empty = true;      // no outputs: every scan is empty
   bool u16 = true;
-  bool smem_filter = false, smem_direct = false;
+  bool smem_filter = false, smem_direct = false, smem_jump = false;
   uint32_t max_pid = 0;
 };
 
@@ -129,13 +129,12 @@ glop_status sync_read(glop_ctx* c, const void* d_src, size_t bytes) {
 }
 
 // -------------------------------------------------------------- kernel launch
-template <bool F, bool S, typename E>
-glop_status launch_pfac_t(glop_ctx* c, int grid, size_t smem, const DevTrie& tr,
-                          const ScanParams& p) {
-  auto k = pfac_tile_kernel<F, S, E>;
+template <typename K>
+glop_status launch_timed(glop_ctx* c, K k, int grid, size_t smem, const DevTrie& tr, const ScanParams& p,
+                         const PfacLayout& L) {
   CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CU(cudaEventRecord(c->ev0, c->stream));
-  k<<<grid, kThreads, smem, c->stream>>>(tr, p);
+  k<<<grid, kThreads, smem, c->stream>>>(tr, p, L);
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;
@@ -143,21 +142,26 @@ glop_status launch_pfac_t(glop_ctx* c, int grid, size_t smem, const DevTrie& tr,
   return GLOP_OK;
 }
 
-glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p) {
-  const bool smem_table = filter ? t->smem_filter : t->smem_direct;
-  const size_t smem = PfacSmem::total(filter, smem_table ? t->view.table_bytes : 0);
-  const int grid = (int)std::min<uint32_t>(p.num_tiles, (uint32_t)c->num_sms);
+template <typename E>
+glop_status launch_pfac_e(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p, int grid) {
   const DevTrie& tr = t->view;
-  if (t->u16) {
-    if (filter) return smem_table ? launch_pfac_t<true, true, uint16_t>(c, grid, smem, tr, p)
-                                  : launch_pfac_t<true, false, uint16_t>(c, grid, smem, tr, p);
-    return smem_table ? launch_pfac_t<false, true, uint16_t>(c, grid, smem, tr, p)
-                      : launch_pfac_t<false, false, uint16_t>(c, grid, smem, tr, p);
+  if (!filter) {
+    const bool st = t->smem_direct;
+    const PfacLayout L = make_pfac_layout(false, false, 0, st ? tr.table_bytes : 0);
+    return st ? launch_timed(c, pfac_direct_kernel<true, E>, grid, L.total, tr, p, L)
+              : launch_timed(c, pfac_direct_kernel<false, E>, grid, L.total, tr, p, L);
   }
-  if (filter) return smem_table ? launch_pfac_t<true, true, uint32_t>(c, grid, smem, tr, p)
-                                : launch_pfac_t<true, false, uint32_t>(c, grid, smem, tr, p);
-  return smem_table ? launch_pfac_t<false, true, uint32_t>(c, grid, smem, tr, p)
-                    : launch_pfac_t<false, false, uint32_t>(c, grid, smem, tr, p);
+  const bool sh = t->smem_jump, st = t->smem_filter;
+  const PfacLayout L = make_pfac_layout(true, !sh, sh ? tr.jump_bytes : 0, st ? tr.table_bytes : 0);
+  if (sh) return st ? launch_timed(c, pfac_filtered_kernel<true, true, E>, grid, L.total, tr, p, L)
+                    : launch_timed(c, pfac_filtered_kernel<false, true, E>, grid, L.total, tr, p, L);
+  return st ? launch_timed(c, pfac_filtered_kernel<true, false, E>, grid, L.total, tr, p, L)
+            : launch_timed(c, pfac_filtered_kernel<false, false, E>, grid, L.total, tr, p, L);
+}
+
+glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p) {
+  const int grid = (int)std::min<uint32_t>(p.num_tiles, (uint32_t)c->num_sms);
+  return t->u16 ? launch_pfac_e<uint16_t>(c, t, filter, p, grid) : launch_pfac_e<uint32_t>(c, t, filter, p, grid);
 }
 
 glop_status radix_sort_keys(glop_ctx* c, unsigned long long* in, unsigned long long* out,
@@ -596,60 +600,79 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         memcpy(&table[idx * 4], &e, 4);
       }
     }
-  // --- filter tables: every root path of length lmin
+  // --- filter tables: root paths of length lmin (q-gram d-mask) and of
+  // length J = min(lmin, 8) (jump table + level-2 bitmap)
   const uint32_t q = lmin ? std::min<uint32_t>(4, lmin) : 1;
   const uint32_t stride = lmin ? std::min<uint32_t>(lmin - q + 1, 8) : 1;
+  const uint32_t J = lmin ? std::min<uint32_t>(lmin, 8) : 1;
   std::vector<uint8_t> dmask(kDmaskBytes, 0);
   std::vector<uint32_t> bm2(kBm2Bits / 32, 0);
-  if (lmin) {
-    struct Item {
-      uint32_t s, d;
-    };
-    std::vector<Item> stack{{0, 0}};
-    std::vector<uint8_t> path(lmin);
-    // iterative DFS carrying the path bytes
-    std::vector<int> next_b(lmin + 1, 0);
-    std::vector<uint32_t> st(lmin + 1, 0);
+  // visits every root path of length `depth`: cb(path bytes, end state)
+  auto for_paths = [&](uint32_t depth, auto&& cb) {
+    std::vector<uint8_t> path(depth + 1);
+    std::vector<uint32_t> st(depth + 1, 0);
+    std::vector<int> nb(depth + 1, 0);
     int d = 0;
-    st[0] = 0;
-    next_b[0] = 0;
     while (d >= 0) {
-      if ((uint32_t)d == lmin) {
-        for (uint32_t k = 0; k < stride; ++k) {
-          uint32_t g = 0;
-          for (uint32_t x = 0; x < q; ++x) g |= (uint32_t)path[k + x] << (8 * x);
-          dmask[qgram_bucket(g, q)] |= (uint8_t)(1u << k);
-        }
-        unsigned long long key = 0;
-        for (uint32_t x = 0; x < std::min<uint32_t>(lmin, 8); ++x)
-          key |= (unsigned long long)path[x] << (8 * x);
-        const uint32_t bit = prefix_bit(key);
-        bm2[bit >> 5] |= 1u << (bit & 31);
+      if ((uint32_t)d == depth) {
+        cb(path.data(), st[d]);
         --d;
         continue;
       }
       bool pushed = false;
-      while (next_b[d] < 256) {
-        const int b = next_b[d]++;
-        const int32_t t = dense[(size_t)st[d] * 256 + b];
-        if (t < 0) continue;
+      while (nb[d] < 256) {
+        const int b = nb[d]++;
+        const int32_t tt = dense[(size_t)st[d] * 256 + b];
+        if (tt < 0) continue;
         path[d] = (uint8_t)b;
-        st[d + 1] = (uint32_t)t;
-        next_b[d + 1] = 0;
+        st[d + 1] = (uint32_t)tt;
+        nb[d + 1] = 0;
         ++d;
         pushed = true;
         break;
       }
       if (!pushed) --d;
     }
+  };
+  std::vector<JumpEntry> jump;
+  uint32_t cap_log2 = 6;
+  if (lmin) {
+    for_paths(lmin, [&](const uint8_t* path, uint32_t) {
+      for (uint32_t k = 0; k < stride; ++k) {
+        uint32_t g = 0;
+        for (uint32_t x = 0; x < q; ++x) g |= (uint32_t)path[k + x] << (8 * x);
+        dmask[qgram_bucket(g, q)] |= (uint8_t)(1u << k);
+      }
+    });
+    std::vector<std::pair<unsigned long long, uint32_t>> keys;
+    for_paths(J, [&](const uint8_t* path, uint32_t s) {
+      unsigned long long key = 0;
+      for (uint32_t x = 0; x < J; ++x) key |= (unsigned long long)path[x] << (8 * x);
+      keys.push_back({key, s});
+      const uint32_t bit = prefix_bit(key);
+      bm2[bit >> 5] |= 1u << (bit & 31);
+    });
+    while ((1ull << cap_log2) < 2 * keys.size()) ++cap_log2;
+    jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
+    const uint32_t mask = (1u << cap_log2) - 1;
+    for (const auto& [key, s] : keys) {
+      uint32_t h = jump_slot(key, cap_log2);
+      while (jump[h].state1) h = (h + 1) & mask;
+      const uint32_t no = off2[s + 1] - off2[s];
+      jump[h] = JumpEntry{key, s + 1, no == 0 ? kOutNone : (no == 1 ? pid2[off2[s]] : kOutMany)};
+    }
+  } else {
+    jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
   }
+  const size_t jump_bytes = jump.size() * sizeof(JumpEntry);
   // --- one device allocation
   const size_t o_cls = 0, o_table = 256, o_off = o_table + table_bytes;
   const size_t o_pid = o_off + up16((size_t)(Q + 1) * 4);
   const size_t o_plen = o_pid + up16(std::max<size_t>(pid2.size(), 1) * 4);
   const size_t o_dmask = o_plen + up16(pid_len.size() * 4);
   const size_t o_bm2 = o_dmask + kDmaskBytes;
-  const size_t total = o_bm2 + kBm2Bytes;
+  const size_t o_jump = o_bm2 + kBm2Bytes;
+  const size_t total = o_jump + jump_bytes;
   std::vector<uint8_t> host(total, 0);
   memcpy(&host[o_cls], cls, 256);
   memcpy(&host[o_table], table.data(), table_bytes);
@@ -658,6 +681,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   memcpy(&host[o_plen], pid_len.data(), pid_len.size() * 4);
   memcpy(&host[o_dmask], dmask.data(), kDmaskBytes);
   memcpy(&host[o_bm2], bm2.data(), kBm2Bytes);
+  memcpy(&host[o_jump], jump.data(), jump_bytes);
   Dev g(c->device);
   void* mem = nullptr;
   CU(cudaMalloc(&mem, total));
@@ -677,6 +701,10 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.pid_len = reinterpret_cast<const uint32_t*>(m + o_plen);
   t->view.dmask = m + o_dmask;
   t->view.bm2 = reinterpret_cast<const uint32_t*>(m + o_bm2);
+  t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
+  t->view.jump_depth = J;
+  t->view.jump_cap_log2 = cap_log2;
+  t->view.jump_bytes = (uint32_t)jump_bytes;
   t->view.Q = Q;
   t->view.C = C;
   t->view.lmin = lmin;
@@ -688,10 +716,14 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->u16 = u16;
   t->max_pid = max_pid;
   const size_t cap = std::min<size_t>(kSmemMax, c->smem_optin ? c->smem_optin : kSmemMax);
-  t->smem_filter = PfacSmem::total(true, table_bytes) <= cap;
-  t->smem_direct = PfacSmem::total(false, table_bytes) <= cap;
+  // shared-memory placement, most valuable first: jump table, then the
+  // transition table (filtered kernel); transition table (direct kernel)
+  t->smem_jump = make_pfac_layout(true, false, (uint32_t)jump_bytes, 0).total <= cap;
+  t->smem_filter = make_pfac_layout(true, !t->smem_jump, t->smem_jump ? (uint32_t)jump_bytes : 0,
+                                    (uint32_t)table_bytes).total <= cap;
+  t->smem_direct = make_pfac_layout(false, false, 0, (uint32_t)table_bytes).total <= cap;
   t->info = glop_trie_info{Q, C, lmin, lmax, q, stride, (uint32_t)eb, t->smem_filter ? 1u : 0u,
-                           (uint64_t)table_bytes};
+                           (uint64_t)table_bytes, J, t->smem_jump ? 1u : 0u, (uint32_t)jump.size(), 0u};
   *out = t;
   return GLOP_OK;
 }

@@ -31,6 +31,7 @@ constexpr uint32_t kHitCap = 2048;          // per-tile hit keys in smem
 constexpr uint32_t kDmaskBytes = 65536;     // level-1 q-gram d-mask buckets
 constexpr uint32_t kBm2Bits = 1u << 18;     // level-2 prefix bitmap
 constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
+constexpr uint32_t kQueueCap = 4096;        // per-tile filter survivors
 
 struct TileDir {
   unsigned long long slot;
@@ -38,6 +39,7 @@ struct TileDir {
   uint32_t overflow;
 };
 
+struct JumpEntry;
 struct DevTrie {
   const uint8_t* cls;       // 256 byte -> class
   const void* table;        // Q x C entries, 0 = no edge
@@ -46,8 +48,10 @@ struct DevTrie {
   const uint32_t* pid_len;  // pattern id -> matched_len
   const uint8_t* dmask;     // kDmaskBytes
   const uint32_t* bm2;      // kBm2Bits / 32 words
+  const JumpEntry* jump;    // open-addressed J-byte jump table
   uint32_t Q, C, lmin, lmax, q, stride;
   uint32_t table_bytes;     // padded to 16
+  uint32_t jump_depth, jump_cap_log2, jump_bytes;
 };
 
 struct ScanParams {
@@ -214,182 +218,305 @@ __device__ __forceinline__ void sort_keys(unsigned long long* keys, uint32_t P) 
 }
 
 // ------------------------------------------------------------------ K1 PFAC
-struct PfacSmem {
-  // byte offsets inside dynamic shared memory
-  static constexpr uint32_t kBars = kStages * kStageBytes;
-  static constexpr uint32_t kCls = kBars + kStages * 8;
-  static constexpr uint32_t kMisc = kCls + 256;          // 16 bytes
-  static constexpr uint32_t kKeys = kMisc + 16;          // kHitCap * 8
-  static constexpr uint32_t kEnd = kKeys + kHitCap * 8;  // then filter, then table
-  static __host__ __device__ uint32_t dmask(bool filter) { return kEnd; }
-  static __host__ __device__ uint32_t bm2(bool filter) { return kEnd + (filter ? kDmaskBytes : 0); }
-  static __host__ __device__ uint32_t table(bool filter) {
-    return kEnd + (filter ? kDmaskBytes + kBm2Bytes : 0);
+// Shared-memory layout (byte offsets), computed on the host per automaton.
+struct PfacLayout {
+  uint32_t bars, cls, misc, keys, queue, dmask, bm2, hash, table, total;
+};
+
+__host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// filter: q-gram d-mask + candidate queue; bm2: level-2 bitmap (only when
+// the jump hash lives in global memory); hash_bytes / table_bytes: 0 when
+// that structure stays in global memory (L2-resident).
+__host__ __device__ inline PfacLayout make_pfac_layout(bool filter, bool bm2, uint32_t hash_bytes,
+                                                        uint32_t table_bytes) {
+  PfacLayout L;
+  uint32_t o = kStages * kStageBytes;
+  L.bars = o; o += kStages * 8;
+  L.cls = o; o += 256;
+  L.misc = o; o += 16;
+  L.keys = o; o += kHitCap * 8;
+  L.queue = o; o += filter ? kQueueCap * 4 : 0;
+  L.dmask = o; o += filter ? kDmaskBytes : 0;
+  L.bm2 = o; o += (filter && bm2) ? kBm2Bytes : 0;
+  o = align16(o);
+  L.hash = o; o += filter ? hash_bytes : 0;
+  o = align16(o);
+  L.table = o; o += table_bytes;
+  L.total = o;
+  return L;
+}
+
+// Jump-table entry: the trie state reached by a J-byte root path
+// (J = min(lmin, 8)), generalising the reference's depth-1/depth-2 RootJump
+// (scan.hpp:81-108) to J levels.  state+1 in `state1` (0 = empty slot); `out`
+// is the single output pattern id of that state, kOutNone or kOutMany.
+struct JumpEntry {
+  unsigned long long key;
+  uint32_t state1;
+  uint32_t out;
+};
+constexpr uint32_t kOutNone = 0xFFFFFFFFu, kOutMany = 0xFFFFFFFEu;
+
+__host__ __device__ __forceinline__ uint32_t jump_slot(unsigned long long key, uint32_t cap_log2) {
+  return (uint32_t)((key * 0xD6E8FEB86659FD93ull) >> (64 - cap_log2));
+}
+
+// Per-CTA tile machinery shared by the filtered and direct kernels.
+struct TileCtx {
+  const DevTrie& tr;
+  const ScanParams& p;
+  const uint8_t* win;
+  uint8_t* s_cls;
+  uint32_t* s_misc;
+  unsigned long long* s_keys;
+  unsigned long long t0, t1;
+  uint32_t wofs;
+
+  __device__ __forceinline__ uint32_t tbyte(unsigned long long x) const {
+    const unsigned long long li = x - t0 + wofs;
+    return li < kStageBytes ? win[li] : __ldg(p.text + x);
   }
-  static __host__ __device__ uint32_t total(bool filter, uint32_t table_bytes) {
-    return table(filter) + table_bytes;
+  __device__ __forceinline__ void emit_pid(unsigned long long i, uint32_t pid) const {
+    if (p.mode == 0) {
+      const uint32_t slot = atomicAdd(&s_misc[0], 1u);
+      if (slot < kHitCap) s_keys[slot] = ((i - t0) << 40) | pid;
+    } else {
+      const unsigned long long slot = atomicAdd(p.g_count, 1ull);
+      if (slot < p.keys_cap) p.keys[slot] = ((p.base + i) << 24) | pid;
+    }
+  }
+  __device__ __forceinline__ void emit_state(unsigned long long i, uint32_t st) const {
+    for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o)
+      emit_pid(i, __ldg(tr.out_pid + o));
+  }
+  // PFAC walk (scan.hpp:142-168) from state st at text position j (the walk
+  // started at i): every visited output state emits; stop at a missing edge
+  // or the end of text.
+  template <bool kSmemTable, typename Entry>
+  __device__ __forceinline__ void walk(const Entry* T, unsigned long long i, uint32_t st,
+                                       unsigned long long j) const {
+    using ET = EntryTraits<Entry>;
+    for (; j < p.n; ++j) {
+      const uint32_t c = s_cls[tbyte(j)];
+      const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
+      if (!e) break;
+      st = e & ET::kMask;
+      if (e & ET::kFlag) emit_state(i, st);
+    }
   }
 };
 
-template <bool kFilter, bool kSmemTable, typename Entry>
-__global__ void __launch_bounds__(kThreads, 1) pfac_tile_kernel(const DevTrie tr, const ScanParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  using ET = EntryTraits<Entry>;
+// Loads the automaton pieces a kernel keeps in shared memory.
+__device__ __forceinline__ void stage_tables(uint8_t* smem, const PfacLayout& L, const DevTrie& tr, bool filter,
+                                             bool bm2, uint32_t hash_bytes, uint32_t table_bytes) {
   const int tid = threadIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PfacSmem::kBars);
-  uint8_t* s_cls = smem + PfacSmem::kCls;
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + PfacSmem::kMisc);
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + PfacSmem::kKeys);
-  uint8_t* s_dmask = smem + PfacSmem::dmask(kFilter);
-  uint32_t* s_bm2 = reinterpret_cast<uint32_t*>(smem + PfacSmem::bm2(kFilter));
-  Entry* s_table = reinterpret_cast<Entry*>(smem + PfacSmem::table(kFilter));
+  if (tid < 16) reinterpret_cast<uint4*>(smem + L.cls)[tid] = reinterpret_cast<const uint4*>(tr.cls)[tid];
+  auto copy = [&](uint32_t off, const void* src, uint32_t bytes) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(smem + off);
+    for (uint32_t i = tid; i < bytes / 16; i += kThreads) d[i] = s[i];
+  };
+  if (filter) copy(L.dmask, tr.dmask, kDmaskBytes);
+  if (bm2) copy(L.bm2, tr.bm2, kBm2Bytes);
+  if (hash_bytes) copy(L.hash, tr.jump, hash_bytes);
+  if (table_bytes) copy(L.table, tr.table, table_bytes);
+}
 
-  // ---- one-time staging of the automaton into shared memory
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(tr.cls);
-    if (tid < 16) reinterpret_cast<uint4*>(s_cls)[tid] = src[tid];
-    if (kFilter) {
-      const uint4* d = reinterpret_cast<const uint4*>(tr.dmask);
-      for (uint32_t i = tid; i < kDmaskBytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_dmask)[i] = d[i];
-      const uint4* b = reinterpret_cast<const uint4*>(tr.bm2);
-      for (uint32_t i = tid; i < kBm2Bytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_bm2)[i] = b[i];
-    }
-    if (kSmemTable) {
-      const uint4* t = reinterpret_cast<const uint4*>(tr.table);
-      for (uint32_t i = tid; i < tr.table_bytes / 16; i += kThreads) reinterpret_cast<uint4*>(s_table)[i] = t[i];
-    }
-    if (tid == 0) {
-      for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-      s_misc[0] = 0;
-      fence_mbar_init();
+// Per-tile epilogue: order the tile's hit keys, reserve a staging slot,
+// write glop_hit records, record the tile directory entry (mode 0).
+__device__ __forceinline__ void tile_epilogue(const TileCtx& tc, uint32_t t) {
+  const int tid = threadIdx.x;
+  const ScanParams& p = tc.p;
+  const uint32_t nh = tc.s_misc[0];
+  const bool over = nh > kHitCap;
+  if (!over && nh > 1) {
+    uint32_t P = 1;
+    while (P < nh) P <<= 1;
+    for (uint32_t x = nh + tid; x < P; x += kThreads) tc.s_keys[x] = ~0ull;
+    __syncthreads();
+    sort_keys(tc.s_keys, P);
+  }
+  if (tid == 0) {
+    const unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
+    p.dir[t].slot = slot;
+    p.dir[t].count = nh;
+    p.dir[t].overflow = over;
+    if (over) atomicOr(p.g_flags, 1u);
+    tc.s_misc[1] = (uint32_t)slot;
+    tc.s_misc[2] = (uint32_t)(slot >> 32);
+  }
+  __syncthreads();
+  const unsigned long long slot = (unsigned long long)tc.s_misc[1] | ((unsigned long long)tc.s_misc[2] << 32);
+  if (!over && slot + nh <= p.staging_cap) {
+    for (uint32_t h = tid; h < nh; h += kThreads) {
+      const unsigned long long key = tc.s_keys[h];
+      const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
+      DevHit out;
+      out.offset = p.base + tc.t0 + (key >> 40);
+      out.pid = pid;
+      out.len = __ldg(tc.tr.pid_len + pid);
+      p.staging[slot + h] = out;
     }
   }
   __syncthreads();
+  if (tid == 0) tc.s_misc[0] = 0;
+}
 
-  const Entry* T = kSmemTable ? s_table : reinterpret_cast<const Entry*>(tr.table);
+// K1 (FILTERED).  Phase A samples every stride-th position and tests its
+// q-gram against the d-mask (bit d set <=> some entry has this q-gram at
+// offset d); survivors are queued.  Phase B takes queued candidates
+// i = P - d, probes the J-byte jump hash (exact), emits the jump state's
+// outputs and walks the remaining levels.  Phase C orders and writes hits.
+template <bool kSmemTable, bool kSmemHash, typename Entry>
+__global__ void __launch_bounds__(kThreads, 1) pfac_filtered_kernel(const DevTrie tr, const ScanParams p,
+                                                                     const PfacLayout L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
+  uint32_t* s_queue = reinterpret_cast<uint32_t*>(smem + L.queue);
+  const uint8_t* s_dmask = smem + L.dmask;
+  const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
+  const JumpEntry* H = kSmemHash ? reinterpret_cast<const JumpEntry*>(smem + L.hash) : tr.jump;
+  const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
+  stage_tables(smem, L, tr, true, !kSmemHash, kSmemHash ? tr.jump_bytes : 0, kSmemTable ? tr.table_bytes : 0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    s_misc[0] = 0;
+    s_misc[3] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
   Ring ring{smem, bars, p.text - ((uintptr_t)p.text & 15), (uint32_t)((uintptr_t)p.text & 15), p.n};
   if (tid == 0)
     for (int k = 0; k < kStages; ++k) {
-      uint32_t t = blockIdx.x + k * gridDim.x;
+      const uint32_t t = blockIdx.x + k * gridDim.x;
       if (t < p.num_tiles) ring.issue(k, t);
     }
+  const uint32_t q = tr.q, S = tr.stride, lmin = tr.lmin, J = tr.jump_depth, cap_log2 = tr.jump_cap_log2;
+  const uint32_t qmask = q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * q)) - 1);
+  const unsigned long long jmask = low_bytes_mask(J);
 
   for (uint32_t k = 0;; ++k) {
     const uint32_t t = blockIdx.x + k * gridDim.x;
     if (t >= p.num_tiles) break;
     const int stage = k % kStages;
     mbar_wait(&bars[stage], (k / kStages) & 1);
-    const uint8_t* win = ring.stages + (size_t)stage * kStageBytes;
-    const unsigned long long t0 = (unsigned long long)t * kTile;
-    const unsigned long long t1 = t0 + kTile < p.own ? t0 + kTile : p.own;
-    const uint32_t wofs = ring.a;  // win index of text position t0
+    TileCtx tc{tr, p, ring.stages + (size_t)stage * kStageBytes, smem + L.cls, s_misc,
+               reinterpret_cast<unsigned long long*>(smem + L.keys), (unsigned long long)t * kTile, 0, ring.a};
+    tc.t1 = tc.t0 + kTile < p.own ? tc.t0 + kTile : p.own;
+    const unsigned long long t0 = tc.t0, t1 = tc.t1;
 
-    // byte of text position x (t0 <= x < n)
-    auto tbyte = [&](unsigned long long x) -> uint32_t {
-      unsigned long long li = x - t0 + wofs;
-      return li < kStageBytes ? win[li] : __ldg(p.text + x);
-    };
-    auto emit = [&](unsigned long long i, uint32_t st) {
-      for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o) {
-        const uint32_t pid = __ldg(tr.out_pid + o);
-        if (p.mode == 0) {
-          uint32_t slot = atomicAdd(&s_misc[0], 1u);
-          if (slot < kHitCap) s_keys[slot] = ((i - t0) << 40) | pid;
-        } else {
-          unsigned long long slot = atomicAdd(p.g_count, 1ull);
-          if (slot < p.keys_cap) p.keys[slot] = ((p.base + i) << 24) | pid;
+    // exact check of candidate start i (t0 <= i < t1, i + lmin <= n)
+    auto candidate = [&](unsigned long long i) {
+      const unsigned long long key = win_u64(tc.win, (uint32_t)(i - t0) + tc.wofs) & jmask;
+      if (!kSmemHash) {
+        const uint32_t b = prefix_bit(key);
+        if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
+      }
+      const uint32_t mask = (1u << cap_log2) - 1;
+      for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & mask) {
+        const JumpEntry e = H[h];
+        if (!e.state1) return;
+        if (e.key != key) continue;
+        const uint32_t st = e.state1 - 1;
+        if (e.out != kOutNone) {
+          if (e.out == kOutMany) tc.emit_state(i, st);
+          else tc.emit_pid(i, e.out);
         }
+        if (tr.lmax > J) tc.template walk<kSmemTable>(T, i, st, i + J);
+        return;
       }
     };
-    // PFAC walk from start i (scan.hpp:125-169): every visited output state
-    // emits; stop at a missing edge or the end of text.
-    auto walk = [&](unsigned long long i) {
-      uint32_t st = 0;
-      for (unsigned long long j = i; j < p.n; ++j) {
-        const uint32_t c = s_cls[tbyte(j)];
-        const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
-        if (!e) break;
-        st = e & ET::kMask;
-        if (e & ET::kFlag) emit(i, st);
+    auto expand = [&](unsigned long long P, uint32_t dm) {
+      while (dm) {
+        const uint32_t d = __ffs(dm) - 1;
+        dm &= dm - 1;
+        if (P < t0 + d) continue;
+        const unsigned long long i = P - d;
+        if (i >= t1 || i + lmin > p.n) continue;
+        candidate(i);
       }
     };
 
-    if (kFilter) {
-      // Sampled q-gram filter.  Every occurrence of an entry (length >= lmin)
-      // starting at i covers [i, i+lmin); the sampled position P = the
-      // multiple of `stride` in [i, i+stride) satisfies P - i = d <= lmin - q,
-      // so the q-gram at P is the entry's q-gram at offset d, recorded in
-      // dmask[bucket] bit d.  Candidates i = P - d then pass an 8-byte prefix
-      // bitmap before the exact walk.
-      const uint32_t q = tr.q, S = tr.stride, lmin = tr.lmin;
-      const uint32_t qmask = q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * q)) - 1);
-      const unsigned long long kmask = low_bytes_mask(lmin < 8 ? lmin : 8);
-      const unsigned long long pfirst = ((t0 + S - 1) / S) * S;
-      const unsigned long long pend = t1 + S - 1;  // exclusive
-      const uint32_t M = pend > pfirst ? (uint32_t)((pend - pfirst + S - 1) / S) : 0;
-      for (uint32_t m = tid; m < M; m += kThreads) {
-        const unsigned long long P = pfirst + (unsigned long long)m * S;
-        if (P + q > p.n) continue;
-        const uint32_t g = win_u32(win, (uint32_t)(P - t0) + wofs) & qmask;
-        uint32_t dm = s_dmask[qgram_bucket(g, q)];
-        while (dm) {
-          const uint32_t d = __ffs(dm) - 1;
-          dm &= dm - 1;
-          if (P < t0 + d) continue;
-          const unsigned long long i = P - d;
-          if (i >= t1 || i + lmin > p.n) continue;
-          const unsigned long long key = win_u64(win, (uint32_t)(i - t0) + wofs) & kmask;
-          const uint32_t b = prefix_bit(key);
-          if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) continue;
-          walk(i);
-        }
+    // Phase A: sampled q-grams (tile-anchored: P = t0 + m*S covers every
+    // start in [t0, t1) with some P - d, 0 <= d < S)
+    const uint32_t M = (uint32_t)((t1 - t0 + S - 1) / S);
+    for (uint32_t m = tid; m < M; m += kThreads) {
+      const unsigned long long P = t0 + (unsigned long long)m * S;
+      if (P + q > p.n) continue;
+      const uint32_t g = win_u32(tc.win, (uint32_t)(P - t0) + tc.wofs) & qmask;
+      const uint32_t dm = s_dmask[qgram_bucket(g, q)];
+      if (dm) {
+        const uint32_t slot = atomicAdd(&s_misc[3], 1u);
+        if (slot < kQueueCap) s_queue[slot] = (m << 8) | dm;
+        else expand(P, dm);  // queue full: exact inline path
       }
-    } else {
-      for (unsigned long long i = t0 + tid; i < t1; i += kThreads) walk(i);
     }
-    __syncthreads();  // stage consumed; hit keys complete
+    __syncthreads();
+    // Phase B: queued candidates, one queue entry per thread
+    const uint32_t nq = min(s_misc[3], kQueueCap);
+    for (uint32_t e = tid; e < nq; e += kThreads) {
+      const uint32_t v = s_queue[e];
+      expand(t0 + (unsigned long long)(v >> 8) * S, v & 0xFFu);
+    }
+    __syncthreads();  // stage consumed, hit keys complete
     if (tid == 0) {
-      uint32_t tn = t + kStages * gridDim.x;
+      s_misc[3] = 0;
+      const uint32_t tn = t + kStages * gridDim.x;
       if (tn < p.num_tiles) {
         fence_proxy_async();
         ring.issue(stage, tn);
       }
     }
-    if (p.mode == 0) {
-      const uint32_t nh = s_misc[0];
-      const bool over = nh > kHitCap;
-      if (!over && nh > 1) {
-        uint32_t P = 1;
-        while (P < nh) P <<= 1;
-        for (uint32_t x = nh + tid; x < P; x += kThreads) s_keys[x] = ~0ull;
-        __syncthreads();
-        sort_keys(s_keys, P);
-      }
-      if (tid == 0) {
-        unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
-        p.dir[t].slot = slot;
-        p.dir[t].count = nh;
-        p.dir[t].overflow = over;
-        if (over) atomicOr(p.g_flags, 1u);
-        s_misc[1] = (uint32_t)slot;
-        s_misc[2] = (uint32_t)(slot >> 32);
-      }
-      __syncthreads();
-      const unsigned long long slot = (unsigned long long)s_misc[1] | ((unsigned long long)s_misc[2] << 32);
-      if (!over && slot + nh <= p.staging_cap) {
-        for (uint32_t h = tid; h < nh; h += kThreads) {
-          const unsigned long long key = s_keys[h];
-          const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
-          DevHit out;
-          out.offset = p.base + t0 + (key >> 40);
-          out.pid = pid;
-          out.len = __ldg(tr.pid_len + pid);
-          p.staging[slot + h] = out;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) s_misc[0] = 0;
+    if (p.mode == 0) tile_epilogue(tc, t);
+    __syncthreads();
+  }
+}
+
+// K1 (DIRECT): the literal one-thread-per-start-byte PFAC walk
+// (scan.hpp:113-170) over the alphabet-compressed table.
+template <bool kSmemTable, typename Entry>
+__global__ void __launch_bounds__(kThreads, 1) pfac_direct_kernel(const DevTrie tr, const ScanParams p,
+                                                                   const PfacLayout L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
+  const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
+  stage_tables(smem, L, tr, false, false, 0, kSmemTable ? tr.table_bytes : 0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    s_misc[0] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  Ring ring{smem, bars, p.text - ((uintptr_t)p.text & 15), (uint32_t)((uintptr_t)p.text & 15), p.n};
+  if (tid == 0)
+    for (int k = 0; k < kStages; ++k) {
+      const uint32_t t = blockIdx.x + k * gridDim.x;
+      if (t < p.num_tiles) ring.issue(k, t);
     }
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t t = blockIdx.x + k * gridDim.x;
+    if (t >= p.num_tiles) break;
+    const int stage = k % kStages;
+    mbar_wait(&bars[stage], (k / kStages) & 1);
+    TileCtx tc{tr, p, ring.stages + (size_t)stage * kStageBytes, smem + L.cls, s_misc,
+               reinterpret_cast<unsigned long long*>(smem + L.keys), (unsigned long long)t * kTile, 0, ring.a};
+    tc.t1 = tc.t0 + kTile < p.own ? tc.t0 + kTile : p.own;
+    for (unsigned long long i = tc.t0 + tid; i < tc.t1; i += kThreads)
+      tc.template walk<kSmemTable>(T, i, 0u, i);
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t tn = t + kStages * gridDim.x;
+      if (tn < p.num_tiles) {
+        fence_proxy_async();
+        ring.issue(stage, tn);
+      }
+    }
+    if (p.mode == 0) tile_epilogue(tc, t);
     __syncthreads();
   }
 }

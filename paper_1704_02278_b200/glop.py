@@ -62,7 +62,8 @@ i32p = C.POINTER(C.c_int32)
 
 class TrieInfo(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("state_count", "classes", "min_depth", "max_depth", "q", "stride",
-                                          "entry_bytes", "table_in_smem")] + [("table_bytes", C.c_uint64)]
+                                          "entry_bytes", "table_in_smem")] + [("table_bytes", C.c_uint64)] + \
+        [(n, C.c_uint32) for n in ("jump_depth", "jump_in_smem", "jump_slots", "reserved")]
 
 
 def _sig(name, *args):
