@@ -130,11 +130,11 @@ glop_status sync_read(glop_ctx* c, const void* d_src, size_t bytes) {
 
 // -------------------------------------------------------------- kernel launch
 template <typename K>
-glop_status launch_timed(glop_ctx* c, K k, int grid, size_t smem, const DevTrie& tr, const ScanParams& p,
+glop_status launch_timed(glop_ctx* c, K k, int grid, const DevTrie& tr, const WarpScanParams& p,
                          const PfacLayout& L) {
-  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
   CU(cudaEventRecord(c->ev0, c->stream));
-  k<<<grid, kThreads, smem, c->stream>>>(tr, p, L);
+  k<<<grid, kWarpKernelThreads, L.total, c->stream>>>(tr, p, L);
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev1, c->stream));
   c->timed = true;
@@ -143,24 +143,23 @@ glop_status launch_timed(glop_ctx* c, K k, int grid, size_t smem, const DevTrie&
 }
 
 template <typename E>
-glop_status launch_pfac_e(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p, int grid) {
+glop_status launch_pfac_e(glop_ctx* c, const glop_trie* t, bool filter, const WarpScanParams& p, int grid) {
   const DevTrie& tr = t->view;
   if (!filter) {
     const bool st = t->smem_direct;
-    const PfacLayout L = make_pfac_layout(false, false, 0, st ? tr.table_bytes : 0);
-    return st ? launch_timed(c, pfac_direct_kernel<true, E>, grid, L.total, tr, p, L)
-              : launch_timed(c, pfac_direct_kernel<false, E>, grid, L.total, tr, p, L);
+    const PfacLayout L = make_warp_layout(false, 0, st ? tr.table_bytes : 0);
+    return st ? launch_timed(c, pfac_warp_kernel<false, true, false, E>, grid, tr, p, L)
+              : launch_timed(c, pfac_warp_kernel<false, false, false, E>, grid, tr, p, L);
   }
   const bool sh = t->smem_jump, st = t->smem_filter;
-  const PfacLayout L = make_pfac_layout(true, !sh, sh ? tr.jump_bytes : 0, st ? tr.table_bytes : 0);
-  if (sh) return st ? launch_timed(c, pfac_filtered_kernel<true, true, E>, grid, L.total, tr, p, L)
-                    : launch_timed(c, pfac_filtered_kernel<false, true, E>, grid, L.total, tr, p, L);
-  return st ? launch_timed(c, pfac_filtered_kernel<true, false, E>, grid, L.total, tr, p, L)
-            : launch_timed(c, pfac_filtered_kernel<false, false, E>, grid, L.total, tr, p, L);
+  const PfacLayout L = make_warp_layout(true, sh ? tr.jump_bytes : 0, st ? tr.table_bytes : 0);
+  if (sh) return st ? launch_timed(c, pfac_warp_kernel<true, true, true, E>, grid, tr, p, L)
+                    : launch_timed(c, pfac_warp_kernel<true, false, true, E>, grid, tr, p, L);
+  return st ? launch_timed(c, pfac_warp_kernel<true, true, false, E>, grid, tr, p, L)
+            : launch_timed(c, pfac_warp_kernel<true, false, false, E>, grid, tr, p, L);
 }
 
-glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const ScanParams& p) {
-  const int grid = (int)std::min<uint32_t>(p.num_tiles, (uint32_t)c->num_sms);
+glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const WarpScanParams& p, int grid) {
   return t->u16 ? launch_pfac_e<uint16_t>(c, t, filter, p, grid) : launch_pfac_e<uint32_t>(c, t, filter, p, grid);
 }
 
@@ -182,17 +181,23 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   if (own == 0 || t->empty) return GLOP_OK;
   const bool filter = kind != GLOP_PFAC_DIRECT;
   const uint32_t num_tiles = (uint32_t)((own + kTile - 1) / kTile);
-  TRY(c->dir.ensure(sizeof(TileDir) * num_tiles));
-  TRY(c->prefix.ensure(sizeof(unsigned long long) * num_tiles));
+  const unsigned long long nseg = (unsigned long long)num_tiles * kConsumerWarps;
+  const uint32_t nb = (uint32_t)((nseg + kSegPerBlock - 1) / kSegPerBlock);
+  const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
+  const unsigned long long regions = (unsigned long long)grid * kConsumerWarps;
+  TRY(c->dir.ensure(sizeof(SegDir) * nseg));
+  TRY(c->bcounts.ensure(4ull * nb));
+  TRY(c->prefix.ensure(8ull * nb + 8));
   TRY(c->misc.ensure(64));
-  size_t want = std::max<size_t>(1 << 20, own / 512);
-  if (c->staging.bytes < want * sizeof(glop_hit)) TRY(c->staging.ensure(want * sizeof(glop_hit)));
-  auto* g_count = c->misc.as<unsigned long long>();
-  auto* g_flags = reinterpret_cast<unsigned int*>(g_count + 1);
+  unsigned long long region = std::max<unsigned long long>(64, (std::max<uint64_t>(1 << 20, own / 512) + regions - 1) / regions);
+  if (c->staging.bytes < region * regions * sizeof(glop_hit))
+    TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
+  region = c->staging.bytes / sizeof(glop_hit) / regions;
+  auto* g = c->misc.as<unsigned long long>();
 
   for (int attempt = 0; attempt < 3; ++attempt) {
-    CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
-    ScanParams p{};
+    CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+    WarpScanParams p{};
     p.text = d_text;
     p.n = n;
     p.own = own;
@@ -200,30 +205,29 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
     p.num_tiles = num_tiles;
     p.mode = 0;
     p.staging = reinterpret_cast<DevHit*>(c->staging.p);
-    p.staging_cap = c->staging.bytes / sizeof(glop_hit);
-    p.g_count = g_count;
-    p.dir = c->dir.as<TileDir>();
-    p.g_flags = g_flags;
-    TRY(launch_pfac(c, t, filter, p));
-    TRY(sync_read(c, c->misc.p, 16));
-    const unsigned long long total = c->h_misc[0];
+    p.region = region;
+    p.dir = c->dir.as<SegDir>();
+    p.g_count = g;
+    TRY(launch_pfac(c, t, filter, p, grid));
+    TRY(sync_read(c, c->misc.p, 32));
+    const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[2];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
     *n_hits = total;
     if (flags & 1u) {
-      // some tile produced more hits than its shared-memory buffer holds:
+      // a slice produced more hits than its shared-memory buffer holds:
       // exact fallback -- global keys, device radix sort
       if (t->max_pid >= (1u << 24) || base + n >= (1ull << 40))
         return fail(GLOP_ECAPACITY, "pfac_scan: hit density fallback limited to 2^24 ids / 2^40 bytes");
       if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
       TRY(c->keys.ensure(total * 8));
       TRY(c->keys_alt.ensure(total * 8));
-      CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
+      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
       p.mode = 1;
       p.keys = c->keys.as<unsigned long long>();
       p.keys_cap = total;
-      TRY(launch_pfac(c, t, filter, p));
+      TRY(launch_pfac(c, t, filter, p, grid));
       TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), total));
-      c->launches += 2;  // + the mode-1 scan
+      c->launches += 2;
       keys_to_hits_kernel<<<std::max<unsigned long long>(1, std::min<unsigned long long>((total + 255) / 256, 4096)), 256, 0,
                             c->stream>>>(c->keys_alt.as<unsigned long long>(), total, t->view.pid_len,
                                          reinterpret_cast<DevHit*>(d_out));
@@ -231,20 +235,22 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
       CU(cudaStreamSynchronize(c->stream));
       return GLOP_OK;
     }
-    if (total > p.staging_cap) {  // grow and rerun
+    if (maxregion > region) {  // a warp's staging region overflowed: grow, rerun
+      region = maxregion + maxregion / 4 + 64;
       c->staging.release();
-      TRY(c->staging.ensure(total * sizeof(glop_hit) + (1 << 20)));
+      TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
       continue;
     }
     if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
     if (total == 0) return GLOP_OK;
-    ++c->launches;
-    tile_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->dir.as<TileDir>(), num_tiles,
-                                                  c->prefix.as<unsigned long long>());
-    ++c->launches;
-    gather_kernel<DevHit><<<std::min<uint32_t>((num_tiles + 7) / 8, 4 * c->num_sms), 256, 0, c->stream>>>(
-        c->dir.as<TileDir>(), c->prefix.as<unsigned long long>(), num_tiles,
-        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out));
+    c->launches += 3;
+    seg_reduce_kernel<<<nb, 1024, 0, c->stream>>>(c->dir.as<SegDir>(), nseg, c->bcounts.as<uint32_t>());
+    block_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<uint32_t>(), nb, c->prefix.as<unsigned long long>(),
+                                                   c->prefix.as<unsigned long long>() + nb);
+    seg_gather_kernel<DevHit><<<nb, 1024, 0, c->stream>>>(c->dir.as<SegDir>(), nseg, c->prefix.as<unsigned long long>(),
+                                                          (uint32_t)grid, region,
+                                                          reinterpret_cast<const DevHit*>(c->staging.p),
+                                                          reinterpret_cast<DevHit*>(d_out));
     CU(cudaGetLastError());
     return GLOP_OK;
   }
@@ -718,10 +724,9 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   const size_t cap = std::min<size_t>(kSmemMax, c->smem_optin ? c->smem_optin : kSmemMax);
   // shared-memory placement, most valuable first: jump table, then the
   // transition table (filtered kernel); transition table (direct kernel)
-  t->smem_jump = make_pfac_layout(true, false, (uint32_t)jump_bytes, 0).total <= cap;
-  t->smem_filter = make_pfac_layout(true, !t->smem_jump, t->smem_jump ? (uint32_t)jump_bytes : 0,
-                                    (uint32_t)table_bytes).total <= cap;
-  t->smem_direct = make_pfac_layout(false, false, 0, (uint32_t)table_bytes).total <= cap;
+  t->smem_jump = make_warp_layout(true, (uint32_t)jump_bytes, 0).total <= cap;
+  t->smem_filter = make_warp_layout(true, t->smem_jump ? (uint32_t)jump_bytes : 0, (uint32_t)table_bytes).total <= cap;
+  t->smem_direct = make_warp_layout(false, 0, (uint32_t)table_bytes).total <= cap;
   t->info = glop_trie_info{Q, C, lmin, lmax, q, stride, (uint32_t)eb, t->smem_filter ? 1u : 0u,
                            (uint64_t)table_bytes, J, t->smem_jump ? 1u : 0u, (uint32_t)jump.size(), 0u};
   *out = t;

@@ -225,28 +225,6 @@ struct PfacLayout {
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-// filter: q-gram d-mask + candidate queue; bm2: level-2 bitmap (only when
-// the jump hash lives in global memory); hash_bytes / table_bytes: 0 when
-// that structure stays in global memory (L2-resident).
-__host__ __device__ inline PfacLayout make_pfac_layout(bool filter, bool bm2, uint32_t hash_bytes,
-                                                        uint32_t table_bytes) {
-  PfacLayout L;
-  uint32_t o = kStages * kStageBytes;
-  L.bars = o; o += kStages * 8;
-  L.cls = o; o += 256;
-  L.misc = o; o += 16;
-  L.keys = o; o += kHitCap * 8;
-  L.queue = o; o += filter ? kQueueCap * 4 : 0;
-  L.dmask = o; o += filter ? kDmaskBytes : 0;
-  L.bm2 = o; o += (filter && bm2) ? kBm2Bytes : 0;
-  o = align16(o);
-  L.hash = o; o += filter ? hash_bytes : 0;
-  o = align16(o);
-  L.table = o; o += table_bytes;
-  L.total = o;
-  return L;
-}
-
 // Jump-table entry: the trie state reached by a J-byte root path
 // (J = min(lmin, 8)), generalising the reference's depth-1/depth-2 RootJump
 // (scan.hpp:81-108) to J levels.  state+1 in `state1` (0 = empty slot); `out`
@@ -262,262 +240,356 @@ __host__ __device__ __forceinline__ uint32_t jump_slot(unsigned long long key, u
   return (uint32_t)((key * 0xD6E8FEB86659FD93ull) >> (64 - cap_log2));
 }
 
-// Per-CTA tile machinery shared by the filtered and direct kernels.
-struct TileCtx {
-  const DevTrie& tr;
-  const ScanParams& p;
-  const uint8_t* win;
-  uint8_t* s_cls;
-  uint32_t* s_misc;
-  unsigned long long* s_keys;
-  unsigned long long t0, t1;
-  uint32_t wofs;
+// ------------------------------------------------------------------ K1 (warp-specialised)
+// One producer warp streams 16 KB tiles HBM -> shared memory with TMA bulk
+// copies through a ring of kWStages stages (full/empty mbarriers).  Each of
+// the kConsumerWarps consumer warps owns a 1 KB slice of every tile and runs
+// it end to end with no CTA-wide barrier: filter, candidates, exact check,
+// ordering of its hits, write-out into its private staging region, and one
+// directory record per (tile, warp) segment.
+constexpr int kConsumerWarps = 16;
+constexpr int kWarpKernelThreads = (kConsumerWarps + 1) * 32;
+constexpr uint32_t kSlice = kTile / kConsumerWarps;  // 1024
+constexpr int kWStages = 4;
+constexpr uint32_t kWQueue = 256;  // per-warp filter survivors
+constexpr uint32_t kWHits = 64;    // per-warp hit keys per slice
 
-  __device__ __forceinline__ uint32_t tbyte(unsigned long long x) const {
-    const unsigned long long li = x - t0 + wofs;
-    return li < kStageBytes ? win[li] : __ldg(p.text + x);
-  }
-  __device__ __forceinline__ void emit_pid(unsigned long long i, uint32_t pid) const {
-    if (p.mode == 0) {
-      const uint32_t slot = atomicAdd(&s_misc[0], 1u);
-      if (slot < kHitCap) s_keys[slot] = ((i - t0) << 40) | pid;
-    } else {
-      const unsigned long long slot = atomicAdd(p.g_count, 1ull);
-      if (slot < p.keys_cap) p.keys[slot] = ((p.base + i) << 24) | pid;
-    }
-  }
-  __device__ __forceinline__ void emit_state(unsigned long long i, uint32_t st) const {
-    for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o)
-      emit_pid(i, __ldg(tr.out_pid + o));
-  }
-  // PFAC walk (scan.hpp:142-168) from state st at text position j (the walk
-  // started at i): every visited output state emits; stop at a missing edge
-  // or the end of text.
-  template <bool kSmemTable, typename Entry>
-  __device__ __forceinline__ void walk(const Entry* T, unsigned long long i, uint32_t st,
-                                       unsigned long long j) const {
-    using ET = EntryTraits<Entry>;
-    for (; j < p.n; ++j) {
-      const uint32_t c = s_cls[tbyte(j)];
-      const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
-      if (!e) break;
-      st = e & ET::kMask;
-      if (e & ET::kFlag) emit_state(i, st);
-    }
-  }
+struct SegDir {
+  uint32_t cursor;  // offset inside the warp's staging region
+  uint32_t count;
 };
 
-// Loads the automaton pieces a kernel keeps in shared memory.
-__device__ __forceinline__ void stage_tables(uint8_t* smem, const PfacLayout& L, const DevTrie& tr, bool filter,
-                                             bool bm2, uint32_t hash_bytes, uint32_t table_bytes) {
-  const int tid = threadIdx.x;
-  if (tid < 16) reinterpret_cast<uint4*>(smem + L.cls)[tid] = reinterpret_cast<const uint4*>(tr.cls)[tid];
-  auto copy = [&](uint32_t off, const void* src, uint32_t bytes) {
-    const uint4* s = reinterpret_cast<const uint4*>(src);
-    uint4* d = reinterpret_cast<uint4*>(smem + off);
-    for (uint32_t i = tid; i < bytes / 16; i += kThreads) d[i] = s[i];
-  };
-  if (filter) copy(L.dmask, tr.dmask, kDmaskBytes);
-  if (bm2) copy(L.bm2, tr.bm2, kBm2Bytes);
-  if (hash_bytes) copy(L.hash, tr.jump, hash_bytes);
-  if (table_bytes) copy(L.table, tr.table, table_bytes);
+struct WarpScanParams {
+  const uint8_t* text;
+  unsigned long long n, own, base;
+  uint32_t num_tiles;
+  int mode;                      // 0 ordered staging; 1 global keys
+  DevHit* staging;
+  unsigned long long region;     // staging records per (CTA, warp) region
+  SegDir* dir;                   // num_tiles * kConsumerWarps
+  unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use
+  unsigned long long* keys;      // mode 1
+  unsigned long long keys_cap;
+};
+
+__host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t hash_bytes, uint32_t table_bytes) {
+  PfacLayout L;
+  uint32_t o = kWStages * kStageBytes;
+  L.bars = o; o += 2 * kWStages * 8;
+  L.cls = o; o += 256;
+  L.misc = o; o += kConsumerWarps * 4;
+  L.keys = o; o += kConsumerWarps * kWHits * 8;
+  L.queue = o; o += filter ? kConsumerWarps * kWQueue * 4 : 0;
+  L.dmask = o; o += filter ? kDmaskBytes : 0;
+  L.bm2 = o; o += filter ? kBm2Bytes : 0;
+  o = align16(o);
+  L.hash = o; o += filter ? hash_bytes : 0;
+  o = align16(o);
+  L.table = o; o += table_bytes;
+  L.total = o;
+  return L;
 }
 
-// Per-tile epilogue: order the tile's hit keys, reserve a staging slot,
-// write glop_hit records, record the tile directory entry (mode 0).
-__device__ __forceinline__ void tile_epilogue(const TileCtx& tc, uint32_t t) {
-  const int tid = threadIdx.x;
-  const ScanParams& p = tc.p;
-  const uint32_t nh = tc.s_misc[0];
-  const bool over = nh > kHitCap;
-  if (!over && nh > 1) {
-    uint32_t P = 1;
-    while (P < nh) P <<= 1;
-    for (uint32_t x = nh + tid; x < P; x += kThreads) tc.s_keys[x] = ~0ull;
-    __syncthreads();
-    sort_keys(tc.s_keys, P);
-  }
-  if (tid == 0) {
-    const unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
-    p.dir[t].slot = slot;
-    p.dir[t].count = nh;
-    p.dir[t].overflow = over;
-    if (over) atomicOr(p.g_flags, 1u);
-    tc.s_misc[1] = (uint32_t)slot;
-    tc.s_misc[2] = (uint32_t)(slot >> 32);
-  }
-  __syncthreads();
-  const unsigned long long slot = (unsigned long long)tc.s_misc[1] | ((unsigned long long)tc.s_misc[2] << 32);
-  if (!over && slot + nh <= p.staging_cap) {
-    for (uint32_t h = tid; h < nh; h += kThreads) {
-      const unsigned long long key = tc.s_keys[h];
-      const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
-      DevHit out;
-      out.offset = p.base + tc.t0 + (key >> 40);
-      out.pid = pid;
-      out.len = __ldg(tc.tr.pid_len + pid);
-      p.staging[slot + h] = out;
+// Ascending sort of keys[0, n), n <= 64, by one warp (smem bitonic).
+__device__ __forceinline__ void warp_sort_keys(unsigned long long* keys, uint32_t n, uint32_t lane) {
+  if (n <= 1) return;
+  uint32_t P = 2;
+  while (P < n) P <<= 1;
+  for (uint32_t x = n + lane; x < P; x += 32) keys[x] = ~0ull;
+  __syncwarp();
+  for (uint32_t k = 2; k <= P; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t x = lane; x < P; x += 32) {
+        const uint32_t y = x ^ j;
+        if (y > x) {
+          const unsigned long long u = keys[x], v = keys[y];
+          if ((u > v) == ((x & k) == 0)) keys[x] = v, keys[y] = u;
+        }
+      }
+      __syncwarp();
     }
-  }
-  __syncthreads();
-  if (tid == 0) tc.s_misc[0] = 0;
 }
 
-// K1 (FILTERED).  Phase A samples every stride-th position and tests its
-// q-gram against the d-mask (bit d set <=> some entry has this q-gram at
-// offset d); survivors are queued.  Phase B takes queued candidates
-// i = P - d, probes the J-byte jump hash (exact), emits the jump state's
-// outputs and walks the remaining levels.  Phase C orders and writes hits.
-template <bool kSmemTable, bool kSmemHash, typename Entry>
-__global__ void __launch_bounds__(kThreads, 1) pfac_filtered_kernel(const DevTrie tr, const ScanParams p,
-                                                                     const PfacLayout L) {
+template <bool kFilter, bool kSmemTable, bool kSmemHash, typename Entry>
+__global__ void __launch_bounds__(kWarpKernelThreads, 1)
+    pfac_warp_kernel(const DevTrie tr, const WarpScanParams p, const PfacLayout L) {
+  using ET = EntryTraits<Entry>;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
-  uint32_t* s_queue = reinterpret_cast<uint32_t*>(smem + L.queue);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + kWStages;
+  const uint8_t* s_cls = smem + L.cls;
   const uint8_t* s_dmask = smem + L.dmask;
   const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
   const JumpEntry* H = kSmemHash ? reinterpret_cast<const JumpEntry*>(smem + L.hash) : tr.jump;
   const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
-  stage_tables(smem, L, tr, true, !kSmemHash, kSmemHash ? tr.jump_bytes : 0, kSmemTable ? tr.table_bytes : 0);
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    s_misc[0] = 0;
-    s_misc[3] = 0;
-    fence_mbar_init();
+
+  // ---- stage the automaton (all warps), init barriers
+  {
+    auto copy = [&](uint32_t off, const void* src, uint32_t bytes) {
+      const uint4* s = reinterpret_cast<const uint4*>(src);
+      uint4* d = reinterpret_cast<uint4*>(smem + off);
+      for (uint32_t i = tid; i < bytes / 16; i += kWarpKernelThreads) d[i] = s[i];
+    };
+    copy(L.cls, tr.cls, 256);
+    if (kFilter) {
+      copy(L.dmask, tr.dmask, kDmaskBytes);
+      copy(L.bm2, tr.bm2, kBm2Bytes);
+      if (kSmemHash) copy(L.hash, tr.jump, tr.jump_bytes);
+    }
+    if (kSmemTable) copy(L.table, tr.table, tr.table_bytes);
+    if (tid < kConsumerWarps) reinterpret_cast<uint32_t*>(smem + L.misc)[tid] = 0;
+    if (tid == 0) {
+      for (int s = 0; s < kWStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], kConsumerWarps);
+      }
+      fence_mbar_init();
+    }
   }
   __syncthreads();
-  Ring ring{smem, bars, p.text - ((uintptr_t)p.text & 15), (uint32_t)((uintptr_t)p.text & 15), p.n};
-  if (tid == 0)
-    for (int k = 0; k < kStages; ++k) {
-      const uint32_t t = blockIdx.x + k * gridDim.x;
-      if (t < p.num_tiles) ring.issue(k, t);
-    }
-  const uint32_t q = tr.q, S = tr.stride, lmin = tr.lmin, J = tr.jump_depth, cap_log2 = tr.jump_cap_log2;
-  const uint32_t qmask = q >= 4 ? 0xFFFFFFFFu : ((1u << (8 * q)) - 1);
+  const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
+  Ring ring{smem, full, p.text - a, a, p.n};
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer
+    if (lane == 0)
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t t = blockIdx.x + k * gridDim.x;
+        if (t >= p.num_tiles) break;
+        const int stage = k % kWStages;
+        if (k >= (uint32_t)kWStages) {
+          mbar_wait(&empty[stage], ((k / kWStages) - 1) & 1);
+          fence_proxy_async();
+        }
+        ring.issue(stage, t);
+      }
+    return;
+  }
+
+  // ---------------- consumers
+  uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kWQueue;
+  uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.misc);  // per-warp hit counters
+  unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.keys) + warp * kWHits;
+  const unsigned long long region_base = (unsigned long long)(blockIdx.x * kConsumerWarps + warp) * p.region;
+  uint32_t cursor = 0;  // records written into this warp's staging region
+  const uint32_t qg = tr.q, S = tr.stride, lmin = tr.lmin, J = tr.jump_depth, cap_log2 = tr.jump_cap_log2;
+  const uint32_t qmask = qg >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qg)) - 1);
   const unsigned long long jmask = low_bytes_mask(J);
+  const uint32_t hmask = (1u << cap_log2) - 1;
 
   for (uint32_t k = 0;; ++k) {
     const uint32_t t = blockIdx.x + k * gridDim.x;
     if (t >= p.num_tiles) break;
-    const int stage = k % kStages;
-    mbar_wait(&bars[stage], (k / kStages) & 1);
-    TileCtx tc{tr, p, ring.stages + (size_t)stage * kStageBytes, smem + L.cls, s_misc,
-               reinterpret_cast<unsigned long long*>(smem + L.keys), (unsigned long long)t * kTile, 0, ring.a};
-    tc.t1 = tc.t0 + kTile < p.own ? tc.t0 + kTile : p.own;
-    const unsigned long long t0 = tc.t0, t1 = tc.t1;
+    const int stage = k % kWStages;
+    mbar_wait(&full[stage], (k / kWStages) & 1);
+    const uint8_t* win = smem + (size_t)stage * kStageBytes;
+    const unsigned long long t0 = (unsigned long long)t * kTile;
+    // this warp's owned starts, tile-local: [s_lo, s_hi)
+    const unsigned long long tile_own = p.own - t0 < kTile ? p.own - t0 : kTile;
+    const uint32_t s_lo = warp * kSlice;
+    const uint32_t s_hi = (uint32_t)min((unsigned long long)(s_lo + kSlice), tile_own);
+    // tile-local offset x <-> window index x + a; global text position t0 + x
+    const unsigned long long avail = p.n - t0;  // bytes from t0 to end of text
+    auto emit = [&](uint32_t x, uint32_t pid) {  // start x (tile-local)
+      if (p.mode == 0) {
+        const uint32_t slot = atomicAdd(&s_nh[warp], 1u);
+        if (slot < kWHits) hk[slot] = ((unsigned long long)(x - s_lo) << 40) | pid;
+      } else {
+        const unsigned long long slot = atomicAdd(p.g_count + 3, 1ull);
+        if (slot < p.keys_cap) p.keys[slot] = ((p.base + t0 + x) << 24) | pid;
+      }
+    };
+    auto tbyte = [&](unsigned long long j) -> uint32_t {  // tile-local j
+      return j + a < kStageBytes ? win[j + a] : __ldg(p.text + t0 + j);
+    };
+    auto emit_state = [&](uint32_t x, uint32_t st) {
+      for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o)
+        emit(x, __ldg(tr.out_pid + o));
+    };
+    // PFAC walk (scan.hpp:142-168) from state st at tile-local byte j
+    auto walk = [&](uint32_t x, uint32_t st, unsigned long long j) {
+      for (; j < avail; ++j) {
+        const uint32_t c = s_cls[tbyte(j)];
+        const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
+        if (!e) break;
+        st = e & ET::kMask;
+        if (e & ET::kFlag) emit_state(x, st);
+      }
+    };
 
-    // exact check of candidate start i (t0 <= i < t1, i + lmin <= n)
-    auto candidate = [&](unsigned long long i) {
-      const unsigned long long key = win_u64(tc.win, (uint32_t)(i - t0) + tc.wofs) & jmask;
-      if (!kSmemHash) {
+    if (kFilter) {
+      // exact check of candidate start x: level-2 bitmap, then the J-byte
+      // jump table (generalised RootJump), then the remaining walk
+      auto candidate = [&](uint32_t x) {
+        const unsigned long long key = win_u64(win, x + a) & jmask;
         const uint32_t b = prefix_bit(key);
         if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
-      }
-      const uint32_t mask = (1u << cap_log2) - 1;
-      for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & mask) {
-        const JumpEntry e = H[h];
-        if (!e.state1) return;
-        if (e.key != key) continue;
-        const uint32_t st = e.state1 - 1;
-        if (e.out != kOutNone) {
-          if (e.out == kOutMany) tc.emit_state(i, st);
-          else tc.emit_pid(i, e.out);
+        for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & hmask) {
+          const JumpEntry e = H[h];
+          if (!e.state1) return;
+          if (e.key != key) continue;
+          const uint32_t st = e.state1 - 1;
+          if (e.out != kOutNone) {
+            if (e.out == kOutMany) emit_state(x, st);
+            else emit(x, e.out);
+          }
+          if (tr.lmax > J) walk(x, st, (unsigned long long)x + J);
+          return;
         }
-        if (tr.lmax > J) tc.template walk<kSmemTable>(T, i, st, i + J);
-        return;
+      };
+      auto drain = [&](uint32_t qn) {  // queue entries: (P << 8) | dmask
+        for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
+          const uint32_t e = e0 + lane;
+          if (e < qn) {
+            const uint32_t v = q[e], P = v >> 8;
+            uint32_t dm = v & 0xFFu;
+            while (dm) {
+              const uint32_t d = __ffs(dm) - 1;
+              dm &= dm - 1;
+              candidate(P - d);
+            }
+          }
+        }
+        __syncwarp();
+      };
+      // sampled positions P = m*S (tile-anchored); this warp evaluates the
+      // P whose candidates P-d (d < S) can fall in [s_lo, s_hi)
+      const uint32_t m0 = (s_lo + S - 1) / S, m1 = (s_hi + 2 * S - 2) / S;  // m*S < s_hi + S - 1
+      uint32_t qn = 0;
+      for (uint32_t base = m0; base < m1; base += 32) {
+        const uint32_t m = base + lane;
+        uint32_t dm = 0;
+        if (m < m1) {
+          const uint32_t P = m * S;
+          if ((unsigned long long)P + qg <= avail) {
+            const uint32_t g = win_u32(win, P + a) & qmask;
+            dm = s_dmask[qgram_bucket(g, qg)];
+            // keep d with s_lo <= P - d < s_hi and P - d + lmin <= avail
+            if (dm) {
+              const uint32_t lo_span = P - s_lo;  // d <= lo_span
+              if (lo_span < 7) dm &= (2u << lo_span) - 1;
+              if (P >= s_hi) dm &= ~((2u << min(P - s_hi, 7u)) - 1);
+              if ((unsigned long long)P + lmin > avail) {
+                const unsigned long long need = (unsigned long long)P + lmin - avail;  // d >= need
+                dm = need > 7 ? 0 : dm & ~((1u << need) - 1);
+              }
+            }
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, dm != 0);
+        if (bal) {
+          if (qn + 32 > kWQueue) {
+            drain(qn);
+            qn = 0;
+          }
+          if (dm) q[qn + __popc(bal & ((1u << lane) - 1))] = ((m * S) << 8) | dm;
+          qn += __popc(bal);
+        }
       }
-    };
-    auto expand = [&](unsigned long long P, uint32_t dm) {
-      while (dm) {
-        const uint32_t d = __ffs(dm) - 1;
-        dm &= dm - 1;
-        if (P < t0 + d) continue;
-        const unsigned long long i = P - d;
-        if (i >= t1 || i + lmin > p.n) continue;
-        candidate(i);
-      }
-    };
+      __syncwarp();
+      drain(qn);
+    } else {
+      // DIRECT: one lane per start byte
+      for (uint32_t x0 = s_lo; x0 < s_hi; x0 += 32)
+        if (x0 + lane < s_hi) walk(x0 + lane, 0u, x0 + lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);  // window no longer read
+    const uint32_t nh = s_nh[warp];
+    __syncwarp();
+    if (lane == 0) s_nh[warp] = 0;
 
-    // Phase A: sampled q-grams (tile-anchored: P = t0 + m*S covers every
-    // start in [t0, t1) with some P - d, 0 <= d < S)
-    const uint32_t M = (uint32_t)((t1 - t0 + S - 1) / S);
-    for (uint32_t m = tid; m < M; m += kThreads) {
-      const unsigned long long P = t0 + (unsigned long long)m * S;
-      if (P + q > p.n) continue;
-      const uint32_t g = win_u32(tc.win, (uint32_t)(P - t0) + tc.wofs) & qmask;
-      const uint32_t dm = s_dmask[qgram_bucket(g, q)];
-      if (dm) {
-        const uint32_t slot = atomicAdd(&s_misc[3], 1u);
-        if (slot < kQueueCap) s_queue[slot] = (m << 8) | dm;
-        else expand(P, dm);  // queue full: exact inline path
+    if (p.mode == 0 && nh) {
+      if (nh > kWHits) {
+        if (lane == 0) atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
+      } else {
+        warp_sort_keys(hk, nh, lane);
+        const bool fits = cursor + nh <= p.region;
+        for (uint32_t h = lane; h < nh && fits; h += 32) {
+          const unsigned long long key = hk[h];
+          const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
+          DevHit out;
+          out.offset = p.base + t0 + s_lo + (key >> 40);
+          out.pid = pid;
+          out.len = __ldg(tr.pid_len + pid);
+          p.staging[region_base + cursor + h] = out;
+        }
+        __syncwarp();
       }
-    }
-    __syncthreads();
-    // Phase B: queued candidates, one queue entry per thread
-    const uint32_t nq = min(s_misc[3], kQueueCap);
-    for (uint32_t e = tid; e < nq; e += kThreads) {
-      const uint32_t v = s_queue[e];
-      expand(t0 + (unsigned long long)(v >> 8) * S, v & 0xFFu);
-    }
-    __syncthreads();  // stage consumed, hit keys complete
-    if (tid == 0) {
-      s_misc[3] = 0;
-      const uint32_t tn = t + kStages * gridDim.x;
-      if (tn < p.num_tiles) {
-        fence_proxy_async();
-        ring.issue(stage, tn);
+      if (lane == 0) {
+        p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, nh};
+        atomicAdd(p.g_count, (unsigned long long)nh);
       }
+      cursor += nh;
+    } else if (p.mode == 0 && lane == 0) {
+      p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, 0};
     }
-    if (p.mode == 0) tile_epilogue(tc, t);
-    __syncthreads();
+  }
+  if (p.mode == 0 && lane == 0 && cursor) atomicMax(p.g_count + 2, (unsigned long long)cursor);
+}
+
+// ---- segment directory -> ordered output
+// Pass 1: per-block sums of segment counts (kSegPerBlock segments per block).
+constexpr uint32_t kSegPerThread = 8;
+constexpr uint32_t kSegPerBlock = 1024 * kSegPerThread;
+
+__global__ void __launch_bounds__(1024) seg_reduce_kernel(const SegDir* dir, unsigned long long nseg,
+                                                          uint32_t* block_sums) {
+  __shared__ uint32_t ws[32];
+  const unsigned long long b = (unsigned long long)blockIdx.x * kSegPerBlock + threadIdx.x * kSegPerThread;
+  uint32_t s = 0;
+  for (uint32_t i = 0; i < kSegPerThread; ++i)
+    if (b + i < nseg) s += dir[b + i].count;
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = ws[threadIdx.x];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
   }
 }
 
-// K1 (DIRECT): the literal one-thread-per-start-byte PFAC walk
-// (scan.hpp:113-170) over the alphabet-compressed table.
-template <bool kSmemTable, typename Entry>
-__global__ void __launch_bounds__(kThreads, 1) pfac_direct_kernel(const DevTrie tr, const ScanParams p,
-                                                                   const PfacLayout L) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
-  const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
-  stage_tables(smem, L, tr, false, false, 0, kSmemTable ? tr.table_bytes : 0);
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    s_misc[0] = 0;
-    fence_mbar_init();
+// Pass 3 (after block_prefix_kernel over block sums): per-block exclusive scan
+// of segment counts, then each thread copies its segments' records.
+template <typename Rec>
+__global__ void __launch_bounds__(1024) seg_gather_kernel(const SegDir* dir, unsigned long long nseg,
+                                                          const unsigned long long* block_prefix,
+                                                          uint32_t grid, unsigned long long region,
+                                                          const Rec* staging, Rec* out) {
+  __shared__ uint32_t ws[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned long long b = (unsigned long long)blockIdx.x * kSegPerBlock + tid * kSegPerThread;
+  uint32_t c[kSegPerThread], s = 0;
+  for (uint32_t i = 0; i < kSegPerThread; ++i) {
+    c[i] = b + i < nseg ? dir[b + i].count : 0;
+    s += c[i];
+  }
+  uint32_t incl = s;  // warp inclusive scan
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t v = ws[lane], iv = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += u;
+    }
+    ws[lane] = iv - v;
   }
   __syncthreads();
-  Ring ring{smem, bars, p.text - ((uintptr_t)p.text & 15), (uint32_t)((uintptr_t)p.text & 15), p.n};
-  if (tid == 0)
-    for (int k = 0; k < kStages; ++k) {
-      const uint32_t t = blockIdx.x + k * gridDim.x;
-      if (t < p.num_tiles) ring.issue(k, t);
-    }
-  for (uint32_t k = 0;; ++k) {
-    const uint32_t t = blockIdx.x + k * gridDim.x;
-    if (t >= p.num_tiles) break;
-    const int stage = k % kStages;
-    mbar_wait(&bars[stage], (k / kStages) & 1);
-    TileCtx tc{tr, p, ring.stages + (size_t)stage * kStageBytes, smem + L.cls, s_misc,
-               reinterpret_cast<unsigned long long*>(smem + L.keys), (unsigned long long)t * kTile, 0, ring.a};
-    tc.t1 = tc.t0 + kTile < p.own ? tc.t0 + kTile : p.own;
-    for (unsigned long long i = tc.t0 + tid; i < tc.t1; i += kThreads)
-      tc.template walk<kSmemTable>(T, i, 0u, i);
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t tn = t + kStages * gridDim.x;
-      if (tn < p.num_tiles) {
-        fence_proxy_async();
-        ring.issue(stage, tn);
-      }
-    }
-    if (p.mode == 0) tile_epilogue(tc, t);
-    __syncthreads();
+  unsigned long long dst = block_prefix[blockIdx.x] + ws[w] + incl - s;
+  for (uint32_t i = 0; i < kSegPerThread; ++i) {
+    if (!c[i]) continue;
+    const unsigned long long seg = b + i;
+    const unsigned long long t = seg / kConsumerWarps, wp = seg % kConsumerWarps;
+    const unsigned long long src = ((t % grid) * kConsumerWarps + wp) * region + dir[seg].cursor;
+    for (uint32_t h = 0; h < c[i]; ++h) out[dst + h] = staging[src + h];
+    dst += c[i];
   }
 }
 

@@ -32,7 +32,7 @@ def torch_cuda():
 def dev_scan(ctx, torch, trie, text: np.ndarray, kernel, own=None, base=0, offset=0):
     """pfac_scan_device over text[offset:] resident in HBM."""
     n = text.size - offset
-    d = torch.from_numpy(np.ascontiguousarray(text)).cuda() if text.size else torch.zeros(1, dtype=torch.uint8).cuda()
+    d = torch.from_numpy(np.array(text, dtype=np.uint8, copy=True)).cuda() if text.size else torch.zeros(1, dtype=torch.uint8).cuda()
     cap = max(1 << 16, 4 * n)
     out = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
     nh = ctx.pfac_scan_device(trie, d.data_ptr() + offset, n, out.data_ptr(), cap, own=own, base=base, kernel=kernel)
@@ -256,3 +256,24 @@ def test_dropin_cpp_binary():
         subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("k,L,lens", [(10000, 8, (8, 8)), (300, 16, (12, 16)), (200, 64, (9, 40)),
+                                      (500, 8, (1, 8)), (64, 4096, (2, 30))])
+def test_kernel_variants_vs_oracle(ctx, torch_cuda, k, L, lens):
+    """Jump table in global memory (k=10000), lmin > 8 (jump depth 8 then a
+    table walk), stride-1 sampling (1-byte patterns), long prefixes."""
+    rng = np.random.default_rng(k + L)
+    text = glop.gen_syslog_host(4 << 20, seed=k)
+    vocab = [text[o:o + int(rng.integers(lens[0], lens[1] + 1))].tobytes()
+             for o in rng.integers(0, text.size - 64, k // 2)]
+    rand = [bytes(rng.integers(32, 127, int(rng.integers(lens[0], lens[1] + 1)), dtype=np.uint8))
+            for _ in range(k - k // 2)]
+    pats = list(dict.fromkeys(vocab + rand))
+    trie = ctx.upload(glop.build_failureless_trie(pats, L))
+    ref = O.pfac_scan(text, O.Trie(pats, L))
+    for kernel in KERNELS:
+        got = dev_scan(ctx, torch_cuda, trie, text, kernel)
+        assert got.tobytes() == ref.tobytes(), (kernel, len(got), len(ref))
+    if k == 10000:
+        assert not trie.info.jump_in_smem
