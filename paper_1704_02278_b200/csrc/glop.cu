@@ -84,7 +84,7 @@ struct glop_ctx {
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
   DBuf text, staging, out, dir, prefix, misc, keys, keys_alt, cub_tmp;
-  DBuf keep, bcounts, bprefix, alerts, kmp_dfa, kmp_cls;
+  DBuf keep, bcounts, bprefix, alerts, kmp_dfa, kmp_cls, spill;
   unsigned long long* h_misc = nullptr;  // pinned readback
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
   bool timed = false;
@@ -194,10 +194,12 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
     TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
   region = c->staging.bytes / sizeof(glop_hit) / regions;
   auto* g = c->misc.as<unsigned long long>();
+  TRY(c->spill.ensure(regions * kWSpill * 8));
 
   for (int attempt = 0; attempt < 3; ++attempt) {
     CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
     WarpScanParams p{};
+    p.spill = c->spill.as<unsigned long long>();
     p.text = d_text;
     p.n = n;
     p.own = own;
@@ -508,7 +510,7 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
-                  &c->kmp_dfa, &c->kmp_cls})
+                  &c->kmp_dfa, &c->kmp_cls, &c->spill})
     b->release();
   cudaFreeHost(c->h_misc);
   if (c->ev0) cudaEventDestroy(c->ev0);

@@ -252,7 +252,8 @@ constexpr int kWarpKernelThreads = (kConsumerWarps + 1) * 32;
 constexpr uint32_t kSlice = kTile / kConsumerWarps;  // 1024
 constexpr int kWStages = 4;
 constexpr uint32_t kWQueue = 256;  // per-warp filter survivors
-constexpr uint32_t kWHits = 64;    // per-warp hit keys per slice
+constexpr uint32_t kWHits = 64;    // per-warp hit keys per slice (smem)
+constexpr uint32_t kWSpill = 8192; // per-warp global spill area (keys), a power of two
 
 struct SegDir {
   uint32_t cursor;  // offset inside the warp's staging region
@@ -270,6 +271,7 @@ struct WarpScanParams {
   unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
+  unsigned long long* spill;     // kWSpill keys per consumer warp (dense slices)
 };
 
 __host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t hash_bytes, uint32_t table_bytes) {
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   Ring ring{smem, full, p.text - a, a, p.n};
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer
+    // ---------------- producer: one lane keeps kWStages tiles in flight
     if (lane == 0)
       for (uint32_t k = 0;; ++k) {
         const uint32_t t = blockIdx.x + k * gridDim.x;
@@ -371,47 +373,53 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kWQueue;
   uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.misc);  // per-warp hit counters
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.keys) + warp * kWHits;
-  const unsigned long long region_base = (unsigned long long)(blockIdx.x * kConsumerWarps + warp) * p.region;
+  const uint32_t gw = blockIdx.x * kConsumerWarps + warp;  // global warp id
+  unsigned long long* spill = p.spill + (size_t)gw * kWSpill;
+  const unsigned long long region_base = (unsigned long long)gw * p.region;
   uint32_t cursor = 0;  // records written into this warp's staging region
   const uint32_t qg = tr.q, S = tr.stride, lmin = tr.lmin, J = tr.jump_depth, cap_log2 = tr.jump_cap_log2;
   const uint32_t qmask = qg >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qg)) - 1);
   const unsigned long long jmask = low_bytes_mask(J);
   const uint32_t hmask = (1u << cap_log2) - 1;
+  const uint32_t lmax = tr.lmax, C = tr.C;
 
   for (uint32_t k = 0;; ++k) {
     const uint32_t t = blockIdx.x + k * gridDim.x;
     if (t >= p.num_tiles) break;
     const int stage = k % kWStages;
     mbar_wait(&full[stage], (k / kWStages) & 1);
-    const uint8_t* win = smem + (size_t)stage * kStageBytes;
+    const uint8_t* sb = smem + (size_t)stage * kStageBytes;  // sb[x + a] = text[t0 + x]
+    const uint8_t* win = sb + a;
     const unsigned long long t0 = (unsigned long long)t * kTile;
-    // this warp's owned starts, tile-local: [s_lo, s_hi)
-    const unsigned long long tile_own = p.own - t0 < kTile ? p.own - t0 : kTile;
+    const uint32_t tile_own = (uint32_t)min(p.own - t0, (unsigned long long)kTile);
+    // text bytes available from t0 (clamped; only the last tiles see < 2^31)
+    const uint32_t avail = (uint32_t)min(p.n - t0, 0x7FFFFFFFull);
     const uint32_t s_lo = warp * kSlice;
-    const uint32_t s_hi = (uint32_t)min((unsigned long long)(s_lo + kSlice), tile_own);
-    // tile-local offset x <-> window index x + a; global text position t0 + x
-    const unsigned long long avail = p.n - t0;  // bytes from t0 to end of text
+    const uint32_t s_hi = min(s_lo + kSlice, tile_own);
+
     auto emit = [&](uint32_t x, uint32_t pid) {  // start x (tile-local)
       if (p.mode == 0) {
         const uint32_t slot = atomicAdd(&s_nh[warp], 1u);
-        if (slot < kWHits) hk[slot] = ((unsigned long long)(x - s_lo) << 40) | pid;
+        const unsigned long long key = ((unsigned long long)(x - s_lo) << 40) | pid;
+        if (slot < kWHits) hk[slot] = key;
+        else if (slot - kWHits < kWSpill - kWHits) spill[slot - kWHits] = key;
       } else {
         const unsigned long long slot = atomicAdd(p.g_count + 3, 1ull);
         if (slot < p.keys_cap) p.keys[slot] = ((p.base + t0 + x) << 24) | pid;
       }
     };
-    auto tbyte = [&](unsigned long long j) -> uint32_t {  // tile-local j
-      return j + a < kStageBytes ? win[j + a] : __ldg(p.text + t0 + j);
+    auto tbyte = [&](uint32_t j) -> uint32_t {  // tile-local j < avail
+      return j + a < kStageBytes ? win[j] : __ldg(p.text + t0 + j);
     };
     auto emit_state = [&](uint32_t x, uint32_t st) {
       for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o)
         emit(x, __ldg(tr.out_pid + o));
     };
     // PFAC walk (scan.hpp:142-168) from state st at tile-local byte j
-    auto walk = [&](uint32_t x, uint32_t st, unsigned long long j) {
+    auto walk = [&](uint32_t x, uint32_t st, uint32_t j) {
       for (; j < avail; ++j) {
         const uint32_t c = s_cls[tbyte(j)];
-        const uint32_t e = kSmemTable ? (uint32_t)T[st * tr.C + c] : (uint32_t)__ldg(T + st * tr.C + c);
+        const uint32_t e = kSmemTable ? (uint32_t)T[st * C + c] : (uint32_t)__ldg(T + st * C + c);
         if (!e) break;
         st = e & ET::kMask;
         if (e & ET::kFlag) emit_state(x, st);
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       // exact check of candidate start x: level-2 bitmap, then the J-byte
       // jump table (generalised RootJump), then the remaining walk
       auto candidate = [&](uint32_t x) {
-        const unsigned long long key = win_u64(win, x + a) & jmask;
+        const unsigned long long key = win_u64(sb, x + a) & jmask;
         const uint32_t b = prefix_bit(key);
         if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
         for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & hmask) {
@@ -434,49 +442,43 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
             if (e.out == kOutMany) emit_state(x, st);
             else emit(x, e.out);
           }
-          if (tr.lmax > J) walk(x, st, (unsigned long long)x + J);
+          if (lmax > J) walk(x, st, x + J);
           return;
         }
       };
       auto drain = [&](uint32_t qn) {  // queue entries: (P << 8) | dmask
-        for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
-          const uint32_t e = e0 + lane;
-          if (e < qn) {
-            const uint32_t v = q[e], P = v >> 8;
-            uint32_t dm = v & 0xFFu;
-            while (dm) {
-              const uint32_t d = __ffs(dm) - 1;
-              dm &= dm - 1;
-              candidate(P - d);
-            }
+        for (uint32_t e = lane; e < qn; e += 32) {
+          const uint32_t v = q[e], P = v >> 8;
+          uint32_t dm = v & 0xFFu;
+          while (dm) {
+            const uint32_t d = __ffs(dm) - 1;
+            dm &= dm - 1;
+            candidate(P - d);
           }
         }
         __syncwarp();
       };
-      // sampled positions P = m*S (tile-anchored); this warp evaluates the
-      // P whose candidates P-d (d < S) can fall in [s_lo, s_hi)
-      const uint32_t m0 = (s_lo + S - 1) / S, m1 = (s_hi + 2 * S - 2) / S;  // m*S < s_hi + S - 1
-      uint32_t qn = 0;
-      for (uint32_t base = m0; base < m1; base += 32) {
-        const uint32_t m = base + lane;
-        uint32_t dm = 0;
-        if (m < m1) {
-          const uint32_t P = m * S;
-          if ((unsigned long long)P + qg <= avail) {
-            const uint32_t g = win_u32(win, P + a) & qmask;
-            dm = s_dmask[qgram_bucket(g, qg)];
-            // keep d with s_lo <= P - d < s_hi and P - d + lmin <= avail
-            if (dm) {
-              const uint32_t lo_span = P - s_lo;  // d <= lo_span
-              if (lo_span < 7) dm &= (2u << lo_span) - 1;
-              if (P >= s_hi) dm &= ~((2u << min(P - s_hi, 7u)) - 1);
-              if ((unsigned long long)P + lmin > avail) {
-                const unsigned long long need = (unsigned long long)P + lmin - avail;  // d >= need
-                dm = need > 7 ? 0 : dm & ~((1u << need) - 1);
-              }
-            }
-          }
+      // d-mask of sampled position P with the validity masks applied:
+      // s_lo <= P - d < s_hi, P - d + lmin <= avail, P + q <= avail
+      auto probe = [&](uint32_t P, bool edge) -> uint32_t {
+        if (edge && P + qg > avail) return 0;
+        uint32_t dm = s_dmask[qgram_bucket(win_u32(sb, P + a) & qmask, qg)];
+        if (edge && dm) {
+          if (P - s_lo < 7) dm &= (2u << (P - s_lo)) - 1;
+          if (P >= s_hi) dm &= ~((2u << min(P - s_hi, 7u)) - 1);
+          if (P + lmin > avail) dm = P + lmin - avail > 7 ? 0 : dm & ~((1u << (P + lmin - avail)) - 1);
         }
+        return dm;
+      };
+      // sampled positions P = m*S (tile-anchored); this warp evaluates the
+      // P whose candidates P - d (d < S) can fall in [s_lo, s_hi)
+      const uint32_t m0 = (s_lo + S - 1) / S, m1 = (s_hi + 2 * S - 2) / S;  // m*S < s_hi + S - 1
+      // positions needing masks: near s_lo (P - s_lo < 7), at/after s_hi,
+      // and everything when the text ends inside this window
+      const bool tail = avail < kTile + 16;
+      const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, safe_hi = s_hi / S;  // [safe_lo, safe_hi) mask-free
+      uint32_t qn = 0;
+      auto push = [&](uint32_t m, uint32_t dm) {
         const uint32_t bal = __ballot_sync(0xffffffffu, dm != 0);
         if (bal) {
           if (qn + 32 > kWQueue) {
@@ -486,8 +488,25 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
           if (dm) q[qn + __popc(bal & ((1u << lane) - 1))] = ((m * S) << 8) | dm;
           qn += __popc(bal);
         }
+      };
+      uint32_t base = m0;
+      if (!tail && base < m1) {
+        // one masked chunk covers the leading edge (safe_lo - m0 <= 8 < 32),
+        // then the interior runs mask-free, two positions per lane per step
+        const uint32_t m = base + lane;
+        push(m, m < m1 ? probe(m * S, m < safe_lo || m >= safe_hi) : 0u);
+        for (base += 32; base + 64 <= safe_hi; base += 64) {
+          const uint32_t ma = base + lane, mb = base + 32 + lane;
+          const uint32_t da = probe(ma * S, false), db = probe(mb * S, false);
+          push(ma, da);
+          push(mb, db);
+        }
       }
-      __syncwarp();
+      for (; base < m1; base += 32) {
+        const uint32_t m = base + lane;
+        const bool edge = tail || m < safe_lo || m >= safe_hi;
+        push(m, m < m1 ? probe(m * S, edge) : 0u);
+      }
       drain(qn);
     } else {
       // DIRECT: one lane per start byte
@@ -500,30 +519,38 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
     __syncwarp();
     if (lane == 0) s_nh[warp] = 0;
 
-    if (p.mode == 0 && nh) {
-      if (nh > kWHits) {
-        if (lane == 0) atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
-      } else {
-        warp_sort_keys(hk, nh, lane);
-        const bool fits = cursor + nh <= p.region;
-        for (uint32_t h = lane; h < nh && fits; h += 32) {
-          const unsigned long long key = hk[h];
-          const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
-          DevHit out;
-          out.offset = p.base + t0 + s_lo + (key >> 40);
-          out.pid = pid;
-          out.len = __ldg(tr.pid_len + pid);
-          p.staging[region_base + cursor + h] = out;
+    if (p.mode == 0) {
+      if (nh) {
+        unsigned long long* keys = hk;
+        if (nh > kWHits) {
+          if (nh > kWSpill) {  // beyond the spill area: global fallback
+            if (lane == 0) atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
+          } else {
+            // dense slice: move the buffered keys behind the spilled ones
+            // and order the whole segment in the warp's global spill area
+            for (uint32_t j = lane; j < kWHits; j += 32) spill[nh - kWHits + j] = hk[j];
+            keys = spill;
+          }
         }
-        __syncwarp();
+        if (nh <= kWSpill) {
+          __syncwarp();
+          warp_sort_keys(keys, nh, lane);
+          if (cursor + nh <= p.region)
+            for (uint32_t h = lane; h < nh; h += 32) {
+              const unsigned long long key = keys[h];
+              const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
+              DevHit out;
+              out.offset = p.base + t0 + s_lo + (key >> 40);
+              out.pid = pid;
+              out.len = __ldg(tr.pid_len + pid);
+              p.staging[region_base + cursor + h] = out;
+            }
+          __syncwarp();
+        }
+        if (lane == 0) atomicAdd(p.g_count, (unsigned long long)nh);
       }
-      if (lane == 0) {
-        p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, nh};
-        atomicAdd(p.g_count, (unsigned long long)nh);
-      }
+      if (lane == 0) p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, nh};
       cursor += nh;
-    } else if (p.mode == 0 && lane == 0) {
-      p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, 0};
     }
   }
   if (p.mode == 0 && lane == 0 && cursor) atomicMax(p.g_count + 2, (unsigned long long)cursor);
