@@ -142,21 +142,28 @@ glop_status launch_timed(glop_ctx* c, K k, int grid, const DevTrie& tr, const Wa
   return GLOP_OK;
 }
 
+template <typename E, uint32_t kS>
+glop_status launch_pfac_s(glop_ctx* c, const glop_trie* t, const WarpScanParams& p, int grid) {
+  const DevTrie& tr = t->view;
+  const bool sh = t->smem_jump, st = t->smem_filter;
+  const PfacLayout L = make_warp_layout(true, sh ? tr.jump_bytes : 0, st ? tr.table_bytes : 0);
+  if (sh) return st ? launch_timed(c, pfac_warp_kernel<true, true, true, E, kS>, grid, tr, p, L)
+                    : launch_timed(c, pfac_warp_kernel<true, false, true, E, kS>, grid, tr, p, L);
+  return st ? launch_timed(c, pfac_warp_kernel<true, true, false, E, kS>, grid, tr, p, L)
+            : launch_timed(c, pfac_warp_kernel<true, false, false, E, kS>, grid, tr, p, L);
+}
+
 template <typename E>
 glop_status launch_pfac_e(glop_ctx* c, const glop_trie* t, bool filter, const WarpScanParams& p, int grid) {
   const DevTrie& tr = t->view;
   if (!filter) {
     const bool st = t->smem_direct;
     const PfacLayout L = make_warp_layout(false, 0, st ? tr.table_bytes : 0);
-    return st ? launch_timed(c, pfac_warp_kernel<false, true, false, E>, grid, tr, p, L)
-              : launch_timed(c, pfac_warp_kernel<false, false, false, E>, grid, tr, p, L);
+    return st ? launch_timed(c, pfac_warp_kernel<false, true, false, E, 0>, grid, tr, p, L)
+              : launch_timed(c, pfac_warp_kernel<false, false, false, E, 0>, grid, tr, p, L);
   }
-  const bool sh = t->smem_jump, st = t->smem_filter;
-  const PfacLayout L = make_warp_layout(true, sh ? tr.jump_bytes : 0, st ? tr.table_bytes : 0);
-  if (sh) return st ? launch_timed(c, pfac_warp_kernel<true, true, true, E>, grid, tr, p, L)
-                    : launch_timed(c, pfac_warp_kernel<true, false, true, E>, grid, tr, p, L);
-  return st ? launch_timed(c, pfac_warp_kernel<true, true, false, E>, grid, tr, p, L)
-            : launch_timed(c, pfac_warp_kernel<true, false, false, E>, grid, tr, p, L);
+  if (tr.q == 4 && tr.stride == 5) return launch_pfac_s<E, 5>(c, t, p, grid);
+  return launch_pfac_s<E, 0>(c, t, p, grid);
 }
 
 glop_status launch_pfac(glop_ctx* c, const glop_trie* t, bool filter, const WarpScanParams& p, int grid) {
@@ -180,8 +187,9 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   if (own > n) return fail(GLOP_EINVAL, "pfac_scan: own > n");
   if (own == 0 || t->empty) return GLOP_OK;
   const bool filter = kind != GLOP_PFAC_DIRECT;
-  const uint32_t num_tiles = (uint32_t)((own + kTile - 1) / kTile);
-  const unsigned long long nseg = (unsigned long long)num_tiles * kConsumerWarps;
+  // tiles are aligned to the 16-byte granule holding the text start
+  const uint32_t num_tiles = (uint32_t)((own + ((uintptr_t)d_text & 15) + kTile - 1) / kTile);
+  const unsigned long long nseg = (unsigned long long)num_tiles * kGroupWarps;
   const uint32_t nb = (uint32_t)((nseg + kSegPerBlock - 1) / kSegPerBlock);
   const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
   const unsigned long long regions = (unsigned long long)grid * kConsumerWarps;
@@ -194,12 +202,10 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
     TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
   region = c->staging.bytes / sizeof(glop_hit) / regions;
   auto* g = c->misc.as<unsigned long long>();
-  TRY(c->spill.ensure(regions * kWSpill * 8));
 
   for (int attempt = 0; attempt < 3; ++attempt) {
     CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
     WarpScanParams p{};
-    p.spill = c->spill.as<unsigned long long>();
     p.text = d_text;
     p.n = n;
     p.own = own;

@@ -242,18 +242,20 @@ __host__ __device__ __forceinline__ uint32_t jump_slot(unsigned long long key, u
 
 // ------------------------------------------------------------------ K1 (warp-specialised)
 // One producer warp streams 16 KB tiles HBM -> shared memory with TMA bulk
-// copies through a ring of kWStages stages (full/empty mbarriers).  Each of
-// the kConsumerWarps consumer warps owns a 1 KB slice of every tile and runs
-// it end to end with no CTA-wide barrier: filter, candidates, exact check,
-// ordering of its hits, write-out into its private staging region, and one
-// directory record per (tile, warp) segment.
+// copies through a ring of kWStages stages (full/empty mbarriers).  The
+// consumer warps form kGroups groups of kGroupWarps; group g takes the CTA's
+// tiles k = g, g + kGroups, ... and each of its warps owns a 4 KB slice of the
+// tile, which it runs end to end with no CTA-wide barrier: filter,
+// candidates, exact check, ordering of its hits, write-out into its private
+// staging region, and one directory record per (tile, slice) segment.
 constexpr int kConsumerWarps = 16;
 constexpr int kWarpKernelThreads = (kConsumerWarps + 1) * 32;
-constexpr uint32_t kSlice = kTile / kConsumerWarps;  // 1024
-constexpr int kWStages = 4;
-constexpr uint32_t kWQueue = 256;  // per-warp filter survivors
-constexpr uint32_t kWHits = 64;    // per-warp hit keys per slice (smem)
-constexpr uint32_t kWSpill = 8192; // per-warp global spill area (keys), a power of two
+constexpr int kGroupWarps = 4;                        // warps sharing one tile
+constexpr int kGroups = kConsumerWarps / kGroupWarps;  // tiles in flight per CTA
+constexpr uint32_t kSlice = kTile / kGroupWarps;       // 4096 bytes per warp per tile
+constexpr int kWStages = 6;
+constexpr uint32_t kWQueue = 128;  // per-warp filter survivors
+constexpr uint32_t kWHits = 128;   // per-warp hit keys of one drain batch (smem)
 
 struct SegDir {
   uint32_t cursor;  // offset inside the warp's staging region
@@ -267,13 +269,14 @@ struct WarpScanParams {
   int mode;                      // 0 ordered staging; 1 global keys
   DevHit* staging;
   unsigned long long region;     // staging records per (CTA, warp) region
-  SegDir* dir;                   // num_tiles * kConsumerWarps
+  SegDir* dir;                   // num_tiles * kGroupWarps
   unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
-  unsigned long long* spill;     // kWSpill keys per consumer warp (dense slices)
 };
 
+// hash_bytes > 0: jump table in shared memory; otherwise it stays in global
+// memory behind the level-2 bitmap kept in shared memory.
 __host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t hash_bytes, uint32_t table_bytes) {
   PfacLayout L;
   uint32_t o = kWStages * kStageBytes;
@@ -283,7 +286,7 @@ __host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t has
   L.keys = o; o += kConsumerWarps * kWHits * 8;
   L.queue = o; o += filter ? kConsumerWarps * kWQueue * 4 : 0;
   L.dmask = o; o += filter ? kDmaskBytes : 0;
-  L.bm2 = o; o += filter ? kBm2Bytes : 0;
+  L.bm2 = o; o += (filter && !hash_bytes) ? kBm2Bytes : 0;
   o = align16(o);
   L.hash = o; o += filter ? hash_bytes : 0;
   o = align16(o);
@@ -312,7 +315,9 @@ __device__ __forceinline__ void warp_sort_keys(unsigned long long* keys, uint32_
     }
 }
 
-template <bool kFilter, bool kSmemTable, bool kSmemHash, typename Entry>
+// kS: compile-time sampling stride (0 = runtime tr.stride; 5 = the 8-byte
+// prefix case, q = 4).
+template <bool kFilter, bool kSmemTable, bool kSmemHash, typename Entry, uint32_t kS>
 __global__ void __launch_bounds__(kWarpKernelThreads, 1)
     pfac_warp_kernel(const DevTrie tr, const WarpScanParams p, const PfacLayout L) {
   using ET = EntryTraits<Entry>;
@@ -336,15 +341,15 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
     copy(L.cls, tr.cls, 256);
     if (kFilter) {
       copy(L.dmask, tr.dmask, kDmaskBytes);
-      copy(L.bm2, tr.bm2, kBm2Bytes);
       if (kSmemHash) copy(L.hash, tr.jump, tr.jump_bytes);
+      else copy(L.bm2, tr.bm2, kBm2Bytes);
     }
     if (kSmemTable) copy(L.table, tr.table, tr.table_bytes);
     if (tid < kConsumerWarps) reinterpret_cast<uint32_t*>(smem + L.misc)[tid] = 0;
     if (tid == 0) {
       for (int s = 0; s < kWStages; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], kConsumerWarps);
+        mbar_init(&empty[s], kGroupWarps);
       }
       fence_mbar_init();
     }
@@ -370,113 +375,182 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   }
 
   // ---------------- consumers
+  // Tile-local coordinates are "window" coordinates y: sb[y] holds aligned
+  // byte A[t*kTile + y], i.e. text position t*kTile + y - a.  Tiles own the
+  // text positions [t*kTile - a, (t+1)*kTile - a), so the window is
+  // 16-byte aligned with the tile and every sampled chunk is word-aligned.
   uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kWQueue;
   uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.misc);  // per-warp hit counters
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.keys) + warp * kWHits;
   const uint32_t gw = blockIdx.x * kConsumerWarps + warp;  // global warp id
-  unsigned long long* spill = p.spill + (size_t)gw * kWSpill;
   const unsigned long long region_base = (unsigned long long)gw * p.region;
   uint32_t cursor = 0;  // records written into this warp's staging region
-  const uint32_t qg = tr.q, S = tr.stride, lmin = tr.lmin, J = tr.jump_depth, cap_log2 = tr.jump_cap_log2;
+  const uint32_t qg = tr.q, S = kS ? kS : tr.stride, lmin = tr.lmin, J = tr.jump_depth;
+  const uint32_t cap_log2 = tr.jump_cap_log2;
   const uint32_t qmask = qg >= 4 ? 0xFFFFFFFFu : ((1u << (8 * qg)) - 1);
   const unsigned long long jmask = low_bytes_mask(J);
   const uint32_t hmask = (1u << cap_log2) - 1;
   const uint32_t lmax = tr.lmax, C = tr.C;
+  const unsigned long long own_end = p.own + a, n_end = p.n + a;  // in aligned coordinates
+  // this warp's slice of every tile and the sampled positions P = m*S whose
+  // candidates P - d (d < S) can start in it, for a full slice
+  const uint32_t group = warp / kGroupWarps, slice = warp % kGroupWarps;
+  const uint32_t s_lo = slice * kSlice;
+  const uint32_t m0 = (s_lo + S - 1) / S, full_m1 = (s_lo + kSlice + 2 * S - 2) / S;
+  const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, full_safe_hi = (s_lo + kSlice) / S;
+  const uint32_t* s_words = reinterpret_cast<const uint32_t*>(smem);
 
-  for (uint32_t k = 0;; ++k) {
+  for (uint32_t k = group;; k += kGroups) {
     const uint32_t t = blockIdx.x + k * gridDim.x;
     if (t >= p.num_tiles) break;
     const int stage = k % kWStages;
     mbar_wait(&full[stage], (k / kWStages) & 1);
-    const uint8_t* sb = smem + (size_t)stage * kStageBytes;  // sb[x + a] = text[t0 + x]
-    const uint8_t* win = sb + a;
-    const unsigned long long t0 = (unsigned long long)t * kTile;
-    const uint32_t tile_own = (uint32_t)min(p.own - t0, (unsigned long long)kTile);
-    // text bytes available from t0 (clamped; only the last tiles see < 2^31)
-    const uint32_t avail = (uint32_t)min(p.n - t0, 0x7FFFFFFFull);
-    const uint32_t s_lo = warp * kSlice;
-    const uint32_t s_hi = min(s_lo + kSlice, tile_own);
+    const uint8_t* sb = smem + (size_t)stage * kStageBytes;
+    const uint32_t* sw = s_words + (size_t)stage * (kStageBytes / 4);
+    const unsigned long long tA = (unsigned long long)t * kTile;
+    // owned window positions [y_lo, y_hi), valid bytes y < avail
+    const uint32_t y_own_hi = (uint32_t)min(own_end - tA, (unsigned long long)kTile);
+    const uint32_t avail = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);
+    const uint32_t lo = (t == 0 && s_lo < a) ? a : s_lo;  // tile 0 starts at text offset 0
+    const uint32_t s_hi = min(s_lo + kSlice, y_own_hi);
+    const unsigned long long off0 = p.base + tA - a;  // text offset of window position 0
+    uint32_t seg_n = 0;  // hits of this slice written so far (warp-uniform)
+    // sorts the buffered batch and appends it to the warp's staging region;
+    // false if the batch overflowed the buffer (nothing written)
+    auto flush = [&]() -> bool {
+      __syncwarp();
+      const uint32_t nb = s_nh[warp];
+      if (p.mode != 0 || nb == 0) return true;
+      if (nb > kWHits) return false;
+      warp_sort_keys(hk, nb, lane);
+      if (cursor + seg_n + nb <= p.region)
+        for (uint32_t h = lane; h < nb; h += 32) {
+          const unsigned long long key = hk[h];
+          const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
+          DevHit out;
+          out.offset = off0 + s_lo + (key >> 40);
+          out.pid = pid;
+          out.len = __ldg(tr.pid_len + pid);
+          p.staging[region_base + cursor + seg_n + h] = out;
+        }
+      seg_n += nb;
+      __syncwarp();
+      if (lane == 0) s_nh[warp] = 0;
+      __syncwarp();
+      return true;
+    };
+    auto discard = [&]() {  // drop the buffered batch (it will be redone)
+      __syncwarp();
+      if (lane == 0) s_nh[warp] = 0;
+      __syncwarp();
+    };
+    // a single start produced more hits than the buffer holds: count them
+    // (so the host can size the exact fallback) and flag the scan
+    auto overflow = [&]() {
+      __syncwarp();
+      if (lane == 0) {
+        atomicAdd(p.g_count, (unsigned long long)s_nh[warp]);
+        atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
+        s_nh[warp] = 0;
+      }
+      __syncwarp();
+    };
 
-    auto emit = [&](uint32_t x, uint32_t pid) {  // start x (tile-local)
+    auto emit = [&](uint32_t y, uint32_t pid) {
       if (p.mode == 0) {
         const uint32_t slot = atomicAdd(&s_nh[warp], 1u);
-        const unsigned long long key = ((unsigned long long)(x - s_lo) << 40) | pid;
-        if (slot < kWHits) hk[slot] = key;
-        else if (slot - kWHits < kWSpill - kWHits) spill[slot - kWHits] = key;
+        if (slot < kWHits) hk[slot] = ((unsigned long long)(y - s_lo) << 40) | pid;
       } else {
         const unsigned long long slot = atomicAdd(p.g_count + 3, 1ull);
-        if (slot < p.keys_cap) p.keys[slot] = ((p.base + t0 + x) << 24) | pid;
+        if (slot < p.keys_cap) p.keys[slot] = ((off0 + y) << 24) | pid;
       }
     };
-    auto tbyte = [&](uint32_t j) -> uint32_t {  // tile-local j < avail
-      return j + a < kStageBytes ? win[j] : __ldg(p.text + t0 + j);
+    auto tbyte = [&](uint32_t y) -> uint32_t {  // y < avail
+      return y < kStageBytes ? sb[y] : __ldg(p.text + (tA + y - a));
     };
-    auto emit_state = [&](uint32_t x, uint32_t st) {
+    auto emit_state = [&](uint32_t y, uint32_t st) {
       for (uint32_t o = __ldg(tr.out_off + st), oe = __ldg(tr.out_off + st + 1); o < oe; ++o)
-        emit(x, __ldg(tr.out_pid + o));
+        emit(y, __ldg(tr.out_pid + o));
     };
-    // PFAC walk (scan.hpp:142-168) from state st at tile-local byte j
-    auto walk = [&](uint32_t x, uint32_t st, uint32_t j) {
+    // PFAC walk (scan.hpp:142-168) from state st at window byte j
+    auto walk = [&](uint32_t y, uint32_t st, uint32_t j) {
       for (; j < avail; ++j) {
         const uint32_t c = s_cls[tbyte(j)];
         const uint32_t e = kSmemTable ? (uint32_t)T[st * C + c] : (uint32_t)__ldg(T + st * C + c);
         if (!e) break;
         st = e & ET::kMask;
-        if (e & ET::kFlag) emit_state(x, st);
+        if (e & ET::kFlag) emit_state(y, st);
       }
     };
 
+#ifdef GLOP_EXP_NOWORK
+    if (false) {
+#else
     if (kFilter) {
-      // exact check of candidate start x: level-2 bitmap, then the J-byte
+#endif
+      // exact check of candidate start y: level-2 bitmap, then the J-byte
       // jump table (generalised RootJump), then the remaining walk
-      auto candidate = [&](uint32_t x) {
-        const unsigned long long key = win_u64(sb, x + a) & jmask;
-        const uint32_t b = prefix_bit(key);
-        if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
+      auto candidate = [&](uint32_t y) {
+        const unsigned long long key = win_u64(sb, y) & jmask;
+        if (!kSmemHash) {
+          const uint32_t b = prefix_bit(key);
+          if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
+        }
         for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & hmask) {
           const JumpEntry e = H[h];
           if (!e.state1) return;
           if (e.key != key) continue;
           const uint32_t st = e.state1 - 1;
           if (e.out != kOutNone) {
-            if (e.out == kOutMany) emit_state(x, st);
-            else emit(x, e.out);
+            if (e.out == kOutMany) emit_state(y, st);
+            else emit(y, e.out);
           }
-          if (lmax > J) walk(x, st, x + J);
+          if (lmax > J) walk(y, st, y + J);
           return;
         }
       };
-      auto drain = [&](uint32_t qn) {  // queue entries: (P << 8) | dmask
-        for (uint32_t e = lane; e < qn; e += 32) {
-          const uint32_t v = q[e], P = v >> 8;
-          uint32_t dm = v & 0xFFu;
-          while (dm) {
-            const uint32_t d = __ffs(dm) - 1;
-            dm &= dm - 1;
-            candidate(P - d);
+      // queue entries (P << 8) | dmask are in increasing P order, so the
+      // hits of consecutive 32-entry batches are ordered batch to batch:
+      // each batch is sorted and flushed on its own.  A batch that overflows
+      // the buffer is redone one entry at a time.
+      auto drain = [&](uint32_t qn) {
+        for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
+          const uint32_t e = e0 + lane;
+          const uint32_t v = e < qn ? q[e] : 0u;
+          auto run = [&]() {
+            uint32_t dm = v & 0xFFu;
+            while (dm) {
+              const uint32_t d = __ffs(dm) - 1;
+              dm &= dm - 1;
+              candidate((v >> 8) - d);
+            }
+          };
+          run();
+          if (!flush()) {
+            discard();
+            for (uint32_t j = 0; j < 32 && e0 + j < qn; ++j) {
+              if (lane == j) run();
+              if (!flush()) overflow();
+            }
           }
         }
-        __syncwarp();
       };
-      // d-mask of sampled position P with the validity masks applied:
-      // s_lo <= P - d < s_hi, P - d + lmin <= avail, P + q <= avail
-      auto probe = [&](uint32_t P, bool edge) -> uint32_t {
-        if (edge && P + qg > avail) return 0;
-        uint32_t dm = s_dmask[qgram_bucket(win_u32(sb, P + a) & qmask, qg)];
-        if (edge && dm) {
-          if (P - s_lo < 7) dm &= (2u << (P - s_lo)) - 1;
+      auto bucket = [&](uint32_t g) -> uint32_t {
+        return kS ? ((g * 0x9E3779B1u) >> 16) : qgram_bucket(g & qmask, qg);  // kS > 0 implies q = 4
+      };
+      // d-mask of sampled position P restricted to lo <= P - d < s_hi,
+      // P - d + lmin <= avail, P + q <= avail
+      auto probe_edge = [&](uint32_t P) -> uint32_t {
+        if (P + qg > avail) return 0;
+        uint32_t dm = s_dmask[bucket(win_u32(sb, P))];
+        if (dm) {
+          if (P < lo) return 0;
+          if (P - lo < 7) dm &= (2u << (P - lo)) - 1;
           if (P >= s_hi) dm &= ~((2u << min(P - s_hi, 7u)) - 1);
           if (P + lmin > avail) dm = P + lmin - avail > 7 ? 0 : dm & ~((1u << (P + lmin - avail)) - 1);
         }
         return dm;
       };
-      // sampled positions P = m*S (tile-anchored); this warp evaluates the
-      // P whose candidates P - d (d < S) can fall in [s_lo, s_hi)
-      const uint32_t m0 = (s_lo + S - 1) / S, m1 = (s_hi + 2 * S - 2) / S;  // m*S < s_hi + S - 1
-      // positions needing masks: near s_lo (P - s_lo < 7), at/after s_hi,
-      // and everything when the text ends inside this window
-      const bool tail = avail < kTile + 16;
-      const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, safe_hi = s_hi / S;  // [safe_lo, safe_hi) mask-free
       uint32_t qn = 0;
       auto push = [&](uint32_t m, uint32_t dm) {
         const uint32_t bal = __ballot_sync(0xffffffffu, dm != 0);
@@ -489,68 +563,99 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
           qn += __popc(bal);
         }
       };
-      uint32_t base = m0;
-      if (!tail && base < m1) {
-        // one masked chunk covers the leading edge (safe_lo - m0 <= 8 < 32),
-        // then the interior runs mask-free, two positions per lane per step
-        const uint32_t m = base + lane;
-        push(m, m < m1 ? probe(m * S, m < safe_lo || m >= safe_hi) : 0u);
-        for (base += 32; base + 64 <= safe_hi; base += 64) {
-          const uint32_t ma = base + lane, mb = base + 32 + lane;
-          const uint32_t da = probe(ma * S, false), db = probe(mb * S, false);
-          push(ma, da);
-          push(mb, db);
+      const bool fast = lo == s_lo && s_hi == s_lo + kSlice && avail >= kTile + 16;  // full interior slice
+      uint32_t m1, safe_hi;
+      if (fast) {
+        m1 = full_m1;
+        safe_hi = full_safe_hi;
+      } else {
+        m1 = s_hi > lo ? (s_hi + 2 * S - 2) / S : 0;
+        safe_hi = 0;  // everything masked
+      }
+      uint32_t base = s_hi > lo ? (lo + S - 1) / S : m1;
+      if (fast) {
+        // leading edge (< 8 positions) plus alignment to a multiple of 4
+        // positions, masked; the interior is mask-free
+        const uint32_t ia = (safe_lo + 3) & ~3u;
+        for (; base < ia; base += 32) {
+          const uint32_t m = base + lane;
+          const bool in = m < ia;
+          uint32_t dm = 0;
+          if (in) dm = m < safe_lo ? probe_edge(m * S) : s_dmask[bucket(win_u32(sb, m * S))];
+          push(m, dm);
+          if (base + 32 >= ia) {  // shift so the next chunk starts at ia
+            base = ia - 32;
+          }
         }
+        base = ia;
+        if (kS) {
+          // 4 consecutive sampled positions per lane from ceil((3S+4)/4)
+          // word-aligned conflict-free loads; one vote per 128 positions
+          constexpr uint32_t kW = (3 * kS + 4 + 3) / 4;
+          for (; base + 128 <= safe_hi; base += 128) {
+            const uint32_t B = (base + 4 * lane) * kS;  // multiple of 4
+            uint32_t w[kW + 1];
+#pragma unroll
+            for (uint32_t i = 0; i <= kW; ++i) w[i] = sw[B / 4 + i];
+            uint32_t dm[4];
+#pragma unroll
+            for (uint32_t u = 0; u < 4; ++u) {
+              const uint32_t o = u * kS;
+              const uint32_t g = (o & 3) ? __funnelshift_r(w[o / 4], w[o / 4 + 1], 8 * (o & 3)) : w[o / 4];
+              dm[u] = s_dmask[bucket(g)];
+            }
+            const uint32_t cnt = (dm[0] != 0) + (dm[1] != 0) + (dm[2] != 0) + (dm[3] != 0);
+            if (__ballot_sync(0xffffffffu, cnt != 0)) {
+              // queue in position order (lane-major): exclusive warp scan
+              uint32_t pre = cnt;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= (uint32_t)o) pre += x;
+              }
+              const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+              if (qn + tot > kWQueue) {
+                drain(qn);
+                qn = 0;
+              }
+              uint32_t at = qn + pre - cnt;
+#pragma unroll
+              for (uint32_t u = 0; u < 4; ++u)
+                if (dm[u]) q[at++] = ((B + u * kS) << 8) | dm[u];
+              qn += tot;
+              __syncwarp();
+            }
+          }
+        }
+        for (; base + 32 <= safe_hi; base += 32)
+          push(base + lane, s_dmask[bucket(win_u32(sb, (base + lane) * S))]);
       }
       for (; base < m1; base += 32) {
         const uint32_t m = base + lane;
-        const bool edge = tail || m < safe_lo || m >= safe_hi;
-        push(m, m < m1 ? probe(m * S, edge) : 0u);
+        push(m, m < m1 ? probe_edge(m * S) : 0u);
       }
       drain(qn);
-    } else {
+    } else if (!kFilter) {
       // DIRECT: one lane per start byte
-      for (uint32_t x0 = s_lo; x0 < s_hi; x0 += 32)
-        if (x0 + lane < s_hi) walk(x0 + lane, 0u, x0 + lane);
+      for (uint32_t y0 = lo; y0 < s_hi; y0 += 32) {
+        if (y0 + lane < s_hi) walk(y0 + lane, 0u, y0 + lane);
+        if (!flush()) {  // dense batch: one start at a time
+          discard();
+          for (uint32_t j = 0; j < 32 && y0 + j < s_hi; ++j) {
+            if (lane == j) walk(y0 + j, 0u, y0 + j);
+            if (!flush()) overflow();
+          }
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);  // window no longer read
-    const uint32_t nh = s_nh[warp];
-    __syncwarp();
-    if (lane == 0) s_nh[warp] = 0;
-
     if (p.mode == 0) {
-      if (nh) {
-        unsigned long long* keys = hk;
-        if (nh > kWHits) {
-          if (nh > kWSpill) {  // beyond the spill area: global fallback
-            if (lane == 0) atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
-          } else {
-            // dense slice: move the buffered keys behind the spilled ones
-            // and order the whole segment in the warp's global spill area
-            for (uint32_t j = lane; j < kWHits; j += 32) spill[nh - kWHits + j] = hk[j];
-            keys = spill;
-          }
-        }
-        if (nh <= kWSpill) {
-          __syncwarp();
-          warp_sort_keys(keys, nh, lane);
-          if (cursor + nh <= p.region)
-            for (uint32_t h = lane; h < nh; h += 32) {
-              const unsigned long long key = keys[h];
-              const uint32_t pid = (uint32_t)(key & 0xFFFFFFFFFFull);
-              DevHit out;
-              out.offset = p.base + t0 + s_lo + (key >> 40);
-              out.pid = pid;
-              out.len = __ldg(tr.pid_len + pid);
-              p.staging[region_base + cursor + h] = out;
-            }
-          __syncwarp();
-        }
-        if (lane == 0) atomicAdd(p.g_count, (unsigned long long)nh);
+      if (lane == 0) {
+        p.dir[(size_t)t * kGroupWarps + slice] = SegDir{cursor, seg_n};
+        if (seg_n) atomicAdd(p.g_count, (unsigned long long)seg_n);
       }
-      if (lane == 0) p.dir[(size_t)t * kConsumerWarps + warp] = SegDir{cursor, nh};
-      cursor += nh;
+      cursor += seg_n;
     }
   }
   if (p.mode == 0 && lane == 0 && cursor) atomicMax(p.g_count + 2, (unsigned long long)cursor);
@@ -613,7 +718,8 @@ __global__ void __launch_bounds__(1024) seg_gather_kernel(const SegDir* dir, uns
   for (uint32_t i = 0; i < kSegPerThread; ++i) {
     if (!c[i]) continue;
     const unsigned long long seg = b + i;
-    const unsigned long long t = seg / kConsumerWarps, wp = seg % kConsumerWarps;
+    const unsigned long long t = seg / kGroupWarps, sl = seg % kGroupWarps;
+    const unsigned long long wp = ((t / grid) % kGroups) * kGroupWarps + sl;  // warp that ran it
     const unsigned long long src = ((t % grid) * kConsumerWarps + wp) * region + dir[seg].cursor;
     for (uint32_t h = 0; h < c[i]; ++h) out[dst + h] = staging[src + h];
     dst += c[i];

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libglop.so")
+LIB_PATH = os.environ.get("GLOP_LIB") or os.path.join(HERE, "libglop.so")  # GLOP_LIB: experiment builds
 
 HIT_DTYPE = np.dtype([("offset", "<u8"), ("pattern_id", "<u4"), ("matched_len", "<u4")])
 ALERT_DTYPE = np.dtype([("offset", "<u8"), ("rule_id", "<u4"), ("pattern_len", "<u4")])
