@@ -28,7 +28,8 @@ constexpr uint32_t kHalo = 64;              // bytes past the tile kept in smem
 constexpr uint32_t kStageBytes = kTile + kHalo + 16;  // +16: alignment slack
 constexpr int kStages = 4;
 constexpr uint32_t kHitCap = 2048;          // per-tile hit keys in smem
-constexpr uint32_t kDmaskBytes = 65536;     // level-1 q-gram d-mask buckets
+constexpr uint32_t kDmaskBits = 15;         // level-1 q-gram d-mask: 2^15 buckets
+constexpr uint32_t kDmaskBytes = 1u << kDmaskBits;
 constexpr uint32_t kBm2Bits = 1u << 18;     // level-2 prefix bitmap
 constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
 constexpr uint32_t kQueueCap = 4096;        // per-tile filter survivors
@@ -114,9 +115,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ------------------------------------------------------------------ hashing
-// Level-1 bucket of a q-gram packed little-endian (q <= 4).  q <= 2 is exact.
+// Level-1 bucket of a q-gram packed little-endian (q <= 4); q = 1 is exact.
 __host__ __device__ __forceinline__ uint32_t qgram_bucket(uint32_t g, uint32_t q) {
-  return q <= 2 ? g : ((g * 0x9E3779B1u) >> 16);
+  return q == 1 ? g : ((g * 0x9E3779B1u) >> (32 - kDmaskBits));
 }
 // Level-2 bit of an (up to) 8-byte prefix packed little-endian.
 __host__ __device__ __forceinline__ uint32_t prefix_bit(unsigned long long key) {
@@ -220,7 +221,7 @@ __device__ __forceinline__ void sort_keys(unsigned long long* keys, uint32_t P) 
 // ------------------------------------------------------------------ K1 PFAC
 // Shared-memory layout (byte offsets), computed on the host per automaton.
 struct PfacLayout {
-  uint32_t bars, cls, misc, keys, queue, dmask, bm2, hash, table, total;
+  uint32_t bars, cls, misc, keys, queue, cand, dmask, bm2, hash, table, total;
 };
 
 __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -255,17 +256,21 @@ constexpr int kGroups = kConsumerWarps / kGroupWarps;  // tiles in flight per CT
 constexpr uint32_t kSlice = kTile / kGroupWarps;       // 4096 bytes per warp per tile
 constexpr int kWStages = 6;
 constexpr uint32_t kWQueue = 128;  // per-warp filter survivors
-constexpr uint32_t kWHits = 128;   // per-warp hit keys of one drain batch (smem)
+constexpr uint32_t kWHits = 64;    // per-warp hit keys of one drain batch (smem)
+constexpr uint32_t kWCand = 256;   // per-warp candidates of one drain batch (32 x 8)
 
 struct SegDir {
-  uint32_t cursor;  // offset inside the warp's staging region
+  uint32_t cursor;  // offset inside the producing warp's staging region
   uint32_t count;
+  uint32_t region;  // producing warp (global id)
+  uint32_t pad;
 };
 
 struct WarpScanParams {
   const uint8_t* text;
   unsigned long long n, own, base;
   uint32_t num_tiles;
+  uint32_t num_units;            // unused (per-CTA count derived in-kernel)
   int mode;                      // 0 ordered staging; 1 global keys
   DevHit* staging;
   unsigned long long region;     // staging records per (CTA, warp) region
@@ -282,11 +287,12 @@ __host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t has
   uint32_t o = kWStages * kStageBytes;
   L.bars = o; o += 2 * kWStages * 8;
   L.cls = o; o += 256;
-  L.misc = o; o += kConsumerWarps * 4;
+  L.misc = o; o += align16((kConsumerWarps + 1 + kWStages) * 4);
   L.keys = o; o += kConsumerWarps * kWHits * 8;
   L.queue = o; o += filter ? kConsumerWarps * kWQueue * 4 : 0;
+  L.cand = o; o += filter ? kConsumerWarps * kWCand * 2 : 0;
   L.dmask = o; o += filter ? kDmaskBytes : 0;
-  L.bm2 = o; o += (filter && !hash_bytes) ? kBm2Bytes : 0;
+  L.bm2 = o; o += filter ? kBm2Bytes : 0;
   o = align16(o);
   L.hash = o; o += filter ? hash_bytes : 0;
   o = align16(o);
@@ -330,6 +336,11 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
   const JumpEntry* H = kSmemHash ? reinterpret_cast<const JumpEntry*>(smem + L.hash) : tr.jump;
   const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
+  // s_misc: [0, 16) per-warp hit counters, [16] unit counter, [17, 17+NST)
+  // the tile each stage currently holds (written by the producer before the
+  // copy, so a consumer's mbarrier parity wait is never a phase behind)
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
+  volatile uint32_t* s_stage_tile = s_misc + kConsumerWarps + 1;
 
   // ---- stage the automaton (all warps), init barriers
   {
@@ -341,11 +352,12 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
     copy(L.cls, tr.cls, 256);
     if (kFilter) {
       copy(L.dmask, tr.dmask, kDmaskBytes);
+      copy(L.bm2, tr.bm2, kBm2Bytes);
       if (kSmemHash) copy(L.hash, tr.jump, tr.jump_bytes);
-      else copy(L.bm2, tr.bm2, kBm2Bytes);
     }
     if (kSmemTable) copy(L.table, tr.table, tr.table_bytes);
-    if (tid < kConsumerWarps) reinterpret_cast<uint32_t*>(smem + L.misc)[tid] = 0;
+    if (tid <= kConsumerWarps + kWStages)
+      s_misc[tid] = tid < kConsumerWarps ? 0 : (tid == kConsumerWarps ? kConsumerWarps : 0xFFFFFFFFu);
     if (tid == 0) {
       for (int s = 0; s < kWStages; ++s) {
         mbar_init(&full[s], 1);
@@ -357,32 +369,33 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   __syncthreads();
   const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
   Ring ring{smem, full, p.text - a, a, p.n};
+  const uint32_t my_tiles = p.num_tiles > blockIdx.x ? (p.num_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
   if (warp == kConsumerWarps) {
     // ---------------- producer: one lane keeps kWStages tiles in flight
     if (lane == 0)
-      for (uint32_t k = 0;; ++k) {
-        const uint32_t t = blockIdx.x + k * gridDim.x;
-        if (t >= p.num_tiles) break;
+      for (uint32_t k = 0; k < my_tiles; ++k) {
         const int stage = k % kWStages;
         if (k >= (uint32_t)kWStages) {
           mbar_wait(&empty[stage], ((k / kWStages) - 1) & 1);
           fence_proxy_async();
         }
-        ring.issue(stage, t);
+        s_stage_tile[stage] = k;
+        ring.issue(stage, blockIdx.x + k * gridDim.x);
       }
     return;
   }
 
   // ---------------- consumers
-  // Tile-local coordinates are "window" coordinates y: sb[y] holds aligned
-  // byte A[t*kTile + y], i.e. text position t*kTile + y - a.  Tiles own the
-  // text positions [t*kTile - a, (t+1)*kTile - a), so the window is
-  // 16-byte aligned with the tile and every sampled chunk is word-aligned.
+  // Work units u = (CTA tile k = u / kGroupWarps, slice u % kGroupWarps) are
+  // taken dynamically: warp w starts with unit w, then grabs the next free
+  // one.  Window coordinates y: sb[y] = aligned byte A[t*kTile + y] = text
+  // position t*kTile + y - a, so chunks are word aligned.
   uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kWQueue;
-  uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.misc);  // per-warp hit counters
+  uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.cand) + warp * kWCand;
+  uint32_t* s_nh = s_misc;
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.keys) + warp * kWHits;
-  const uint32_t gw = blockIdx.x * kConsumerWarps + warp;  // global warp id
+  const uint32_t gw = blockIdx.x * kConsumerWarps + warp;  // staging region of this warp
   const unsigned long long region_base = (unsigned long long)gw * p.region;
   uint32_t cursor = 0;  // records written into this warp's staging region
   const uint32_t qg = tr.q, S = kS ? kS : tr.stride, lmin = tr.lmin, J = tr.jump_depth;
@@ -391,30 +404,35 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   const unsigned long long jmask = low_bytes_mask(J);
   const uint32_t hmask = (1u << cap_log2) - 1;
   const uint32_t lmax = tr.lmax, C = tr.C;
-  const unsigned long long own_end = p.own + a, n_end = p.n + a;  // in aligned coordinates
-  // this warp's slice of every tile and the sampled positions P = m*S whose
-  // candidates P - d (d < S) can start in it, for a full slice
-  const uint32_t group = warp / kGroupWarps, slice = warp % kGroupWarps;
-  const uint32_t s_lo = slice * kSlice;
-  const uint32_t m0 = (s_lo + S - 1) / S, full_m1 = (s_lo + kSlice + 2 * S - 2) / S;
-  const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, full_safe_hi = (s_lo + kSlice) / S;
+  const unsigned long long own_end = p.own + a, n_end = p.n + a;  // aligned coordinates
   const uint32_t* s_words = reinterpret_cast<const uint32_t*>(smem);
 
-  for (uint32_t k = group;; k += kGroups) {
+  for (uint32_t u = warp; u < my_tiles * kGroupWarps;) {
+    const uint32_t k = u / kGroupWarps, slice = u % kGroupWarps;
     const uint32_t t = blockIdx.x + k * gridDim.x;
-    if (t >= p.num_tiles) break;
     const int stage = k % kWStages;
+    while (s_stage_tile[stage] != k) __nanosleep(32);
     mbar_wait(&full[stage], (k / kWStages) & 1);
     const uint8_t* sb = smem + (size_t)stage * kStageBytes;
     const uint32_t* sw = s_words + (size_t)stage * (kStageBytes / 4);
     const unsigned long long tA = (unsigned long long)t * kTile;
-    // owned window positions [y_lo, y_hi), valid bytes y < avail
     const uint32_t y_own_hi = (uint32_t)min(own_end - tA, (unsigned long long)kTile);
-    const uint32_t avail = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);
+    const uint32_t avail = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);  // valid bytes y < avail
+    const uint32_t s_lo = slice * kSlice;
     const uint32_t lo = (t == 0 && s_lo < a) ? a : s_lo;  // tile 0 starts at text offset 0
     const uint32_t s_hi = min(s_lo + kSlice, y_own_hi);
     const unsigned long long off0 = p.base + tA - a;  // text offset of window position 0
     uint32_t seg_n = 0;  // hits of this slice written so far (warp-uniform)
+
+    auto emit = [&](uint32_t y, uint32_t pid) {
+      if (p.mode == 0) {
+        const uint32_t slot = atomicAdd(&s_nh[warp], 1u);
+        if (slot < kWHits) hk[slot] = ((unsigned long long)(y - s_lo) << 40) | pid;
+      } else {
+        const unsigned long long slot = atomicAdd(p.g_count + 3, 1ull);
+        if (slot < p.keys_cap) p.keys[slot] = ((off0 + y) << 24) | pid;
+      }
+    };
     // sorts the buffered batch and appends it to the warp's staging region;
     // false if the batch overflowed the buffer (nothing written)
     auto flush = [&]() -> bool {
@@ -455,16 +473,6 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       }
       __syncwarp();
     };
-
-    auto emit = [&](uint32_t y, uint32_t pid) {
-      if (p.mode == 0) {
-        const uint32_t slot = atomicAdd(&s_nh[warp], 1u);
-        if (slot < kWHits) hk[slot] = ((unsigned long long)(y - s_lo) << 40) | pid;
-      } else {
-        const unsigned long long slot = atomicAdd(p.g_count + 3, 1ull);
-        if (slot < p.keys_cap) p.keys[slot] = ((off0 + y) << 24) | pid;
-      }
-    };
     auto tbyte = [&](uint32_t y) -> uint32_t {  // y < avail
       return y < kStageBytes ? sb[y] : __ldg(p.text + (tA + y - a));
     };
@@ -488,14 +496,13 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
 #else
     if (kFilter) {
 #endif
-      // exact check of candidate start y: level-2 bitmap, then the J-byte
-      // jump table (generalised RootJump), then the remaining walk
-      auto candidate = [&](uint32_t y) {
+      // level-2 test of candidate start y: the J-byte prefix must hit the
+      // prefix bitmap; survivors probe the jump table (exact, generalised
+      // RootJump, scan.hpp:81-108) and walk the remaining levels.
+      auto check = [&](uint32_t y) {
         const unsigned long long key = win_u64(sb, y) & jmask;
-        if (!kSmemHash) {
-          const uint32_t b = prefix_bit(key);
-          if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
-        }
+        const uint32_t b = prefix_bit(key);
+        if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
         for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & hmask) {
           const JumpEntry e = H[h];
           if (!e.state1) return;
@@ -509,34 +516,51 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
           return;
         }
       };
-      // queue entries (P << 8) | dmask are in increasing P order, so the
+      // Queue entries (P << 8) | dmask are in increasing P order, so the
       // hits of consecutive 32-entry batches are ordered batch to batch:
-      // each batch is sorted and flushed on its own.  A batch that overflows
-      // the buffer is redone one entry at a time.
+      // each batch is expanded into candidates (one per set d bit), checked
+      // 32 at a time, then sorted and flushed.  A batch that overflows the
+      // hit buffer is redone one entry at a time.
       auto drain = [&](uint32_t qn) {
         for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
-          const uint32_t e = e0 + lane;
-          const uint32_t v = e < qn ? q[e] : 0u;
-          auto run = [&]() {
-            uint32_t dm = v & 0xFFu;
+          const uint32_t v = e0 + lane < qn ? q[e0 + lane] : 0u;
+          const uint32_t c = __popc(v & 0xFFu);
+          uint32_t pre = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= (uint32_t)o) pre += x;
+          }
+          const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+          {
+            uint32_t at = pre - c, dm = v & 0xFFu;
             while (dm) {
               const uint32_t d = __ffs(dm) - 1;
               dm &= dm - 1;
-              candidate((v >> 8) - d);
+              cand[at++] = (uint16_t)((v >> 8) - d);
             }
-          };
-          run();
+          }
+          __syncwarp();
+          for (uint32_t c0 = 0; c0 < tot; c0 += 32)
+            if (c0 + lane < tot) check(cand[c0 + lane]);
           if (!flush()) {
             discard();
             for (uint32_t j = 0; j < 32 && e0 + j < qn; ++j) {
-              if (lane == j) run();
+              if (lane == j) {
+                uint32_t dm = v & 0xFFu;
+                while (dm) {
+                  const uint32_t d = __ffs(dm) - 1;
+                  dm &= dm - 1;
+                  check((v >> 8) - d);
+                }
+              }
               if (!flush()) overflow();
             }
           }
         }
       };
       auto bucket = [&](uint32_t g) -> uint32_t {
-        return kS ? ((g * 0x9E3779B1u) >> 16) : qgram_bucket(g & qmask, qg);  // kS > 0 implies q = 4
+        return kS ? ((g * 0x9E3779B1u) >> (32 - kDmaskBits)) : qgram_bucket(g & qmask, qg);  // kS > 0: q = 4
       };
       // d-mask of sampled position P restricted to lo <= P - d < s_hi,
       // P - d + lmin <= avail, P + q <= avail
@@ -563,34 +587,26 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
           qn += __popc(bal);
         }
       };
-      const bool fast = lo == s_lo && s_hi == s_lo + kSlice && avail >= kTile + 16;  // full interior slice
-      uint32_t m1, safe_hi;
-      if (fast) {
-        m1 = full_m1;
-        safe_hi = full_safe_hi;
-      } else {
-        m1 = s_hi > lo ? (s_hi + 2 * S - 2) / S : 0;
-        safe_hi = 0;  // everything masked
-      }
+      // sampled positions P = m*S whose candidates P - d (d < S) can start in
+      // [lo, s_hi): m in [ceil(lo/S), ceil((s_hi+S-1)/S)); positions in
+      // [safe_lo, safe_hi) need no range masks on a full interior slice
+      const bool fast = lo == s_lo && s_hi == s_lo + kSlice && avail >= kTile + 16;
+      const uint32_t m1 = s_hi > lo ? (s_hi + 2 * S - 2) / S : 0;
       uint32_t base = s_hi > lo ? (lo + S - 1) / S : m1;
       if (fast) {
-        // leading edge (< 8 positions) plus alignment to a multiple of 4
-        // positions, masked; the interior is mask-free
+        const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, safe_hi = s_hi / S;
+        // leading edge plus alignment to a multiple of 4 positions, masked
         const uint32_t ia = (safe_lo + 3) & ~3u;
-        for (; base < ia; base += 32) {
+        {
           const uint32_t m = base + lane;
-          const bool in = m < ia;
           uint32_t dm = 0;
-          if (in) dm = m < safe_lo ? probe_edge(m * S) : s_dmask[bucket(win_u32(sb, m * S))];
+          if (m < ia) dm = m < safe_lo ? probe_edge(m * S) : s_dmask[bucket(win_u32(sb, m * S))];
           push(m, dm);
-          if (base + 32 >= ia) {  // shift so the next chunk starts at ia
-            base = ia - 32;
-          }
         }
         base = ia;
         if (kS) {
-          // 4 consecutive sampled positions per lane from ceil((3S+4)/4)
-          // word-aligned conflict-free loads; one vote per 128 positions
+          // 4 consecutive sampled positions per lane from word-aligned,
+          // conflict-free loads; one vote per 128 positions
           constexpr uint32_t kW = (3 * kS + 4 + 3) / 4;
           for (; base + 128 <= safe_hi; base += 128) {
             const uint32_t B = (base + 4 * lane) * kS;  // multiple of 4
@@ -599,10 +615,10 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
             for (uint32_t i = 0; i <= kW; ++i) w[i] = sw[B / 4 + i];
             uint32_t dm[4];
 #pragma unroll
-            for (uint32_t u = 0; u < 4; ++u) {
-              const uint32_t o = u * kS;
+            for (uint32_t v = 0; v < 4; ++v) {
+              const uint32_t o = v * kS;
               const uint32_t g = (o & 3) ? __funnelshift_r(w[o / 4], w[o / 4 + 1], 8 * (o & 3)) : w[o / 4];
-              dm[u] = s_dmask[bucket(g)];
+              dm[v] = s_dmask[bucket(g)];
             }
             const uint32_t cnt = (dm[0] != 0) + (dm[1] != 0) + (dm[2] != 0) + (dm[3] != 0);
             if (__ballot_sync(0xffffffffu, cnt != 0)) {
@@ -620,8 +636,8 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
               }
               uint32_t at = qn + pre - cnt;
 #pragma unroll
-              for (uint32_t u = 0; u < 4; ++u)
-                if (dm[u]) q[at++] = ((B + u * kS) << 8) | dm[u];
+              for (uint32_t v = 0; v < 4; ++v)
+                if (dm[v]) q[at++] = ((B + v * kS) << 8) | dm[v];
               qn += tot;
               __syncwarp();
             }
@@ -649,14 +665,17 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);  // window no longer read
-    if (p.mode == 0) {
-      if (lane == 0) {
-        p.dir[(size_t)t * kGroupWarps + slice] = SegDir{cursor, seg_n};
+    uint32_t next = 0;
+    if (lane == 0) {
+      mbar_arrive(&empty[stage]);  // this slice of the window is no longer read
+      if (p.mode == 0) {
+        p.dir[(size_t)t * kGroupWarps + slice] = SegDir{cursor, seg_n, gw, 0};
         if (seg_n) atomicAdd(p.g_count, (unsigned long long)seg_n);
       }
-      cursor += seg_n;
+      next = atomicAdd(&s_misc[kConsumerWarps], 1u);
     }
+    cursor += seg_n;
+    u = __shfl_sync(0xffffffffu, next, 0);
   }
   if (p.mode == 0 && lane == 0 && cursor) atomicMax(p.g_count + 2, (unsigned long long)cursor);
 }
@@ -718,9 +737,7 @@ __global__ void __launch_bounds__(1024) seg_gather_kernel(const SegDir* dir, uns
   for (uint32_t i = 0; i < kSegPerThread; ++i) {
     if (!c[i]) continue;
     const unsigned long long seg = b + i;
-    const unsigned long long t = seg / kGroupWarps, sl = seg % kGroupWarps;
-    const unsigned long long wp = ((t / grid) % kGroups) * kGroupWarps + sl;  // warp that ran it
-    const unsigned long long src = ((t % grid) * kConsumerWarps + wp) * region + dir[seg].cursor;
+    const unsigned long long src = (unsigned long long)dir[seg].region * region + dir[seg].cursor;
     for (uint32_t h = 0; h < c[i]; ++h) out[dst + h] = staging[src + h];
     dst += c[i];
   }
