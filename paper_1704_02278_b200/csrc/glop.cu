@@ -189,7 +189,7 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   const bool filter = kind != GLOP_PFAC_DIRECT;
   // tiles are aligned to the 16-byte granule holding the text start
   const uint32_t num_tiles = (uint32_t)((own + ((uintptr_t)d_text & 15) + kTile - 1) / kTile);
-  const unsigned long long nseg = (unsigned long long)num_tiles * kGroupWarps;
+  const unsigned long long nseg = num_tiles;
   const uint32_t nb = (uint32_t)((nseg + kSegPerBlock - 1) / kSegPerBlock);
   const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
   const unsigned long long regions = (unsigned long long)grid * kConsumerWarps;

@@ -23,7 +23,7 @@
 namespace glop {
 
 constexpr int kThreads = 512;
-constexpr uint32_t kTile = 16384;           // owned start positions per tile
+constexpr uint32_t kTile = 4096;            // owned start positions per tile
 constexpr uint32_t kHalo = 64;              // bytes past the tile kept in smem
 constexpr uint32_t kStageBytes = kTile + kHalo + 16;  // +16: alignment slack
 constexpr int kStages = 4;
@@ -139,7 +139,9 @@ struct Ring {
   unsigned long long n;
 
   __device__ void issue(int stage, uint32_t t) const {  // one thread
-    uint8_t* dst = stages + (size_t)stage * kStageBytes;
+    issue_to(stages + (size_t)stage * kStageBytes, &bars[stage], t);
+  }
+  __device__ void issue_to(uint8_t* dst, uint64_t* bar, uint32_t t) const {  // one thread
     const unsigned long long lo = (unsigned long long)t * kTile;
     const unsigned long long hi = lo + kStageBytes;
     const unsigned long long vlo = lo > a ? lo : a;               // valid data
@@ -149,10 +151,10 @@ struct Ring {
     for (unsigned long long x = vlo; x < tlo && x < vhi; ++x) dst[x - lo] = A[x];
     for (unsigned long long x = thi > vlo ? thi : vlo; x < vhi; ++x) dst[x - lo] = A[x];
     if (thi > tlo) {
-      mbar_arrive_tx(&bars[stage], (uint32_t)(thi - tlo));
-      bulk_g2s(dst + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), &bars[stage]);
+      mbar_arrive_tx(bar, (uint32_t)(thi - tlo));
+      bulk_g2s(dst + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), bar);
     } else {
-      mbar_arrive(&bars[stage]);
+      mbar_arrive(bar);
     }
   }
 };
@@ -241,20 +243,18 @@ __host__ __device__ __forceinline__ uint32_t jump_slot(unsigned long long key, u
   return (uint32_t)((key * 0xD6E8FEB86659FD93ull) >> (64 - cap_log2));
 }
 
-// ------------------------------------------------------------------ K1 (warp-specialised)
-// One producer warp streams 16 KB tiles HBM -> shared memory with TMA bulk
-// copies through a ring of kWStages stages (full/empty mbarriers).  The
-// consumer warps form kGroups groups of kGroupWarps; group g takes the CTA's
-// tiles k = g, g + kGroups, ... and each of its warps owns a 4 KB slice of the
-// tile, which it runs end to end with no CTA-wide barrier: filter,
-// candidates, exact check, ordering of its hits, write-out into its private
-// staging region, and one directory record per (tile, slice) segment.
+// ------------------------------------------------------------------ K1 (per-warp pipelines)
+// Sixteen warps per CTA, one CTA per SM.  The CTA takes a contiguous range of
+// 4 KB tiles; each warp grabs tiles from it (shared-memory counter) and
+// double-buffers them privately: lane 0 issues the TMA bulk copy of the next
+// tile into the warp's idle buffer (own mbarrier) while the warp scans the
+// current one.  No two warps ever wait for each other.  A warp runs its tile
+// end to end: q-gram filter, candidate queue, exact check, ordering of its
+// hits, write-out into its private staging region, and one directory record
+// per tile.
 constexpr int kConsumerWarps = 16;
-constexpr int kWarpKernelThreads = (kConsumerWarps + 1) * 32;
-constexpr int kGroupWarps = 4;                        // warps sharing one tile
-constexpr int kGroups = kConsumerWarps / kGroupWarps;  // tiles in flight per CTA
-constexpr uint32_t kSlice = kTile / kGroupWarps;       // 4096 bytes per warp per tile
-constexpr int kWStages = 6;
+constexpr int kWarpKernelThreads = kConsumerWarps * 32;
+constexpr int kWBuf = 2;           // private tile buffers per warp (double buffering)
 constexpr uint32_t kWQueue = 128;  // per-warp filter survivors
 constexpr uint32_t kWHits = 64;    // per-warp hit keys of one drain batch (smem)
 constexpr uint32_t kWCand = 256;   // per-warp candidates of one drain batch (32 x 8)
@@ -274,7 +274,7 @@ struct WarpScanParams {
   int mode;                      // 0 ordered staging; 1 global keys
   DevHit* staging;
   unsigned long long region;     // staging records per (CTA, warp) region
-  SegDir* dir;                   // num_tiles * kGroupWarps
+  SegDir* dir;                   // one record per tile
   unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
@@ -284,10 +284,10 @@ struct WarpScanParams {
 // memory behind the level-2 bitmap kept in shared memory.
 __host__ __device__ inline PfacLayout make_warp_layout(bool filter, uint32_t hash_bytes, uint32_t table_bytes) {
   PfacLayout L;
-  uint32_t o = kWStages * kStageBytes;
-  L.bars = o; o += 2 * kWStages * 8;
+  uint32_t o = kConsumerWarps * kWBuf * kStageBytes;  // private tile buffers
+  L.bars = o; o += kConsumerWarps * kWBuf * 8;
   L.cls = o; o += 256;
-  L.misc = o; o += align16((kConsumerWarps + 1 + kWStages) * 4);
+  L.misc = o; o += align16((kConsumerWarps + 1) * 4);
   L.keys = o; o += kConsumerWarps * kWHits * 8;
   L.queue = o; o += filter ? kConsumerWarps * kWQueue * 4 : 0;
   L.cand = o; o += filter ? kConsumerWarps * kWCand * 2 : 0;
@@ -329,18 +329,18 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   using ET = EntryTraits<Entry>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
-  uint64_t* empty = full + kWStages;
   const uint8_t* s_cls = smem + L.cls;
   const uint8_t* s_dmask = smem + L.dmask;
   const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
   const JumpEntry* H = kSmemHash ? reinterpret_cast<const JumpEntry*>(smem + L.hash) : tr.jump;
   const Entry* T = kSmemTable ? reinterpret_cast<const Entry*>(smem + L.table) : reinterpret_cast<const Entry*>(tr.table);
-  // s_misc: [0, 16) per-warp hit counters, [16] unit counter, [17, 17+NST)
-  // the tile each stage currently holds (written by the producer before the
-  // copy, so a consumer's mbarrier parity wait is never a phase behind)
+  // s_misc: [0, kConsumerWarps) per-warp hit counters, [kConsumerWarps] next tile
   uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + L.misc);
-  volatile uint32_t* s_stage_tile = s_misc + kConsumerWarps + 1;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars) + warp * kWBuf;
+  uint8_t* bufs = smem + (size_t)warp * kWBuf * kStageBytes;
+  // this CTA's contiguous range of tiles [t_begin, t_end)
+  const uint32_t per = (p.num_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t t_begin = min(blockIdx.x * per, p.num_tiles), t_end = min(t_begin + per, p.num_tiles);
 
   // ---- stage the automaton (all warps), init barriers
   {
@@ -356,41 +356,27 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       if (kSmemHash) copy(L.hash, tr.jump, tr.jump_bytes);
     }
     if (kSmemTable) copy(L.table, tr.table, tr.table_bytes);
-    if (tid <= kConsumerWarps + kWStages)
-      s_misc[tid] = tid < kConsumerWarps ? 0 : (tid == kConsumerWarps ? kConsumerWarps : 0xFFFFFFFFu);
-    if (tid == 0) {
-      for (int s = 0; s < kWStages; ++s) {
-        mbar_init(&full[s], 1);
-        mbar_init(&empty[s], kGroupWarps);
-      }
-      fence_mbar_init();
-    }
+    if (tid <= kConsumerWarps) s_misc[tid] = tid < kConsumerWarps ? 0 : t_begin + kConsumerWarps * kWBuf;
+    if (lane < kWBuf) mbar_init(&bars[lane], 1);
+    if (tid == 0) fence_mbar_init();
   }
   __syncthreads();
   const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
-  Ring ring{smem, full, p.text - a, a, p.n};
-  const uint32_t my_tiles = p.num_tiles > blockIdx.x ? (p.num_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  Ring ring{nullptr, nullptr, p.text - a, a, p.n};
 
-  if (warp == kConsumerWarps) {
-    // ---------------- producer: one lane keeps kWStages tiles in flight
-    if (lane == 0)
-      for (uint32_t k = 0; k < my_tiles; ++k) {
-        const int stage = k % kWStages;
-        if (k >= (uint32_t)kWStages) {
-          mbar_wait(&empty[stage], ((k / kWStages) - 1) & 1);
-          fence_proxy_async();
-        }
-        s_stage_tile[stage] = k;
-        ring.issue(stage, blockIdx.x + k * gridDim.x);
-      }
-    return;
+  // Each warp double-buffers its own tiles: lane 0 keeps kWBuf - 1 tiles in
+  // flight (TMA bulk copies into the warp's private buffers) while the warp
+  // scans the current one.  Tiles come from the CTA's range: the first
+  // kWBuf per warp statically, then the next free one.
+  uint32_t pend[kWBuf];  // tile held / in flight per buffer (t_end = none)
+#pragma unroll
+  for (uint32_t b = 0; b < kWBuf; ++b) {
+    pend[b] = t_begin + warp * kWBuf + b;
+    if (pend[b] >= t_end) pend[b] = t_end;
+    if (lane == 0 && pend[b] < t_end) ring.issue_to(bufs + b * kStageBytes, &bars[b], pend[b]);
   }
+  uint32_t use[kWBuf] = {};  // completed uses per buffer (mbarrier phase)
 
-  // ---------------- consumers
-  // Work units u = (CTA tile k = u / kGroupWarps, slice u % kGroupWarps) are
-  // taken dynamically: warp w starts with unit w, then grabs the next free
-  // one.  Window coordinates y: sb[y] = aligned byte A[t*kTile + y] = text
-  // position t*kTile + y - a, so chunks are word aligned.
   uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kWQueue;
   uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.cand) + warp * kWCand;
   uint32_t* s_nh = s_misc;
@@ -405,24 +391,23 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
   const uint32_t hmask = (1u << cap_log2) - 1;
   const uint32_t lmax = tr.lmax, C = tr.C;
   const unsigned long long own_end = p.own + a, n_end = p.n + a;  // aligned coordinates
-  const uint32_t* s_words = reinterpret_cast<const uint32_t*>(smem);
 
-  for (uint32_t u = warp; u < my_tiles * kGroupWarps;) {
-    const uint32_t k = u / kGroupWarps, slice = u % kGroupWarps;
-    const uint32_t t = blockIdx.x + k * gridDim.x;
-    const int stage = k % kWStages;
-    while (s_stage_tile[stage] != k) __nanosleep(32);
-    mbar_wait(&full[stage], (k / kWStages) & 1);
-    const uint8_t* sb = smem + (size_t)stage * kStageBytes;
-    const uint32_t* sw = s_words + (size_t)stage * (kStageBytes / 4);
+  for (uint32_t b = 0;; b = (b + 1 == kWBuf) ? 0 : b + 1) {
+    const uint32_t t = pend[b];
+    if (t >= t_end) break;
+    mbar_wait(&bars[b], use[b] & 1);
+    ++use[b];
+    // Window coordinates y: sb[y] = aligned byte A[t*kTile + y] = text
+    // position t*kTile + y - a, so chunks are word aligned.
+    const uint8_t* sb = bufs + b * kStageBytes;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
     const unsigned long long tA = (unsigned long long)t * kTile;
-    const uint32_t y_own_hi = (uint32_t)min(own_end - tA, (unsigned long long)kTile);
+    const uint32_t s_hi = (uint32_t)min(own_end - tA, (unsigned long long)kTile);
     const uint32_t avail = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);  // valid bytes y < avail
-    const uint32_t s_lo = slice * kSlice;
-    const uint32_t lo = (t == 0 && s_lo < a) ? a : s_lo;  // tile 0 starts at text offset 0
-    const uint32_t s_hi = min(s_lo + kSlice, y_own_hi);
+    const uint32_t s_lo = 0;
+    const uint32_t lo = t == 0 ? a : 0;  // tile 0 starts at text offset 0
     const unsigned long long off0 = p.base + tA - a;  // text offset of window position 0
-    uint32_t seg_n = 0;  // hits of this slice written so far (warp-uniform)
+    uint32_t seg_n = 0;  // hits of this tile written so far (warp-uniform)
 
     auto emit = [&](uint32_t y, uint32_t pid) {
       if (p.mode == 0) {
@@ -501,8 +486,8 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       // RootJump, scan.hpp:81-108) and walk the remaining levels.
       auto check = [&](uint32_t y) {
         const unsigned long long key = win_u64(sb, y) & jmask;
-        const uint32_t b = prefix_bit(key);
-        if (!((s_bm2[b >> 5] >> (b & 31)) & 1u)) return;
+        const uint32_t bit = prefix_bit(key);
+        if (!((s_bm2[bit >> 5] >> (bit & 31)) & 1u)) return;
         for (uint32_t h = jump_slot(key, cap_log2);; h = (h + 1) & hmask) {
           const JumpEntry e = H[h];
           if (!e.state1) return;
@@ -522,6 +507,9 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       // 32 at a time, then sorted and flushed.  A batch that overflows the
       // hit buffer is redone one entry at a time.
       auto drain = [&](uint32_t qn) {
+#ifdef GLOP_EXP_NODRAIN
+        qn = 0;
+#endif
         for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
           const uint32_t v = e0 + lane < qn ? q[e0 + lane] : 0u;
           const uint32_t c = __popc(v & 0xFFu);
@@ -589,12 +577,12 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
       };
       // sampled positions P = m*S whose candidates P - d (d < S) can start in
       // [lo, s_hi): m in [ceil(lo/S), ceil((s_hi+S-1)/S)); positions in
-      // [safe_lo, safe_hi) need no range masks on a full interior slice
-      const bool fast = lo == s_lo && s_hi == s_lo + kSlice && avail >= kTile + 16;
+      // [safe_lo, safe_hi) need no range masks on a full interior tile
+      const bool fast = lo == 0 && s_hi == kTile && avail >= kTile + 16;
       const uint32_t m1 = s_hi > lo ? (s_hi + 2 * S - 2) / S : 0;
       uint32_t base = s_hi > lo ? (lo + S - 1) / S : m1;
       if (fast) {
-        const uint32_t safe_lo = (s_lo + 7 + S - 1) / S, safe_hi = s_hi / S;
+        const uint32_t safe_lo = (7 + S - 1) / S, safe_hi = kTile / S;
         // leading edge plus alignment to a multiple of 4 positions, masked
         const uint32_t ia = (safe_lo + 3) & ~3u;
         {
@@ -664,18 +652,24 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
         }
       }
     }
+    // buffer b is free: refill it with the next tile of the CTA's range
     __syncwarp();
-    uint32_t next = 0;
+    uint32_t nxt = t_end;
     if (lane == 0) {
-      mbar_arrive(&empty[stage]);  // this slice of the window is no longer read
       if (p.mode == 0) {
-        p.dir[(size_t)t * kGroupWarps + slice] = SegDir{cursor, seg_n, gw, 0};
+        p.dir[t] = SegDir{cursor, seg_n, gw, 0};
         if (seg_n) atomicAdd(p.g_count, (unsigned long long)seg_n);
       }
-      next = atomicAdd(&s_misc[kConsumerWarps], 1u);
+      nxt = atomicAdd(&s_misc[kConsumerWarps], 1u);
+      if (nxt < t_end) {
+        fence_proxy_async();
+        ring.issue_to(bufs + b * kStageBytes, &bars[b], nxt);
+      } else {
+        nxt = t_end;
+      }
     }
+    pend[b] = __shfl_sync(0xffffffffu, nxt, 0);
     cursor += seg_n;
-    u = __shfl_sync(0xffffffffu, next, 0);
   }
   if (p.mode == 0 && lane == 0 && cursor) atomicMax(p.g_count + 2, (unsigned long long)cursor);
 }
