@@ -60,16 +60,18 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kind: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    summary (profiles/), or None."""
+def ncu_traffic(kind: str, tag: str):
+    """dram bytes (read + write) per launch of the dominant kernel from the
+    committed ncu summary (profiles/ncu_summary.json, written by
+    tools/ncu_summarize.py from one `ncu --set full` capture of this
+    workload), or None when no capture of this workload is committed."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             s = json.load(f)
-        return s.get(kind, {}).get("dram_bytes_per_launch"), s.get(kind, {}).get("bytes_per_launch")
+        return s.get(kind, {}).get(tag, {}).get("dram_bytes_per_launch")
     except Exception:
-        return None, None
+        return None
 
 
 class ClockSampler:
@@ -295,7 +297,7 @@ def main():
     value = 8 * total / (ms / 1e3) / 1e9
     peak, peak_src = peaks()
     achieved = sh.own / (kernel_ms / 1e3) / 1e9  # GB/s of the dominant kernel
-    traffic, _ = ncu_traffic("pfac_tile_kernel")
+    traffic = ncu_traffic("pfac_warp_kernel", f"k{args.patterns}") if args.bytes_per_gpu == 8e9 else None
     line = {"metric": METRIC, "value": round(value, 2), "unit": "Gbps", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
@@ -303,7 +305,7 @@ def main():
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "pfac_tile_kernel", "kernel_ms": round(kernel_ms, 4),
+                         "kernel": "pfac_warp_kernel", "kernel_ms": round(kernel_ms, 4),
                          "algorithmic_bytes_per_launch": sh.own,
                          "step_share": round(kernel_ms / ms, 3)},
             "gpu_launches": launches, "clocks": clocks,
@@ -390,7 +392,7 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
                 "workload": "configs[1]: KMP single pattern 'Failed password' over 1 GB synthetic syslog",
                 "bytes_per_gpu": S, "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("kmp_tile_kernel")[0],
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("kmp_tile_kernel", "kmp"),
                          "peak_source": peak_src, "kernel": "kmp_tile_kernel", "kernel_ms": round(kernel_ms, 4)},
             "gpu_launches": launches, "clocks": sampler.summary(), "results": {"matches": int(nm),
                                                                               "comparisons": int(cmp_)}}
