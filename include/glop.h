@@ -65,11 +65,18 @@ typedef struct glop_ctx glop_ctx;
 typedef struct glop_trie glop_trie;
 typedef struct glop_rules glop_rules;
 
-/* PFAC kernel selection.  AUTO picks the q-gram-filtered kernel (the
- * GPU analogue of the reference's RootJump, scan.hpp:81-108); DIRECT is
- * the literal one-thread-per-byte walk (scan.hpp:113-170).  Both are exact
- * and return identical results. */
-typedef enum { GLOP_PFAC_AUTO = 0, GLOP_PFAC_FILTERED = 1, GLOP_PFAC_DIRECT = 2 } glop_pfac_kernel;
+/* PFAC kernel selection.  FILTERED is the general q-gram-filtered kernel
+ * (the GPU analogue of the reference's RootJump, scan.hpp:81-108); PREFIX8
+ * the lean kernel for automata whose outputs all lie at depth >= 8 (8-byte
+ * prefixes: aligned 4-gram sampling + 8-byte key bitmap); DIRECT the literal
+ * one-thread-per-byte walk (scan.hpp:113-170).  AUTO picks PREFIX8 when it
+ * applies, else FILTERED.  All are exact and return identical results. */
+typedef enum {
+  GLOP_PFAC_AUTO = 0,
+  GLOP_PFAC_FILTERED = 1,
+  GLOP_PFAC_DIRECT = 2,
+  GLOP_PFAC_PREFIX8 = 3
+} glop_pfac_kernel;
 
 const char* glop_last_error(void);
 const char* glop_version(void);

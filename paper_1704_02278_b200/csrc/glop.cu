@@ -18,6 +18,7 @@
 
 #include "glop.h"
 #include "glop_kernels.cuh"
+#include "pfac8.cuh"
 #include "logtrawl/automaton.hpp"
 #include "logtrawl/detail/abi.hpp"
 #include "workload.hpp"
@@ -100,6 +101,7 @@ struct glop_trie {
   bool empty = true;      // no outputs: every scan is empty
   bool u16 = true;
   bool smem_filter = false, smem_direct = false, smem_jump = false;
+  bool p8 = false;  // every output at depth >= 8: pfac8_kernel applies
   uint32_t max_pid = 0;
 };
 
@@ -179,6 +181,113 @@ glop_status radix_sort_keys(glop_ctx* c, unsigned long long* in, unsigned long l
   return GLOP_OK;
 }
 
+// pfac8 path (every output at depth >= 8), same contract as below.
+glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_text, uint64_t n,
+                            uint64_t own, uint64_t base, glop_hit* d_out, uint64_t cap, uint64_t* n_hits) {
+  const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
+  const uint32_t num_tiles = (uint32_t)((own + a + kP8Tile - 1) / kP8Tile);
+  const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
+  const uint32_t per = (num_tiles + grid - 1) / grid;
+  const unsigned long long regions = (unsigned long long)grid * kP8Warps;
+  const uint32_t nb = (uint32_t)((num_tiles + kSegPerBlock - 1) / kSegPerBlock);
+  TRY(c->dir.ensure(sizeof(P8Dir) * num_tiles));
+  TRY(c->bcounts.ensure(4ull * nb));
+  TRY(c->prefix.ensure(8ull * nb + 8));
+  TRY(c->misc.ensure(64));
+  unsigned long long region =
+      std::max<unsigned long long>(64, (std::max<uint64_t>(1 << 20, own / 512) + regions - 1) / regions);
+  if (c->staging.bytes < region * regions * sizeof(glop_hit))
+    TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
+  region = c->staging.bytes / sizeof(glop_hit) / regions;
+  const P8Layout L = make_p8_layout();
+  auto* g = c->misc.as<unsigned long long>();
+  auto launch = [&](const P8Params& p) -> glop_status {
+    auto k = t->info.max_depth > 8 ? (t->u16 ? pfac8_kernel<true, uint16_t> : pfac8_kernel<true, uint32_t>)
+                                   : (t->u16 ? pfac8_kernel<false, uint16_t> : pfac8_kernel<false, uint32_t>);
+    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    CU(cudaEventRecord(c->ev0, c->stream));
+    k<<<grid, kP8Threads, L.total, c->stream>>>(t->view, p, L);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev1, c->stream));
+    c->timed = true;
+    ++c->launches;
+    return GLOP_OK;
+  };
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+    P8Params p{};
+    p.text = d_text;
+    p.n = n;
+    p.own = own;
+    p.base = base;
+    p.num_tiles = num_tiles;
+    p.per = per;
+    p.mode = 0;
+    p.staging = reinterpret_cast<DevHit*>(c->staging.p);
+    p.region = region;
+    p.dir = c->dir.as<P8Dir>();
+    p.g_count = g;
+    p.dmask8 = t->view.dmask8;
+    TRY(launch(p));
+    TRY(sync_read(c, c->misc.p, 32));
+    const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[2];
+    const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
+    if (getenv("GLOP_DEBUG"))
+      fprintf(stderr, "pfac8: tiles %u grid %d per %u region %llu -> total %llu flags %u maxregion %llu\n", num_tiles,
+              grid, per, region, total, flags, maxregion);
+    *n_hits = total;
+    if (flags & 1u) {
+      // a drain round produced more hits than the warp's buffer holds: exact
+      // fallback -- global keys, device radix sort
+      if (t->max_pid >= (1u << 24) || base + n >= (1ull << 40))
+        return fail(GLOP_ECAPACITY, "pfac_scan: hit density fallback limited to 2^24 ids / 2^40 bytes");
+      // size the key buffer with a counting pass (keys_cap = 0 counts only)
+      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+      p.mode = 1;
+      p.keys = nullptr;
+      p.keys_cap = 0;
+      TRY(launch(p));
+      TRY(sync_read(c, c->misc.p, 32));
+      const unsigned long long exact_total = c->h_misc[3];
+      *n_hits = exact_total;
+      if (exact_total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
+      TRY(c->keys.ensure(exact_total * 8 + 8));
+      TRY(c->keys_alt.ensure(exact_total * 8 + 8));
+      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+      p.keys = c->keys.as<unsigned long long>();
+      p.keys_cap = exact_total;
+      TRY(launch(p));
+      if (exact_total == 0) return GLOP_OK;
+      TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), exact_total));
+      c->launches += 2;
+      keys_to_hits_kernel<<<std::max<unsigned long long>(1, std::min<unsigned long long>((exact_total + 255) / 256, 4096)),
+                            256, 0, c->stream>>>(c->keys_alt.as<unsigned long long>(), exact_total, t->view.pid_len,
+                                                 reinterpret_cast<DevHit*>(d_out));
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(c->stream));
+      return GLOP_OK;
+    }
+    if (maxregion > region) {  // a warp's staging region overflowed: grow, rerun
+      region = maxregion + maxregion / 4 + 64;
+      c->staging.release();
+      TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
+      continue;
+    }
+    if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
+    if (total == 0) return GLOP_OK;
+    c->launches += 3;
+    p8_reduce_kernel<<<nb, 1024, 0, c->stream>>>(c->dir.as<P8Dir>(), num_tiles, c->bcounts.as<uint32_t>());
+    block_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<uint32_t>(), nb, c->prefix.as<unsigned long long>(),
+                                                   c->prefix.as<unsigned long long>() + nb);
+    p8_gather_kernel<<<nb, 1024, 0, c->stream>>>(c->dir.as<P8Dir>(), num_tiles, c->prefix.as<unsigned long long>(),
+                                                 per, region, reinterpret_cast<const DevHit*>(c->staging.p),
+                                                 reinterpret_cast<DevHit*>(d_out));
+    CU(cudaGetLastError());
+    return GLOP_OK;
+  }
+  return fail(GLOP_ECUDA, "pfac_scan: staging did not converge");
+}
+
 // PFAC over d_text[0, n): starts [0, own), offsets + base, sorted hits to out.
 glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_text,
                                   uint64_t n, uint64_t own, uint64_t base, glop_pfac_kernel kind,
@@ -186,6 +295,10 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   *n_hits = 0;
   if (own > n) return fail(GLOP_EINVAL, "pfac_scan: own > n");
   if (own == 0 || t->empty) return GLOP_OK;
+  if (kind == GLOP_PFAC_PREFIX8 && !t->p8)
+    return fail(GLOP_EINVAL, "pfac_scan: PREFIX8 kernel needs every output at depth >= 8");
+  if ((kind == GLOP_PFAC_AUTO && t->p8) || kind == GLOP_PFAC_PREFIX8)
+    return pfac8_scan_impl(c, t, d_text, n, own, base, d_out, cap, n_hits);
   const bool filter = kind != GLOP_PFAC_DIRECT;
   // tiles are aligned to the 16-byte granule holding the text start
   const uint32_t num_tiles = (uint32_t)((own + ((uintptr_t)d_text & 15) + kTile - 1) / kTile);
@@ -621,6 +734,10 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   const uint32_t J = lmin ? std::min<uint32_t>(lmin, 8) : 1;
   std::vector<uint8_t> dmask(kDmaskBytes, 0);
   std::vector<uint32_t> bm2(kBm2Bits / 32, 0);
+  // pfac8 level 1 (outputs only at depth >= 8): bit d-1 of the bucket of the
+  // 4-gram at offset d (1..4) of every 8-byte root path
+  std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
+  const bool p8 = lmin >= 8;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -663,6 +780,9 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       unsigned long long key = 0;
       for (uint32_t x = 0; x < J; ++x) key |= (unsigned long long)path[x] << (8 * x);
       keys.push_back({key, s});
+      if (p8)
+        for (uint32_t d = 1; d <= 4; ++d)
+          dmask8[qgram_bucket((uint32_t)(key >> (8 * d)), 4)] |= (uint8_t)(1u << (d - 1));
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
     });
@@ -685,7 +805,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   const size_t o_plen = o_pid + up16(std::max<size_t>(pid2.size(), 1) * 4);
   const size_t o_dmask = o_plen + up16(pid_len.size() * 4);
   const size_t o_bm2 = o_dmask + kDmaskBytes;
-  const size_t o_jump = o_bm2 + kBm2Bytes;
+  const size_t o_dmask8 = o_bm2 + kBm2Bytes;
+  const size_t o_jump = o_dmask8 + kP8DmaskBytes;
   const size_t total = o_jump + jump_bytes;
   std::vector<uint8_t> host(total, 0);
   memcpy(&host[o_cls], cls, 256);
@@ -695,6 +816,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   memcpy(&host[o_plen], pid_len.data(), pid_len.size() * 4);
   memcpy(&host[o_dmask], dmask.data(), kDmaskBytes);
   memcpy(&host[o_bm2], bm2.data(), kBm2Bytes);
+  memcpy(&host[o_dmask8], dmask8.data(), kP8DmaskBytes);
   memcpy(&host[o_jump], jump.data(), jump_bytes);
   Dev g(c->device);
   void* mem = nullptr;
@@ -716,6 +838,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.dmask = m + o_dmask;
   t->view.bm2 = reinterpret_cast<const uint32_t*>(m + o_bm2);
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
+  t->view.dmask8 = m + o_dmask8;
+  t->p8 = p8;
   t->view.jump_depth = J;
   t->view.jump_cap_log2 = cap_log2;
   t->view.jump_bytes = (uint32_t)jump_bytes;

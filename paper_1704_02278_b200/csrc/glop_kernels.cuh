@@ -30,7 +30,8 @@ constexpr int kStages = 4;
 constexpr uint32_t kHitCap = 2048;          // per-tile hit keys in smem
 constexpr uint32_t kDmaskBits = 15;         // level-1 q-gram d-mask: 2^15 buckets
 constexpr uint32_t kDmaskBytes = 1u << kDmaskBits;
-constexpr uint32_t kBm2Bits = 1u << 18;     // level-2 prefix bitmap
+constexpr uint32_t kBm2Log2 = 18;
+constexpr uint32_t kBm2Bits = 1u << kBm2Log2;  // level-2 prefix bitmap
 constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
 constexpr uint32_t kQueueCap = 4096;        // per-tile filter survivors
 
@@ -50,6 +51,7 @@ struct DevTrie {
   const uint8_t* dmask;     // kDmaskBytes
   const uint32_t* bm2;      // kBm2Bits / 32 words
   const JumpEntry* jump;    // open-addressed J-byte jump table
+  const uint8_t* dmask8;    // pfac8 level-1 d-masks (lmin >= 8), 2^15 bytes
   uint32_t Q, C, lmin, lmax, q, stride;
   uint32_t table_bytes;     // padded to 16
   uint32_t jump_depth, jump_cap_log2, jump_bytes;
@@ -119,9 +121,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __host__ __device__ __forceinline__ uint32_t qgram_bucket(uint32_t g, uint32_t q) {
   return q == 1 ? g : ((g * 0x9E3779B1u) >> (32 - kDmaskBits));
 }
-// Level-2 bit of an (up to) 8-byte prefix packed little-endian.
+// Level-2 bit of an (up to) 8-byte prefix packed little-endian (lo, hi
+// 32-bit halves): two 32-bit multiplies, cheaper than a 64-bit one on the SM.
+__host__ __device__ __forceinline__ uint32_t prefix_hash32(uint32_t lo, uint32_t hi) {
+  return (lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u);
+}
+__host__ __device__ __forceinline__ uint32_t prefix_bit32(uint32_t lo, uint32_t hi) {
+  return prefix_hash32(lo, hi) >> (32 - kBm2Log2);
+}
 __host__ __device__ __forceinline__ uint32_t prefix_bit(unsigned long long key) {
-  return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 46);
+  return prefix_bit32((uint32_t)key, (uint32_t)(key >> 32));
 }
 __host__ __device__ __forceinline__ unsigned long long low_bytes_mask(uint32_t k) {
   return k >= 8 ? ~0ull : ((1ull << (8 * k)) - 1);

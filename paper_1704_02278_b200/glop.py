@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("GLOP_LIB") or os.path.join(HERE, "libglop.so")  # GLO
 HIT_DTYPE = np.dtype([("offset", "<u8"), ("pattern_id", "<u4"), ("matched_len", "<u4")])
 ALERT_DTYPE = np.dtype([("offset", "<u8"), ("rule_id", "<u4"), ("pattern_len", "<u4")])
 
-PFAC_AUTO, PFAC_FILTERED, PFAC_DIRECT = 0, 1, 2
+PFAC_AUTO, PFAC_FILTERED, PFAC_DIRECT, PFAC_PREFIX8 = 0, 1, 2, 3
 
 
 class GlopError(RuntimeError):

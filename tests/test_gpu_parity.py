@@ -13,7 +13,8 @@ from paper_1704_02278_b200 import glop
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = [glop.PFAC_FILTERED, glop.PFAC_DIRECT]
+# AUTO runs the PREFIX8 kernel whenever every output lies at depth >= 8
+KERNELS = [glop.PFAC_AUTO, glop.PFAC_FILTERED, glop.PFAC_DIRECT]
 
 
 @pytest.fixture(scope="module")
@@ -185,8 +186,38 @@ def test_large_syslog_vs_oracle(ctx, torch_cuda, k):
     trie = ctx.upload(glop.build_failureless_trie(pats, 8))
     ref = O.pfac_scan(text, O.Trie(pats, 8))
     assert len(ref) > 0
-    for kernel in KERNELS:
+    assert trie.info.min_depth >= 8
+    for kernel in KERNELS + [glop.PFAC_PREFIX8]:
         assert dev_scan(ctx, torch_cuda, trie, text, kernel).tobytes() == ref.tobytes()
+
+
+def test_prefix8_shards_and_dense(ctx, torch_cuda):
+    """PREFIX8 kernel: shards with halo == whole == oracle; colliding
+    prefixes (several ids per state); a hit-dense text (exact fallback)."""
+    text = glop.gen_syslog_host(6 << 20, seed=31)
+    pats, _ = glop.gen_rules(300, seed=5)
+    pats += [b"Failed password", b"Failed passwd", b"<38>1 2026-", b"\n<38>1 20"]
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    assert trie.info.min_depth == 8
+    ref = O.pfac_scan(text, O.Trie(pats, 8))
+    whole = dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_PREFIX8)
+    assert whole.tobytes() == ref.tobytes()
+    for shards in (2, 7):
+        S = -(-text.size // shards)
+        parts = []
+        for g in range(shards):
+            lo, hi = g * S, min((g + 1) * S, text.size)
+            rd = min(hi + 7, text.size)
+            parts.append(dev_scan(ctx, torch_cuda, trie, text[lo:rd], glop.PFAC_PREFIX8, own=hi - lo, base=lo))
+        assert np.concatenate(parts).tobytes() == whole.tobytes()
+    dense = np.frombuffer(b"A" * 70000 + b"AAAAAAAAB" + b"A" * 3001, np.uint8)
+    dp = [b"AAAAAAAAx", b"AAAAAAAAy", b"AAAAAAAB", b"AAAAAAAAB"]
+    dtrie = ctx.upload(glop.build_failureless_trie(dp, 8))
+    dref = O.pfac_scan(dense, O.Trie(dp, 8))
+    assert len(dref) > 100000
+    assert dev_scan(ctx, torch_cuda, dtrie, dense, glop.PFAC_PREFIX8).tobytes() == dref.tobytes()
+    with pytest.raises(glop.InvalidArgument):  # PREFIX8 needs depth >= 8 outputs
+        dev_scan(ctx, torch_cuda, ctx.upload(glop.build_failureless_trie([b"AB"], 8)), dense, glop.PFAC_PREFIX8)
 
 
 def test_shards_with_halo_equal_whole(ctx, torch_cuda):
