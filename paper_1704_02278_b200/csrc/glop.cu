@@ -186,16 +186,15 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
                             uint64_t own, uint64_t base, glop_hit* d_out, uint64_t cap, uint64_t* n_hits) {
   const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
   const uint32_t num_tiles = (uint32_t)((own + a + kP8Tile - 1) / kP8Tile);
-  const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
+  const int grid = (int)std::min<uint32_t>((num_tiles + kP8Warps - 1) / kP8Warps, (uint32_t)c->num_sms);
   const uint32_t per = (num_tiles + grid - 1) / grid;
+  const uint32_t sub = (per + kP8Warps - 1) / kP8Warps;
   const unsigned long long regions = (unsigned long long)grid * kP8Warps;
-  const uint32_t nb = (uint32_t)((num_tiles + kSegPerBlock - 1) / kSegPerBlock);
-  TRY(c->dir.ensure(sizeof(P8Dir) * num_tiles));
-  TRY(c->bcounts.ensure(4ull * nb));
-  TRY(c->prefix.ensure(8ull * nb + 8));
+  TRY(c->bcounts.ensure(8 * regions));
+  TRY(c->prefix.ensure(8 * regions));
   TRY(c->misc.ensure(64));
   unsigned long long region =
-      std::max<unsigned long long>(64, (std::max<uint64_t>(1 << 20, own / 512) + regions - 1) / regions);
+      std::max<unsigned long long>(256, (std::max<uint64_t>(1 << 20, own / 512) + regions - 1) / regions);
   if (c->staging.bytes < region * regions * sizeof(glop_hit))
     TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
   region = c->staging.bytes / sizeof(glop_hit) / regions;
@@ -222,10 +221,11 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
     p.base = base;
     p.num_tiles = num_tiles;
     p.per = per;
+    p.sub = sub;
     p.mode = 0;
     p.staging = reinterpret_cast<DevHit*>(c->staging.p);
     p.region = region;
-    p.dir = c->dir.as<P8Dir>();
+    p.counts = c->bcounts.as<unsigned long long>();
     p.g_count = g;
     p.dmask8 = t->view.dmask8;
     TRY(launch(p));
@@ -233,15 +233,13 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
     const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[2];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
     if (getenv("GLOP_DEBUG"))
-      fprintf(stderr, "pfac8: tiles %u grid %d per %u region %llu -> total %llu flags %u maxregion %llu\n", num_tiles,
-              grid, per, region, total, flags, maxregion);
+      fprintf(stderr, "pfac8: tiles %u grid %d per %u sub %u region %llu -> total %llu flags %u maxregion %llu\n",
+              num_tiles, grid, per, sub, region, total, flags, maxregion);
     *n_hits = total;
     if (flags & 1u) {
-      // a drain round produced more hits than the warp's buffer holds: exact
-      // fallback -- global keys, device radix sort
-      if (t->max_pid >= (1u << 24) || base + n >= (1ull << 40))
-        return fail(GLOP_ECAPACITY, "pfac_scan: hit density fallback limited to 2^24 ids / 2^40 bytes");
-      // size the key buffer with a counting pass (keys_cap = 0 counts only)
+      // one lane of a drain round produced more hits than the warp's buffer
+      // holds: exact fallback -- global keys, device radix sort.  A counting
+      // pass (keys_cap = 0) sizes the key buffer.
       CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
       p.mode = 1;
       p.keys = nullptr;
@@ -275,13 +273,12 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
     }
     if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
     if (total == 0) return GLOP_OK;
-    c->launches += 3;
-    p8_reduce_kernel<<<nb, 1024, 0, c->stream>>>(c->dir.as<P8Dir>(), num_tiles, c->bcounts.as<uint32_t>());
-    block_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<uint32_t>(), nb, c->prefix.as<unsigned long long>(),
-                                                   c->prefix.as<unsigned long long>() + nb);
-    p8_gather_kernel<<<nb, 1024, 0, c->stream>>>(c->dir.as<P8Dir>(), num_tiles, c->prefix.as<unsigned long long>(),
-                                                 per, region, reinterpret_cast<const DevHit*>(c->staging.p),
-                                                 reinterpret_cast<DevHit*>(d_out));
+    c->launches += 2;
+    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
+                                                 c->prefix.as<unsigned long long>());
+    p8_gather_kernel<<<(uint32_t)regions, 256, 0, c->stream>>>(
+        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
+        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out));
     CU(cudaGetLastError());
     return GLOP_OK;
   }
@@ -297,7 +294,11 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   if (own == 0 || t->empty) return GLOP_OK;
   if (kind == GLOP_PFAC_PREFIX8 && !t->p8)
     return fail(GLOP_EINVAL, "pfac_scan: PREFIX8 kernel needs every output at depth >= 8");
-  if ((kind == GLOP_PFAC_AUTO && t->p8) || kind == GLOP_PFAC_PREFIX8)
+  // pfac8 keys are (offset << 24 | id): offsets < 2^40, ids < 2^24
+  const bool p8_ok = t->p8 && t->max_pid < (1u << 24) && base + n < (1ull << 40);
+  if (kind == GLOP_PFAC_PREFIX8 && !p8_ok)
+    return fail(GLOP_EINVAL, "pfac_scan: PREFIX8 kernel needs ids < 2^24 and offsets < 2^40");
+  if ((kind == GLOP_PFAC_AUTO && p8_ok) || kind == GLOP_PFAC_PREFIX8)
     return pfac8_scan_impl(c, t, d_text, n, own, base, d_out, cap, n_hits);
   const bool filter = kind != GLOP_PFAC_DIRECT;
   // tiles are aligned to the 16-byte granule holding the text start
@@ -782,7 +783,11 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       keys.push_back({key, s});
       if (p8)
         for (uint32_t d = 1; d <= 4; ++d)
-          dmask8[qgram_bucket((uint32_t)(key >> (8 * d)), 4)] |= (uint8_t)(1u << (d - 1));
+        {
+          const uint32_t g = (uint32_t)(key >> (8 * d));
+          dmask8[p8_h1(g)] |= (uint8_t)(1u << (d - 1));
+          dmask8[p8_h2(g)] |= (uint8_t)(16u << (d - 1));
+        }
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
     });
