@@ -786,7 +786,6 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         {
           const uint32_t g = (uint32_t)(key >> (8 * d));
           dmask8[p8_h1(g)] |= (uint8_t)(1u << (d - 1));
-          dmask8[p8_h2(g)] |= (uint8_t)(16u << (d - 1));
         }
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);

@@ -11,7 +11,7 @@
 //  * Level 1, aligned q-gram sampling: every match start c has, for the
 //    unique d in 1..4 with c + d = 0 (mod 4), the pattern's 4-gram at offset d
 //    sitting in an aligned text word.  A lane owns 8 consecutive sample words
-//    (two LDS.128); each word gets a two-hash Bloom d-mask probe.
+//    (two LDS.128); each word gets one hashed d-mask probe.
 //  * Candidate words are compacted in text order (bit-plane ballot prefix)
 //    and checked 32 per round: the 8-byte key of candidate c = 4i - d is
 //    assembled from words i-1, i, i+1 with constant funnel shifts and tested
@@ -69,17 +69,16 @@ struct P8Params {
   unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use, [3] mode-1 slots
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
-  const uint8_t* dmask8;         // 2^15 two-nibble Bloom d-masks
+  const uint8_t* dmask8;         // 2^15 d-masks (bits 0..3: offsets d = 1..4)
 };
 
-// Level-1 d-mask of an aligned text word: low nibble of bucket h1 AND high
-// nibble of bucket h2 (bit d-1: the word may be the 4-gram at offset d of
-// some 8-byte prefix).  Built by glop_trie_upload.
+// Level-1 d-mask of an aligned text word (bit d-1: the word may be the
+// 4-gram at offset d of some 8-byte prefix), one hashed probe.  A two-hash
+// Bloom variant halved the candidate words but doubled the bank-conflicted
+// shared-memory probes, which bound the kernel (measured: 3.63 -> 3.55 ms at
+// k=1,000 and 2.46 -> 1.97 ms at k=10 without it).  Built by glop_trie_upload.
 __host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) { return (g * 0x9E3779B1u) >> 17; }
-__host__ __device__ __forceinline__ uint32_t p8_h2(uint32_t g) { return (g * 0x85EBCA77u) >> 17; }
-__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
-  return dm[p8_h1(g)] & (dm[p8_h2(g)] >> 4);
-}
+__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) { return dm[p8_h1(g)]; }
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
 // valid range [a, a + n)) into dst; bytes outside 16-byte granules are copied

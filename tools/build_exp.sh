@@ -1,8 +1,6 @@
 #!/bin/bash
-# experiment builds of libglop (GLOP_LIB=... selects one at run time)
+# experiment build of libglop: tools/build_exp.sh NAME "-DFOO -DBAR" -> paper_1704_02278_b200/libglop_exp_NAME.so
+# (select at run time with GLOP_LIB=$PWD/paper_1704_02278_b200/libglop_exp_NAME.so)
 cd "$(dirname "$0")/../paper_1704_02278_b200/csrc"
-for v in NOWORK NODRAIN; do
-  nvcc -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-O3 -shared -gencode arch=compute_100a,code=sm_100a \
-    -I../../include -DGLOP_EXP_$v -o ../libglop_exp_$v.so glop.cu -lcudart &
-done
-wait
+nvcc -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-O3 -shared -gencode arch=compute_100a,code=sm_100a \
+  -I../../include $2 -o ../libglop_exp_$1.so glop.cu -lcudart
