@@ -88,7 +88,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -297,7 +297,8 @@ def main():
     value = 8 * total / (ms / 1e3) / 1e9
     peak, peak_src = peaks()
     achieved = sh.own / (kernel_ms / 1e3) / 1e9  # GB/s of the dominant kernel
-    traffic = ncu_traffic("pfac_warp_kernel", f"k{args.patterns}") if args.bytes_per_gpu == 8e9 else None
+    kname = "pfac8_kernel" if info.min_depth >= 8 and args.kernel == "auto" else "pfac_warp_kernel"
+    traffic = ncu_traffic(kname, f"k{args.patterns}") if args.bytes_per_gpu == 8e9 else None
     line = {"metric": METRIC, "value": round(value, 2), "unit": "Gbps", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
@@ -305,7 +306,7 @@ def main():
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "pfac_warp_kernel", "kernel_ms": round(kernel_ms, 4),
+                         "kernel": kname, "kernel_ms": round(kernel_ms, 4),
                          "algorithmic_bytes_per_launch": sh.own,
                          "step_share": round(kernel_ms / ms, 3)},
             "gpu_launches": launches, "clocks": clocks,
@@ -392,8 +393,8 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
                 "workload": "configs[1]: KMP single pattern 'Failed password' over 1 GB synthetic syslog",
                 "bytes_per_gpu": S, "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("kmp_tile_kernel", "kmp"),
-                         "peak_source": peak_src, "kernel": "kmp_tile_kernel", "kernel_ms": round(kernel_ms, 4)},
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic("kmp2_kernel", "kmp"),
+                         "peak_source": peak_src, "kernel": "kmp2_kernel", "kernel_ms": round(kernel_ms, 4)},
             "gpu_launches": launches, "clocks": sampler.summary(), "results": {"matches": int(nm),
                                                                               "comparisons": int(cmp_)}}
     if rank == 0 and world == 1 and not args.no_cpu:

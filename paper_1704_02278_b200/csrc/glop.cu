@@ -19,6 +19,7 @@
 #include "glop.h"
 #include "glop_kernels.cuh"
 #include "pfac8.cuh"
+#include "kmp.cuh"
 #include "logtrawl/automaton.hpp"
 #include "logtrawl/detail/abi.hpp"
 #include "workload.hpp"
@@ -85,7 +86,7 @@ struct glop_ctx {
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
   DBuf text, staging, out, dir, prefix, misc, keys, keys_alt, cub_tmp;
-  DBuf keep, bcounts, bprefix, alerts, kmp_dfa, kmp_cls, spill;
+  DBuf keep, bcounts, bprefix, alerts, kmp_dfa, spill;
   unsigned long long* h_misc = nullptr;  // pinned readback
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
   bool timed = false;
@@ -379,29 +380,12 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
   return fail(GLOP_ECUDA, "pfac_scan: staging did not converge");
 }
 
-// KMP DFA (see glop_kernels.cuh): replays kmp.hpp:52-66 for each (state, class).
-void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::vector<uint8_t>& cls,
-                   uint32_t& C, std::vector<uint32_t>& dfa) {
-  cls.assign(256, 0);
-  bool used[256] = {};
-  for (uint32_t i = 0; i < m; ++i) used[p[i]] = true;
-  C = 1;
-  int rep[257];
-  int other = -1;
-  for (int b = 0; b < 256; ++b) {
-    if (used[b]) {
-      rep[C] = b;
-      cls[b] = (uint8_t)C++;
-    } else if (other < 0) {
-      other = b;
-    }
-  }
-  rep[0] = other;  // -1 if all bytes occur (class 0 then unused)
-  dfa.assign((size_t)m * C, 0);
+// KMP DFA (see kmp.cuh): replays kmp.hpp:52-66 for each (state, byte):
+// next state | match << 13 | comparisons << 14.
+void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::vector<uint32_t>& dfa) {
+  dfa.assign((size_t)m * 256, 0);
   for (uint32_t j0 = 0; j0 < m; ++j0)
-    for (uint32_t c = 0; c < C; ++c) {
-      if (rep[c] < 0) continue;
-      const uint8_t b = (uint8_t)rep[c];
+    for (uint32_t b = 0; b < 256; ++b) {
       uint32_t j = j0, cmp = 0, match = 0;
       for (;;) {
         ++cmp;
@@ -418,7 +402,7 @@ void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::
           break;
         }
       }
-      dfa[(size_t)j0 * C + c] = j | (match << 13) | (cmp << 14);
+      dfa[(size_t)j0 * 256 + b] = j | (match << 13) | (cmp << 14);
     }
 }
 
@@ -430,78 +414,77 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
   if (own > n) return fail(GLOP_EINVAL, "kmp_search: own > n");
   if (m == 0 || n < m || own == 0) return GLOP_OK;  // kmp.hpp:50
   if (m >= 8192) return fail(GLOP_EINVAL, "kmp_search: pattern longer than 8191 bytes");
-  for (uint32_t i = 0; i < m; ++i)
-    if (fail_tab[i] > i) return fail(GLOP_EINVAL, "kmp_search: bad failure table");
-  std::vector<uint8_t> cls;
+  // chunks resynchronise from the previous m-1 bytes, which is exact for the
+  // pattern's own prefix function (kmp.hpp:25-36); reject any other table
+  for (uint32_t i = 0, k = 0; i < m; ++i) {
+    if (i > 0) {
+      while (k > 0 && pat[i] != pat[k]) k = fail_tab[k - 1];
+      if (pat[i] == pat[k]) ++k;
+    }
+    if (fail_tab[i] != (i ? k : 0u))
+      return fail(GLOP_EINVAL, "kmp_search: failure table is not the pattern's prefix function");
+  }
   std::vector<uint32_t> dfa;
-  uint32_t C = 0;
-  build_kmp_dfa(pat, m, fail_tab, cls, C, dfa);
-  const uint32_t words = (uint32_t)((dfa.size() + 3) & ~size_t(3));
-  dfa.resize(words, 0);
-  TRY(c->kmp_dfa.ensure(words * 4));
-  TRY(c->kmp_cls.ensure(256));
-  CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), words * 4, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemcpyAsync(c->kmp_cls.p, cls.data(), 256, cudaMemcpyHostToDevice, c->stream));
-  const uint32_t num_tiles = (uint32_t)((own + kKmpTile - 1) / kKmpTile);
+  build_kmp_dfa(pat, m, fail_tab, dfa);
+  TRY(c->kmp_dfa.ensure(dfa.size() * 4));
+  CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), dfa.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  const uint64_t end_lim = std::min<uint64_t>(own + m - 1, n);  // starts < own
+  const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
+  const uint32_t num_tiles = (uint32_t)((end_lim + a + kK2Tile - 1) / kK2Tile);
   TRY(c->dir.ensure(sizeof(TileDir) * num_tiles));
   TRY(c->prefix.ensure(sizeof(unsigned long long) * num_tiles));
   TRY(c->misc.ensure(64));
   size_t want = std::max<size_t>(1 << 20, own / 1024);
   if (c->staging.bytes < want * 8) TRY(c->staging.ensure(want * 8));
   auto* g_count = c->misc.as<unsigned long long>();
-  const bool smem_dfa = KmpSmem::kDfa + (size_t)words * 4 <= kSmemMax;
-  const size_t smem = KmpSmem::kDfa + (smem_dfa ? (size_t)words * 4 : 0);
+  const bool smem_dfa = m <= kK2SmemDfaMax;
+  const size_t smem = K2Smem::kDfa + (smem_dfa ? (size_t)m * 1024 : 0);
   const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
+  auto launch = [&](const K2Params& p) -> glop_status {
+    auto k = smem_dfa ? kmp2_kernel<true> : kmp2_kernel<false>;
+    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaEventRecord(c->ev0, c->stream));
+    k<<<grid, kK2Threads, smem, c->stream>>>(p);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev1, c->stream));
+    c->timed = true;
+    ++c->launches;
+    return GLOP_OK;
+  };
   for (int attempt = 0; attempt < 3; ++attempt) {
     CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
-    KmpParams p{};
+    K2Params p{};
     p.text = d_text;
     p.n = n;
-    p.own = own;
+    p.end_lim = end_lim;
     p.base = base;
     p.m = m;
-    p.C = C;
     p.num_tiles = num_tiles;
-    p.dfa = c->kmp_dfa.as<uint32_t>();
-    p.cls = c->kmp_cls.as<uint8_t>();
-    p.dfa_words = words;
     p.p0 = pat[0];
+    p.dfa = c->kmp_dfa.as<uint32_t>();
     p.staging = c->staging.as<unsigned long long>();
     p.staging_cap = c->staging.bytes / 8;
     p.g_count = g_count;
     p.dir = c->dir.as<TileDir>();
     p.g_flags = reinterpret_cast<unsigned int*>(g_count + 1);
     p.comparisons = g_count + 2;
-    CU(cudaEventRecord(c->ev0, c->stream));
-    if (smem_dfa) {
-      CU(cudaFuncSetAttribute(kmp_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kmp_tile_kernel<true><<<grid, kThreads, smem, c->stream>>>(p);
-    } else {
-      CU(cudaFuncSetAttribute(kmp_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kmp_tile_kernel<false><<<grid, kThreads, smem, c->stream>>>(p);
-    }
-    CU(cudaGetLastError());
-    CU(cudaEventRecord(c->ev1, c->stream));
-    c->timed = true;
-    ++c->launches;
+    TRY(launch(p));
     TRY(sync_read(c, c->misc.p, 24));
     const unsigned long long total = c->h_misc[0];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
     *n_offsets = total;
     if (comparisons) *comparisons += c->h_misc[2];
     if (flags & 1u) {
-      // > kKmpHitCap matches in one tile: exact fallback -- every match as a
+      // > kK2HitCap matches in one tile: exact fallback -- every match as a
       // global key, then a device radix sort.
       if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
-      TRY(c->keys.ensure(total * 8));
+      TRY(c->keys.ensure(total * 8 + 8));
       CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
       p.mode = 1;
       p.keys = c->keys.as<unsigned long long>();
       p.keys_cap = total;
       p.comparisons = g_count + 3;  // already counted by the first pass
-      if (smem_dfa) kmp_tile_kernel<true><<<grid, kThreads, smem, c->stream>>>(p);
-      else kmp_tile_kernel<false><<<grid, kThreads, smem, c->stream>>>(p);
-      CU(cudaGetLastError());
+      TRY(launch(p));
       TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), total));
       CU(cudaStreamSynchronize(c->stream));
       return GLOP_OK;
@@ -514,10 +497,9 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
     }
     if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
     if (total == 0) return GLOP_OK;
-    ++c->launches;
+    c->launches += 2;
     tile_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->dir.as<TileDir>(), num_tiles,
                                                   c->prefix.as<unsigned long long>());
-    ++c->launches;
     gather_kernel<unsigned long long>
         <<<std::min<uint32_t>((num_tiles + 7) / 8, 4 * c->num_sms), 256, 0, c->stream>>>(
             c->dir.as<TileDir>(), c->prefix.as<unsigned long long>(), num_tiles,
@@ -630,7 +612,7 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
-                  &c->kmp_dfa, &c->kmp_cls, &c->spill})
+                  &c->kmp_dfa, &c->spill})
     b->release();
   cudaFreeHost(c->h_misc);
   if (c->ev0) cudaEventDestroy(c->ev0);

@@ -1,6 +1,6 @@
 // glop_kernels.cuh -- sm_100a device code for the GLoP matching path.
 //
-//   pfac_tile_kernel  K1  PFAC scan (scan.hpp:113-202), two variants:
+//   pfac_warp_kernel  K1  PFAC scan (scan.hpp:113-202), two variants:
 //                         FILTERED: sampled q-gram filter + 8-byte prefix
 //                         bitmap in shared memory, then the trie walk only for
 //                         survivors (GPU analogue of RootJump, scan.hpp:81-108)
@@ -8,8 +8,7 @@
 //   tile_prefix / gather  K2  deterministic (offset, pattern_id) order
 //                         (scan.hpp:197-201) without a global sort
 //   verify_*          K3  stage-2 suffix check (verify.hpp:69-105)
-//   kmp_tile_kernel   K4  chunk-parallel KMP with (m-1)-byte warm-up
-//                         (kmp.hpp:41-69), exact comparison counts
+//   (K4 KMP: kmp.cuh; the 8-byte-prefix PFAC fast path: pfac8.cuh)
 //   gen_syslog_kernel     synthetic corpus (bench input, not the path)
 //
 // Text is streamed HBM -> shared memory with 1-D TMA bulk copies
@@ -932,185 +931,7 @@ __global__ void keys_to_alerts_kernel(const unsigned long long* keys, unsigned l
   }
 }
 
-// ------------------------------------------------------------------ K4 KMP
-// DFA entry for (state j, class c): next state (13 bits) | match << 13 |
-// comparisons << 14, replaying the reference loop (kmp.hpp:52-66) exactly.
-constexpr uint32_t kKmpChunk = 132;  // 33 words: lane-private banks
-constexpr uint32_t kKmpTile = kKmpChunk * kThreads;  // 67584 owned bytes
-constexpr uint32_t kKmpPre = 256;    // warm-up bytes kept before the tile
-constexpr uint32_t kKmpStageBytes = kKmpPre + kKmpTile + 16;
-constexpr int kKmpStages = 2;
-constexpr uint32_t kKmpHitCap = 2048;
-
-struct KmpParams {
-  const uint8_t* text;
-  unsigned long long n, own, base;
-  uint32_t m, C, num_tiles;
-  const uint32_t* dfa;  // m x C
-  const uint8_t* cls;   // 256
-  uint32_t dfa_words;   // padded to 4
-  uint32_t first_class; // class of p[0]
-  uint32_t p0;          // p[0]
-  unsigned long long* staging;
-  unsigned long long staging_cap;
-  unsigned long long* g_count;
-  TileDir* dir;
-  unsigned int* g_flags;
-  unsigned long long* comparisons;
-  int mode;                    // 0: per-tile order; 1: global keys (fallback)
-  unsigned long long* keys;    // mode 1: start offsets
-  unsigned long long keys_cap;
-};
-
-struct KmpSmem {
-  static constexpr uint32_t kBars = kKmpStages * kKmpStageBytes;
-  static constexpr uint32_t kCls = kBars + kKmpStages * 8;
-  static constexpr uint32_t kMisc = kCls + 256;
-  static constexpr uint32_t kKeys = kMisc + 16;
-  static constexpr uint32_t kDfa = kKeys + kKmpHitCap * 8;
-};
-
-template <bool kSmemDfa>
-__global__ void __launch_bounds__(kThreads, 1) kmp_tile_kernel(const KmpParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int tid = threadIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KmpSmem::kBars);
-  uint8_t* s_cls = smem + KmpSmem::kCls;
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + KmpSmem::kMisc);
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + KmpSmem::kKeys);
-  uint32_t* s_dfa = reinterpret_cast<uint32_t*>(smem + KmpSmem::kDfa);
-  if (tid < 16) reinterpret_cast<uint4*>(s_cls)[tid] = reinterpret_cast<const uint4*>(p.cls)[tid];
-  if (kSmemDfa)
-    for (uint32_t i = tid; i < p.dfa_words / 4; i += kThreads)
-      reinterpret_cast<uint4*>(s_dfa)[i] = reinterpret_cast<const uint4*>(p.dfa)[i];
-  if (tid == 0) {
-    for (int s = 0; s < kKmpStages; ++s) mbar_init(&bars[s], 1);
-    s_misc[0] = 0;
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint32_t* D = kSmemDfa ? s_dfa : p.dfa;
-  const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
-  const uint8_t* A = p.text - a;
-  // stage holds A[t*kKmpTile + a - kKmpPre .. ) rounded down to 16: text
-  // position x lives at win[x - wbase]
-  auto issue = [&](int stage, uint32_t t) {
-    uint8_t* dst = smem + (size_t)stage * kKmpStageBytes;
-    const long long lo_s = (long long)t * kKmpTile + a - kKmpPre;  // A coords, 16-aligned
-    const unsigned long long lo = lo_s < 0 ? 0 : (unsigned long long)lo_s;
-    const unsigned long long dst_off = (unsigned long long)(lo_s < 0 ? -lo_s : 0);
-    const unsigned long long hi = (unsigned long long)(lo_s + kKmpStageBytes);
-    const unsigned long long vlo = lo > a ? lo : a, vhi = hi < a + p.n ? hi : a + p.n;
-    unsigned long long tlo = (vlo + 15) & ~15ull, thi = vhi & ~15ull;
-    if (thi < tlo) thi = tlo;
-    for (unsigned long long x = vlo; x < tlo && x < vhi; ++x) dst[dst_off + x - lo] = A[x];
-    for (unsigned long long x = thi > vlo ? thi : vlo; x < vhi; ++x) dst[dst_off + x - lo] = A[x];
-    if (thi > tlo) {
-      mbar_arrive_tx(&bars[stage], (uint32_t)(thi - tlo));
-      bulk_g2s(dst + dst_off + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), &bars[stage]);
-    } else {
-      mbar_arrive(&bars[stage]);
-    }
-  };
-  if (tid == 0)
-    for (int k = 0; k < kKmpStages; ++k) {
-      uint32_t t = blockIdx.x + k * gridDim.x;
-      if (t < p.num_tiles) issue(k, t);
-    }
-  unsigned long long cmp_total = 0;
-  const uint32_t p0x4 = p.p0 * 0x01010101u;
-  for (uint32_t k = 0;; ++k) {
-    const uint32_t t = blockIdx.x + k * gridDim.x;
-    if (t >= p.num_tiles) break;
-    const int stage = k % kKmpStages;
-    mbar_wait(&bars[stage], (k / kKmpStages) & 1);
-    const uint8_t* win = smem + (size_t)stage * kKmpStageBytes;
-    const unsigned long long t0 = (unsigned long long)t * kKmpTile;
-    // win index of text position x: x - t0 + kKmpPre
-    const unsigned long long c0 = t0 + (unsigned long long)tid * kKmpChunk;
-    const unsigned long long c1 = min(c0 + kKmpChunk, p.own);
-    if (c0 < c1) {
-      auto tbyte = [&](unsigned long long x) -> uint32_t {
-        long long li = (long long)(x - t0) + kKmpPre;
-        return (li >= 0 && li < (long long)kKmpStageBytes) ? win[li] : __ldg(p.text + x);
-      };
-      // warm-up: (m-1) bytes before the chunk resynchronise the state
-      uint32_t j = 0;
-      unsigned long long x = c0 >= p.m - 1 ? c0 - (p.m - 1) : 0;
-      for (; x < c0; ++x) j = D[j * p.C + s_cls[tbyte(x)]] & 0x1FFFu;
-      unsigned long long cmp = 0;
-      x = c0;
-      while (x < c1) {
-        // state-0 skip: four bytes none of which is p[0] keep state 0, one
-        // comparison each
-        if (j == 0 && x + 4 <= c1 && ((x - t0 + kKmpPre) & 3) == 0 &&
-            (x - t0 + kKmpPre + 4) <= kKmpStageBytes) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(win + (x - t0 + kKmpPre));
-          if (__vcmpeq4(w, p0x4) == 0) {
-            cmp += 4;
-            x += 4;
-            continue;
-          }
-        }
-        const uint32_t e = D[j * p.C + s_cls[tbyte(x)]];
-        cmp += e >> 14;
-        if (e & 0x2000u) {
-          if (p.mode == 0) {
-            const uint32_t slot = atomicAdd(&s_misc[0], 1u);
-            if (slot < kKmpHitCap) s_keys[slot] = x - t0;  // match ends at x
-          } else {
-            const unsigned long long slot = atomicAdd(p.g_count, 1ull);
-            if (slot < p.keys_cap) p.keys[slot] = p.base + x + 1 - p.m;
-          }
-        }
-        j = e & 0x1FFFu;
-        ++x;
-      }
-      cmp_total += cmp;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t tn = t + kKmpStages * gridDim.x;
-      if (tn < p.num_tiles) {
-        fence_proxy_async();
-        issue(stage, tn);
-      }
-    }
-    if (p.mode != 0) {
-      __syncthreads();
-      continue;
-    }
-    const uint32_t nh = s_misc[0];
-    const bool over = nh > kKmpHitCap;
-    if (!over && nh > 1) {
-      uint32_t P = 1;
-      while (P < nh) P <<= 1;
-      for (uint32_t y = nh + tid; y < P; y += kThreads) s_keys[y] = ~0ull;
-      __syncthreads();
-      sort_keys(s_keys, P);
-    }
-    if (tid == 0) {
-      unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
-      p.dir[t].slot = slot;
-      p.dir[t].count = nh;
-      p.dir[t].overflow = over;
-      if (over) atomicOr(p.g_flags, 1u);
-      s_misc[1] = (uint32_t)slot;
-      s_misc[2] = (uint32_t)(slot >> 32);
-    }
-    __syncthreads();
-    const unsigned long long slot = (unsigned long long)s_misc[1] | ((unsigned long long)s_misc[2] << 32);
-    if (!over && slot + nh <= p.staging_cap)
-      for (uint32_t h = tid; h < nh; h += kThreads)
-        p.staging[slot + h] = p.base + t0 + s_keys[h] + 1 - p.m;
-    __syncthreads();
-    if (tid == 0) s_misc[0] = 0;
-    __syncthreads();
-  }
-  // comparisons: warp reduce then one atomic per warp
-  for (int o = 16; o; o >>= 1) cmp_total += __shfl_xor_sync(0xffffffffu, cmp_total, o);
-  if ((tid & 31) == 0 && cmp_total) atomicAdd(p.comparisons, cmp_total);
-}
+// K4 KMP: see kmp.cuh.
 
 // ------------------------------------------------------------------ corpus
 __global__ void gen_syslog_kernel(uint8_t* out, unsigned long long begin, unsigned long long n,

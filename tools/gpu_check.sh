@@ -13,4 +13,5 @@ timeout 300 python bench.py --patterns 10 --no-cpu --no-e2e > gpurun_out/bench_k
 if [ "${PROFILE:-1}" = 1 ]; then
   timeout 900 tools/profile_pfac.sh k1000
   timeout 600 tools/profile_pfac.sh k10 --patterns 10
+  KREGEX=kmp2 timeout 600 tools/profile_pfac.sh kmp --config kmp
 fi
