@@ -87,6 +87,9 @@ struct glop_ctx {
   cudaStream_t stream = nullptr;
   DBuf text, staging, out, dir, prefix, misc, keys, keys_alt, cub_tmp;
   DBuf keep, bcounts, bprefix, alerts, kmp_dfa, spill;
+  DBuf sbuf[2];                                  // streamed text chunks (host-text pipeline)
+  cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
+  cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   unsigned long long* h_misc = nullptr;  // pinned readback
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
   bool timed = false;
@@ -110,12 +113,13 @@ struct glop_rules {
   int device = 0;
   void* mem = nullptr;
   DevRules view{};
-  std::vector<uint64_t> lens;
+  uint64_t max_len = 0;
 };
 
 namespace {
 
 constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per CTA on sm_100
+constexpr uint64_t kStreamChunk = 256ull << 20;  // host-text pipeline chunk
 
 struct Dev {
   explicit Dev(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); dev = d; }
@@ -572,6 +576,86 @@ glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* 
   return GLOP_OK;
 }
 
+// Host-text pipeline for large inputs (streaming ingest):
+// the text is copied in kStreamChunk pieces (+ a halo for the trie walk and
+// the stage-2 suffix compare) on a copy stream into two device buffers, so
+// the H2D copy of chunk i+1 overlaps the scan + verify of chunk i.  Chunk
+// results are exact and ordered (ownership of starts, scan.hpp:230-232), so
+// the alerts are the concatenation of the chunks' alerts.
+glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* h_text,
+                                  uint64_t n, uint64_t own, uint64_t base, glop_alert** alerts,
+                                  uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits) {
+  const uint64_t halo = std::max<uint64_t>(std::max<uint64_t>(t->info.max_depth, r->max_len), 1) - 1;
+  const uint64_t chunks = (own + kStreamChunk - 1) / kStreamChunk;
+  for (int b = 0; b < 2; ++b) TRY(c->sbuf[b].ensure(kStreamChunk + halo + 64));
+  const uint32_t k = r->view.n_patterns;
+  TRY(c->spill.ensure((size_t)(k + 1) * 8));
+  uint64_t* d_counts = c->spill.as<uint64_t>();
+  CU(cudaMemsetAsync(d_counts, 0, (size_t)(k + 1) * 8, c->stream));
+  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
+  TRY(c->out.ensure(cap * sizeof(glop_hit)));
+  DBuf& acc = c->alerts;  // accumulated alerts (device); grows rarely, kept across calls
+  uint64_t total = 0, hits = 0;
+  auto copy = [&](uint64_t i) -> glop_status {
+    const uint64_t lo = i * kStreamChunk;
+    const uint64_t rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - lo) + halo, n - lo);
+    CU(cudaStreamWaitEvent(c->cstream, c->ev_free[i & 1], 0));
+    CU(cudaMemcpyAsync(c->sbuf[i & 1].p, h_text + lo, rd, cudaMemcpyHostToDevice, c->cstream));
+    CU(cudaEventRecord(c->ev_copied[i & 1], c->cstream));
+    return GLOP_OK;
+  };
+  // ev_free[b]: buffer b may be overwritten (recorded after its chunk's work)
+  CU(cudaEventRecord(c->ev_free[0], c->stream));
+  CU(cudaEventRecord(c->ev_free[1], c->stream));
+  glop_status st = copy(0);
+  for (uint64_t i = 0; i < chunks && st == GLOP_OK; ++i) {
+    if (i + 1 < chunks) TRY(copy(i + 1));
+    const uint64_t lo = i * kStreamChunk, own_i = std::min<uint64_t>(kStreamChunk, own - lo);
+    const uint64_t rd = std::min<uint64_t>(own_i + halo, n - lo);
+    const uint8_t* d_text = c->sbuf[i & 1].as<uint8_t>();
+    CU(cudaStreamWaitEvent(c->stream, c->ev_copied[i & 1], 0));
+    uint64_t nh = 0;
+    glop_status s = pfac_scan_device_impl(c, t, d_text, rd, own_i, base + lo, GLOP_PFAC_AUTO, c->out.as<glop_hit>(),
+                                          cap, &nh);
+    if (s == GLOP_ECAPACITY && nh > cap) {
+      c->out.release();
+      cap = nh;
+      TRY(c->out.ensure(cap * sizeof(glop_hit)));
+      s = pfac_scan_device_impl(c, t, d_text, rd, own_i, base + lo, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
+    }
+    if (s != GLOP_OK) return s;
+    hits += nh;
+    if ((total + nh) * sizeof(glop_alert) > acc.bytes) {  // grow, keeping the alerts so far
+      DBuf bigger;
+      TRY(bigger.ensure(std::max<uint64_t>(2 * acc.bytes, (total + nh + (1 << 16)) * sizeof(glop_alert))));
+      if (total) CU(cudaMemcpyAsync(bigger.p, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToDevice, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      acc.release();
+      acc = bigger;
+      bigger.p = nullptr;
+    }
+    uint64_t kept = 0;
+    TRY(verify_device_impl(c, r, d_text, rd, base + lo, c->out.as<glop_hit>(), nh, acc.as<glop_alert>() + total,
+                           &kept, d_counts));
+    CU(cudaEventRecord(c->ev_free[i & 1], c->stream));
+    total += kept;
+  }
+  if (stage1_hits) *stage1_hits = hits;
+  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(total, 1) * sizeof(glop_alert)));
+  cudaError_t e = a ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess && total)
+    e = cudaMemcpyAsync(a, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && counts) e = cudaMemcpyAsync(counts, d_counts, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(a);
+    return fail(e == cudaErrorMemoryAllocation ? GLOP_ENOMEM : GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *alerts = a;
+  *n_alerts = total;
+  return GLOP_OK;
+}
+
 }  // namespace
 
 // ============================================================== C ABI
@@ -598,6 +682,11 @@ glop_status glop_ctx_create(int device, glop_ctx** out) {
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_misc, 64);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     delete c;
     return fail(GLOP_ECUDA, cudaGetErrorString(e));
@@ -612,8 +701,16 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
-                  &c->kmp_dfa, &c->spill})
+                  &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1]})
     b->release();
+  if (c->cstream) {
+    cudaStreamSynchronize(c->cstream);
+    cudaStreamDestroy(c->cstream);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+  }
   cudaFreeHost(c->h_misc);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -939,6 +1036,7 @@ glop_status glop_rules_upload(glop_ctx* c, const uint8_t* bytes, const uint64_t*
   r->view.off = reinterpret_cast<const unsigned long long*>(static_cast<uint8_t*>(mem) + o_off);
   r->view.n_patterns = k;
   r->view.prefix_len = prefix_len;
+  for (uint32_t i = 0; i < k; ++i) r->max_len = std::max<uint64_t>(r->max_len, off[i + 1] - off[i]);
   *out = r;
   return GLOP_OK;
 }
@@ -1113,10 +1211,13 @@ glop_status glop_run_pfac_pipeline_shard(glop_ctx* c, const glop_trie* t, const 
                                          int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
                                          uint64_t* counts, uint64_t* stage1_hits) {
   if (!c || !t || !r || !alerts || !n_alerts) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline: null argument");
+  if (own > n) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline: own > n");
   std::lock_guard<std::mutex> lk(c->mu);
   Dev g(c->device);
   *alerts = nullptr;
   *n_alerts = 0;
+  if (!text_on_device && own > kStreamChunk)
+    return run_pipeline_streamed(c, t, r, text, n, own, base, alerts, n_alerts, counts, stage1_hits);
   const uint8_t* d_text = nullptr;
   TRY(to_device_text(c, text, n, text_on_device, &d_text));
   uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));

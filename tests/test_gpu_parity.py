@@ -308,3 +308,31 @@ def test_kernel_variants_vs_oracle(ctx, torch_cuda, k, L, lens):
         assert got.tobytes() == ref.tobytes(), (kernel, len(got), len(ref))
     if k == 10000:
         assert not trie.info.jump_in_smem
+
+
+def test_streamed_host_pipeline(ctx, torch_cuda):
+    """Host-text pipeline (chunked H2D overlapped with scan + verify, SURVEY
+    §8f row 2) == the device-resident pipeline: alerts, counts, stage-1 hits,
+    across chunk boundaries, with a shard's own/base and a halo."""
+    n = (256 << 20) * 2 + 12345  # > 2 streaming chunks
+    d = torch_cuda.empty(n + 64, dtype=torch_cuda.uint8, device="cuda")
+    ctx.gen_syslog_device(d.data_ptr(), n, seed=77)
+    ctx.synchronize()
+    host = d[:n].cpu().numpy()
+    pats, _ = glop.gen_rules(1000, seed=606)
+    pats += [b"Failed password for invalid user", b"session opened for user root by"]
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    rules = ctx.upload_rules(pats, 8)
+    for own, base in ((n, 0), (n - 1000, 5 << 30)):
+        ref = ctx.run_pfac_pipeline(trie, rules, d.data_ptr(), n, True, own=own, base=base)
+        got = ctx.run_pfac_pipeline(trie, rules, host.ctypes.data, n, False, own=own, base=base)
+        assert got[2] == ref[2] and len(ref[0]) > 1000
+        assert got[0].tobytes() == ref[0].tobytes()
+        assert np.array_equal(got[1], ref[1])
+    # and both equal the oracle on a window that straddles the first chunk boundary
+    lo = (256 << 20) - 5000
+    win = host[lo: lo + 20000]
+    w_alerts = ctx.run_pfac_pipeline(trie, rules, win.ctypes.data, win.size, False)[0]
+    ref_alerts = O.verify_hits(win, O.pfac_scan(win, O.Trie(pats, 8)), pats, 8)
+    assert np.array_equal(w_alerts["offset"], ref_alerts["offset"])
+    assert np.array_equal(w_alerts["rule_id"], ref_alerts["rule_id"])
