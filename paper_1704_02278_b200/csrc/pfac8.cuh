@@ -33,9 +33,10 @@ constexpr int kP8Threads = kP8Warps * 32;
 constexpr uint32_t kP8Tile = 2048;                 // owned starts per tile (TMA unit)
 constexpr uint32_t kP8Stage = kP8Tile + 16;        // + words 512..515 (halo)
 constexpr uint32_t kP8Chunk = 1024;                // bytes sampled per iteration (8 words / lane)
-constexpr uint32_t kP8Queue = kP8Chunk / 4;        // candidate words per chunk, worst case
-constexpr uint32_t kP8Hits = 64;                   // hit keys per warp in smem
-constexpr uint32_t kP8DmaskBytes = 1u << 15;
+constexpr uint32_t kP8Queue = 32 + kP8Chunk / 4;    // candidate words: < 32 carried + one chunk
+constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
+constexpr uint32_t kP8DmaskLog2 = 16;
+constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;
 
 struct P8Layout {
   uint32_t bufs, bars, queue, hits, nh, dmask, bm2, cls, total;
@@ -69,7 +70,7 @@ struct P8Params {
   unsigned long long* g_count;   // [0] total hits, [1] flags, [2] max region use, [3] mode-1 slots
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
-  const uint8_t* dmask8;         // 2^15 d-masks (bits 0..3: offsets d = 1..4)
+  const uint8_t* dmask8;         // 2^16 d-masks (bits 0..3: offsets d = 1..4)
 };
 
 // Level-1 d-mask of an aligned text word (bit d-1: the word may be the
@@ -77,7 +78,7 @@ struct P8Params {
 // Bloom variant halved the candidate words but doubled the bank-conflicted
 // shared-memory probes, which bound the kernel (measured: 3.63 -> 3.55 ms at
 // k=1,000 and 2.46 -> 1.97 ms at k=10 without it).  Built by glop_trie_upload.
-__host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) { return (g * 0x9E3779B1u) >> 17; }
+__host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) { return (g * 0x9E3779B1u) >> (32 - kP8DmaskLog2); }
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) { return dm[p8_h1(g)]; }
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
@@ -242,56 +243,67 @@ __global__ void __launch_bounds__(kP8Threads, 1)
       }
     };
 
-    // Chunks of 1 KB: lane l samples tile words W + 8 l + 1 .. + 8 (the 4
-    // chunks cover candidates 0..4095 of the tile).
+    // Chunks of 1 KB: lane l samples tile words W + 8 l + 1 .. + 8 (the
+    // chunks cover candidates 0..kP8Tile-1 of the tile).  Candidate words
+    // enter the queue q in text order; full 32-entry rounds are drained after
+    // each chunk (the < 32 left over move to the front), and the pass
+    // W == kP8Tile / 4 drains the rest.
+    uint32_t qh = 0, qt = 0;
 #pragma unroll 1
-    for (uint32_t W = 0; W < kP8Tile / 4; W += kP8Chunk / 4) {
-      const uint4 va = reinterpret_cast<const uint4*>(sw + W)[2 * lane];
-      const uint4 vb = reinterpret_cast<const uint4*>(sw + W)[2 * lane + 1];
-      const uint32_t wn = sw[W + kP8Chunk / 4];
-      uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
-      if (lane == 31) w8 = wn;
-      uint32_t m[8];
-      m[0] = p8_dmask(s_dmask, va.y);
-      m[1] = p8_dmask(s_dmask, va.z);
-      m[2] = p8_dmask(s_dmask, va.w);
-      m[3] = p8_dmask(s_dmask, vb.x);
-      m[4] = p8_dmask(s_dmask, vb.y);
-      m[5] = p8_dmask(s_dmask, vb.z);
-      m[6] = p8_dmask(s_dmask, vb.w);
-      m[7] = p8_dmask(s_dmask, w8);
-      const uint32_t lo4 = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
-      const uint32_t hi4 = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
-      const uint32_t any = __ballot_sync(0xffffffffu, (lo4 | hi4) != 0);
-      if (!any) continue;
-      // candidate words of this lane (d-masks are < 16: adding 0x7F to a byte
-      // sets its top bit iff the byte is non-zero), bit-plane warp prefix
-      const uint32_t cnt = __popc((lo4 + 0x7F7F7F7Fu) & 0x80808080u) + __popc((hi4 + 0x7F7F7F7Fu) & 0x80808080u);
-      uint32_t tot, pre;
-      if (!__ballot_sync(0xffffffffu, cnt > 1)) {
-        tot = __popc(any);
-        pre = __popc(any & ltmask);
-      } else {
-        tot = 0, pre = 0;
+    for (uint32_t W = 0; W <= kP8Tile / 4; W += kP8Chunk / 4) {
+      const bool tail = W == kP8Tile / 4;
+      if (qh) {  // carry the < 32 undrained entries to the front
+        const uint32_t pend = qt - qh;
+        const uint32_t v = lane < pend ? q[qh + lane] : 0u;
+        __syncwarp();
+        if (lane < pend) q[lane] = v;
+        qh = 0;
+        qt = pend;
+        __syncwarp();
+      }
+      if (!tail) {
+        const uint4 va = reinterpret_cast<const uint4*>(sw + W)[2 * lane];
+        const uint4 vb = reinterpret_cast<const uint4*>(sw + W)[2 * lane + 1];
+        const uint32_t wn = sw[W + kP8Chunk / 4];
+        uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
+        if (lane == 31) w8 = wn;
+        uint32_t m[8];
+        m[0] = p8_dmask(s_dmask, va.y);
+        m[1] = p8_dmask(s_dmask, va.z);
+        m[2] = p8_dmask(s_dmask, va.w);
+        m[3] = p8_dmask(s_dmask, vb.x);
+        m[4] = p8_dmask(s_dmask, vb.y);
+        m[5] = p8_dmask(s_dmask, vb.z);
+        m[6] = p8_dmask(s_dmask, vb.w);
+        m[7] = p8_dmask(s_dmask, w8);
+        const uint32_t lo4 = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
+        const uint32_t hi4 = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
+        if (__ballot_sync(0xffffffffu, (lo4 | hi4) != 0)) {
+          // candidate words of this lane (d-masks are < 16: adding 0x7F to a
+          // byte sets its top bit iff the byte is non-zero), bit-plane prefix
+          const uint32_t cnt =
+              __popc((lo4 + 0x7F7F7F7Fu) & 0x80808080u) + __popc((hi4 + 0x7F7F7F7Fu) & 0x80808080u);
+          uint32_t tot = 0, at = qt;
 #pragma unroll
-        for (uint32_t bit = 0; bit < 4; ++bit) {
-          const uint32_t bb = __ballot_sync(0xffffffffu, (cnt >> bit) & 1u);
-          tot += __popc(bb) << bit;
-          pre += __popc(bb & ltmask) << bit;
+          for (uint32_t bit = 0; bit < 4; ++bit) {
+            const uint32_t bb = __ballot_sync(0xffffffffu, (cnt >> bit) & 1u);
+            tot += __popc(bb) << bit;
+            at += __popc(bb & ltmask) << bit;
+          }
+          const uint32_t wbase = (W + 8 * lane + 1) << 4;
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            if (m[j]) q[at++] = wbase + 16 * j + m[j];
+          qt += tot;
+          __syncwarp();
         }
       }
-      {
-        uint32_t* qp = q + pre;
-        const uint32_t wbase = (W + 8 * lane + 1) << 4;
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j)
-          if (m[j]) *qp++ = wbase + 16 * j + m[j];
-      }
-      __syncwarp();
 #pragma unroll 1
-      for (uint32_t r = 0; r < tot; r += 32) {
+      while (qt - qh >= 32 || (tail && qt != qh)) {
+        const uint32_t pend = qt - qh;
         // ---- 8-byte keys of up to 32 candidate words -> prefix bitmap
-        const uint32_t e = r + lane < tot ? q[r + lane] : 16u;  // idle lanes: word 1, no bits
+        const uint32_t e = lane < pend ? q[qh + lane] : 16u;  // idle lanes: word 1, no bits
+        qh += min(pend, 32u);
         const uint32_t i = e >> 4;
         uint32_t mm = e & 15u;
         const uint32_t w0 = sw[i - 1], w1 = sw[i], w2 = sw[i + 1];
