@@ -37,9 +37,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["glop", "reference"], default="glop")
-    ap.add_argument("--config", choices=["pfac", "kmp"], default="pfac")
-    ap.add_argument("--bytes-per-gpu", type=float, default=8e9)
-    ap.add_argument("--patterns", type=int, default=1000)
+    ap.add_argument("--config", choices=["pfac", "kmp", "dpi"], default="pfac",
+                    help="pfac: configs[2]/[3] syslog; kmp: configs[1]; dpi: configs[4] packet payloads")
+    ap.add_argument("--bytes-per-gpu", type=float, default=None,
+                    help="default 8e9 (pfac), 1e9 (kmp), 4e9 (dpi: 32 GB over 8 GPUs)")
+    ap.add_argument("--patterns", type=int, default=None, help="default 1000 (pfac), 10000 (dpi)")
     ap.add_argument("--prefix-len", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--rules-seed", type=int, default=606)
@@ -48,7 +50,21 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline work")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.bytes_per_gpu is None:
+        a.bytes_per_gpu = {"pfac": 8e9, "kmp": 1e9, "dpi": 4e9}[a.config]
+    if a.patterns is None:
+        a.patterns = 10000 if a.config == "dpi" else 1000
+    return a
+
+
+def workload_rules(args, glop):
+    """The config's pattern set (bytes) and text generators (host, device)."""
+    if args.config == "dpi":
+        pats = glop.gen_dpi_rules(args.patterns, args.rules_seed, 8, 24)
+        return pats, glop.gen_payload_host, "gen_payload_device"
+    pats, _ = glop.gen_rules(args.patterns, args.rules_seed)
+    return pats, glop.gen_syslog_host, "gen_syslog_device"
 
 
 def peaks():
@@ -166,13 +182,13 @@ def run_reference(args):
                   "bytes": int(args.bytes_per_gpu), "sample_bytes": sample}
         desc = f"kmp_multi (kmp.hpp:74) single-threaded by design on the first {sample} bytes"
     else:
-        pats, _ = glop.gen_rules(args.patterns, args.rules_seed)
-        probe = glop.gen_syslog_host(64 << 20, args.seed)
+        pats, gen_host, _ = workload_rules(args, glop)
+        probe = gen_host(64 << 20, args.seed)
         timer = O.ref_time_pfac if ref is not None else (lambda t, q, l, w, r: O.port_time_pfac(t, q, l, w, r))
         secs, _ = timer(probe, pats, args.prefix_len, 0, 1)
         per_byte = max(secs[0], 1e-6) / probe.size
         sample = int(min(args.bytes_per_gpu, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
-        text = glop.gen_syslog_host(sample, args.seed)
+        text = gen_host(sample, args.seed)
         secs, na = timer(text, pats, args.prefix_len, args.warmup, args.steps)
         cores = int(ref.ref_default_workers()) if ref is not None else 1
         metric = METRIC
@@ -193,8 +209,13 @@ def run_reference(args):
 
 
 def workload_config(args, world):
-    return {"workload": "configs[2]/[3]: PFAC, %d patterns (8-byte prefixes), %.0f GB synthetic RFC 5424 syslog "
-                        "per GPU" % (args.patterns, args.bytes_per_gpu / 1e9),
+    if args.config == "dpi":
+        what = ("configs[4] DPI mode: PFAC, %d Snort-style contents (8..24 bytes; 8-byte prefixes + stage-2 "
+                "verify), %.0f GB synthetic packet payloads per GPU" % (args.patterns, args.bytes_per_gpu / 1e9))
+    else:
+        what = ("configs[2]/[3]: PFAC, %d patterns (8-byte prefixes), %.0f GB synthetic RFC 5424 syslog per GPU"
+                % (args.patterns, args.bytes_per_gpu / 1e9))
+    return {"workload": what,
             "bytes_per_gpu": int(args.bytes_per_gpu), "total_bytes": int(args.bytes_per_gpu) * world,
             "patterns": args.patterns, "prefix_len": args.prefix_len, "corpus_seed": args.seed,
             "rules_seed": args.rules_seed, "kernel": args.kernel,
@@ -242,14 +263,14 @@ def main():
     if args.config == "kmp":
         return bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks)
 
-    pats, _ = glop.gen_rules(args.patterns, args.rules_seed)
+    pats, _, gen_dev = workload_rules(args, glop)
     trie = ctx.upload(glop.build_failureless_trie(pats, args.prefix_len))
     rules = ctx.upload_rules(pats, args.prefix_len)
     info = trie.info
     halo = max(info.max_depth, max(len(p) for p in pats)) - 1
     sh = plan_shards(total, world, halo)[rank]
     d_text = torch.empty(sh.read + 64, dtype=torch.uint8, device="cuda")
-    ctx.gen_syslog_device(d_text.data_ptr(), sh.read, args.seed, begin=sh.lo)
+    getattr(ctx, gen_dev)(d_text.data_ptr(), sh.read, args.seed, begin=sh.lo)
     ctx.synchronize()
     cap = max(1 << 20, S // 256)
     d_hits = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
@@ -298,11 +319,13 @@ def main():
     peak, peak_src = peaks()
     achieved = sh.own / (kernel_ms / 1e3) / 1e9  # GB/s of the dominant kernel
     kname = "pfac8_kernel" if info.min_depth >= 8 and args.kernel == "auto" else "pfac_warp_kernel"
-    traffic = ncu_traffic(kname, f"k{args.patterns}") if args.bytes_per_gpu == 8e9 else None
+    tag = "dpi" if args.config == "dpi" else f"k{args.patterns}"
+    traffic = ncu_traffic(kname, tag) if args.bytes_per_gpu == {"dpi": 4e9}.get(args.config, 8e9) else None
     line = {"metric": METRIC, "value": round(value, 2), "unit": "Gbps", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic RFC 5424 syslog generated on device (csrc/corpus.h), seeded",
+            "data": ("synthetic packet payloads generated on device (csrc/payload.h), seeded" if args.config == "dpi"
+                     else "synthetic RFC 5424 syslog generated on device (csrc/corpus.h), seeded"),
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
@@ -359,7 +382,7 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
 
     from paper_1704_02278_b200 import glop
 
-    S = int(min(args.bytes_per_gpu, 1e9)) if args.bytes_per_gpu == 8e9 else int(args.bytes_per_gpu)
+    S = int(args.bytes_per_gpu)
     p = b"Failed password"
     d_text = torch.empty(S + 64, dtype=torch.uint8, device="cuda")
     ctx.gen_syslog_device(d_text.data_ptr(), S, args.seed, begin=rank * S)

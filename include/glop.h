@@ -227,6 +227,18 @@ glop_status glop_gen_syslog_device(glop_ctx* ctx, uint8_t* d_out, uint64_t begin
                                    uint64_t seed);
 glop_status glop_gen_syslog_host(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed,
                                  unsigned threads);
+/* Bytes [begin, begin+n) of synthetic packet-payload stream `seed` (DPI
+ * configuration, paper_1704_02278_b200/csrc/payload.h); device and host forms
+ * are byte-identical. */
+glop_status glop_gen_payload_device(glop_ctx* ctx, uint8_t* d_out, uint64_t begin, uint64_t n,
+                                    uint64_t seed);
+glop_status glop_gen_payload_host(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed,
+                                  unsigned threads);
+/* Snort-style content rules for the DPI configuration: k distinct contents of
+ * min_len..max_len bytes (half random full-byte, half payload windows).
+ * bytes must hold k*max_len; off receives k+1 offsets. */
+glop_status glop_gen_dpi_rules(uint32_t k, uint32_t seed, uint32_t min_len, uint32_t max_len,
+                               uint8_t* bytes, uint64_t* off);
 /* Reference corpus semantics (loggen.hpp:44-57), host only. */
 glop_status glop_gen_reference_log(uint8_t* out, uint64_t size, uint32_t seed, uint64_t line_len);
 /* Synthetic rule set: k patterns of `len` bytes, half with the reference's

@@ -1296,6 +1296,36 @@ glop_status glop_gen_syslog_host(uint8_t* out, uint64_t begin, uint64_t n, uint6
   return GLOP_OK;
 }
 
+glop_status glop_gen_payload_device(glop_ctx* c, uint8_t* d_out, uint64_t begin, uint64_t n, uint64_t seed) {
+  if (n == 0) return GLOP_OK;
+  Dev g(c->device);
+  const uint64_t blocks = (begin + n - 1) / glop_payload::kBlock - begin / glop_payload::kBlock + 1;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((blocks + 127) / 128, 65535);
+  ++c->launches;
+  gen_payload_kernel<<<grid, 128, 0, c->stream>>>(d_out, begin, n, seed);
+  CU(cudaGetLastError());
+  return GLOP_OK;
+}
+
+glop_status glop_gen_payload_host(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads) {
+  glop_workload::gen_payload(out, begin, n, seed, threads);
+  return GLOP_OK;
+}
+
+glop_status glop_gen_dpi_rules(uint32_t k, uint32_t seed, uint32_t min_len, uint32_t max_len, uint8_t* bytes,
+                               uint64_t* off) {
+  if (min_len < 1 || max_len < min_len) return fail(GLOP_EINVAL, "glop_gen_dpi_rules: bad lengths");
+  const auto rules = glop_workload::dpi_rules(k, seed, min_len, max_len);
+  uint64_t o = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    off[i] = o;
+    memcpy(bytes + o, rules[i].data(), rules[i].size());
+    o += rules[i].size();
+  }
+  off[k] = o;
+  return GLOP_OK;
+}
+
 glop_status glop_gen_reference_log(uint8_t* out, uint64_t size, uint32_t seed, uint64_t line_len) {
   if (size == 0 || line_len < 2) return fail(GLOP_EINVAL, "generate_log: bad size/line_len");
   std::string s = glop_workload::reference_generate_log(size, seed, line_len);

@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "corpus.h"
+#include "payload.h"
 
 namespace glop {
 
@@ -944,6 +945,19 @@ __global__ void gen_syslog_kernel(uint8_t* out, unsigned long long begin, unsign
     const unsigned long long e = (b + 1) * kBlock < begin + n ? (b + 1) * kBlock : begin + n;
     glop_corpus::gen_block_range(out + (s - begin), seed, b, (uint32_t)(s - b * kBlock),
                                  (uint32_t)(e - b * kBlock));
+  }
+}
+
+__global__ void gen_payload_kernel(uint8_t* out, unsigned long long begin, unsigned long long n,
+                                   unsigned long long seed) {
+  using glop_payload::kBlock;
+  const unsigned long long b0 = begin / kBlock, b1 = (begin + n - 1) / kBlock + 1;
+  for (unsigned long long b = b0 + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; b < b1;
+       b += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long s = b * kBlock > begin ? b * kBlock : begin;
+    const unsigned long long e = (b + 1) * kBlock < begin + n ? (b + 1) * kBlock : begin + n;
+    glop_payload::gen_block_range(out + (s - begin), seed, b, (uint32_t)(s - b * kBlock),
+                                  (uint32_t)(e - b * kBlock));
   }
 }
 

@@ -10,10 +10,12 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
 #include "corpus.h"
+#include "payload.h"
 
 namespace glop_workload {
 
@@ -42,6 +44,93 @@ inline void gen_syslog(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed,
     lo = hi;
   }
   for (auto& t : pool) t.join();
+}
+
+// Bytes [begin, begin+n) of the synthetic packet-payload stream `seed`
+// (payload.h), generated on `threads` host threads.
+inline void gen_payload(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads = 0) {
+  using glop_payload::kBlock;
+  if (n == 0) return;
+  const uint64_t b0 = begin / kBlock, b1 = (begin + n - 1) / kBlock + 1;
+  if (!threads) threads = std::max(1u, std::thread::hardware_concurrency());
+  threads = (unsigned)std::min<uint64_t>(threads, b1 - b0);
+  auto work = [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t b = lo; b < hi; ++b) {
+      const uint64_t s = std::max(begin, b * kBlock), e = std::min(begin + n, (b + 1) * kBlock);
+      glop_payload::gen_block_range(out + (s - begin), seed, b, (uint32_t)(s - b * kBlock),
+                                    (uint32_t)(e - b * kBlock));
+    }
+  };
+  std::vector<std::thread> pool;
+  uint64_t per = (b1 - b0) / threads, extra = (b1 - b0) % threads, lo = b0;
+  for (unsigned t = 0; t < threads; ++t) {
+    uint64_t hi = lo + per + (t < extra ? 1 : 0);
+    pool.emplace_back(work, lo, hi);
+    lo = hi;
+  }
+  for (auto& t : pool) t.join();
+}
+
+// Snort-style content rule set for the DPI configuration: k distinct
+// contents of min_len..max_len bytes: half uniformly random over the full
+// byte alphabet, 45% windows of the payload stream (seed 1, first 4 MiB) whose
+// 8-byte prefix occurs at most twice there (Snort contents are distinctive),
+// 5% non-periodic windows of the attack strings the payloads carry (frequent
+// alerts); a rejected window becomes a random content, so generation always
+// terminates.
+// At most 3 contents share an 8-byte prefix (stage-2 verification separates
+// them).
+inline std::vector<std::string> dpi_rules(size_t k, uint32_t seed, size_t min_len, size_t max_len) {
+  std::vector<uint8_t> sample(4u << 20);
+  gen_payload(sample.data(), 0, sample.size(), 1);
+  std::vector<uint64_t> grams(sample.size() - 7);
+  for (size_t i = 0; i + 8 <= sample.size(); ++i) memcpy(&grams[i], sample.data() + i, 8);
+  std::sort(grams.begin(), grams.end());
+  auto freq = [&](const std::string& b) {
+    uint64_t g;
+    memcpy(&g, b.data(), 8);
+    return std::upper_bound(grams.begin(), grams.end(), g) - std::lower_bound(grams.begin(), grams.end(), g);
+  };
+  std::vector<std::string> attacks;
+  for (const char* a = glop_payload::kAttackHost; *a;) {
+    const char* e = a;
+    while (*e && *e != '|') ++e;
+    if ((size_t)(e - a) >= min_len) attacks.emplace_back(a, e);
+    a = *e ? e + 1 : e;
+  }
+  std::mt19937_64 rng(seed * 0x9E3779B97F4A7C15ull + 77);
+  std::unordered_set<std::string> used;
+  std::unordered_map<std::string, int> per_prefix;
+  std::vector<std::string> out;
+  while (out.size() < k) {
+    size_t len = min_len + rng() % (max_len - min_len + 1);
+    std::string b;
+    const size_t kind = out.size() % 20;
+    if (kind < 10) {
+      b.resize(len);
+      for (size_t i = 0; i < len; ++i) b[i] = (char)(rng() & 0xFF);
+    } else if (kind < 19) {
+      b.assign(reinterpret_cast<const char*>(sample.data()) + rng() % (sample.size() - len), len);
+      if (freq(b) > 2) b.clear();  // frequent protocol text: random content instead
+    } else {
+      const std::string& a = attacks[rng() % attacks.size()];
+      len = std::min(len, a.size());
+      b = a.substr(rng() % (a.size() - len + 1), len);
+      bool seen[256] = {};
+      int distinct = 0;
+      for (size_t i = 0; i < 8; ++i) distinct += !seen[(uint8_t)b[i]], seen[(uint8_t)b[i]] = true;
+      if (distinct < 6) b.clear();  // periodic ("../../..") windows: random content instead
+    }
+    if (b.empty()) {
+      b.resize(len);
+      for (size_t i = 0; i < len; ++i) b[i] = (char)(rng() & 0xFF);
+    }
+    if (used.count(b) || per_prefix[b.substr(0, 8)] >= 3) continue;
+    ++per_prefix[b.substr(0, 8)];
+    used.insert(b);
+    out.push_back(std::move(b));
+  }
+  return out;
 }
 
 // Reference corpus semantics (loggen.hpp:35-57): MT19937 low-byte rejection

@@ -108,6 +108,9 @@ _sig("glop_memcpy", vp, vp, vp, C.c_uint64, C.c_int)
 _sig("glop_gen_syslog_device", vp, vp, C.c_uint64, C.c_uint64, C.c_uint64)
 _sig("glop_gen_syslog_host", vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint)
 _sig("glop_gen_reference_log", vp, C.c_uint64, C.c_uint32, C.c_uint64)
+_sig("glop_gen_payload_device", vp, vp, C.c_uint64, C.c_uint64, C.c_uint64)
+_sig("glop_gen_payload_host", vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint)
+_sig("glop_gen_dpi_rules", C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u8p, u64p)
 _sig("glop_gen_rules", C.c_uint32, C.c_uint32, C.c_uint32, u8p, u8p)
 _sig("glop_build_failureless_trie", u8p, u64p, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(i32p),
      u32p, C.POINTER(u32p), C.POINTER(vp))
@@ -193,6 +196,24 @@ def gen_syslog_host(n: int, seed: int, begin: int = 0, threads: int = 0, out: np
     if n:
         _check(_lib.glop_gen_syslog_host(buf.ctypes.data_as(vp), begin, n, seed, threads), "gen_syslog_host")
     return buf
+
+
+def gen_payload_host(n: int, seed: int, begin: int = 0, threads: int = 0) -> np.ndarray:
+    """Bytes [begin, begin+n) of the synthetic packet-payload stream (DPI config)."""
+    buf = np.empty(n, dtype=np.uint8)
+    if n:
+        _check(_lib.glop_gen_payload_host(buf.ctypes.data_as(vp), begin, n, seed, threads), "gen_payload_host")
+    return buf
+
+
+def gen_dpi_rules(k: int, seed: int, min_len: int = 8, max_len: int = 24) -> list[bytes]:
+    """Snort-style content set for the DPI config (see csrc/workload.hpp)."""
+    b = np.zeros(max(k * max_len, 1), dtype=np.uint8)
+    off = np.zeros(k + 1, dtype=np.uint64)
+    _check(_lib.glop_gen_dpi_rules(k, seed, min_len, max_len, b.ctypes.data_as(u8p), off.ctypes.data_as(u64p)),
+           "gen_dpi_rules")
+    raw = b.tobytes()
+    return [raw[int(off[i]):int(off[i + 1])] for i in range(k)]
 
 
 def gen_reference_log(size: int, seed: int, line_len: int = 80) -> np.ndarray:
@@ -400,3 +421,6 @@ class Context:
 
     def gen_syslog_device(self, d_out: int, n: int, seed: int, begin: int = 0):
         _check(_lib.glop_gen_syslog_device(self.h, d_out, begin, n, seed), "gen_syslog_device")
+
+    def gen_payload_device(self, d_out: int, n: int, seed: int, begin: int = 0):
+        _check(_lib.glop_gen_payload_device(self.h, d_out, begin, n, seed), "gen_payload_device")

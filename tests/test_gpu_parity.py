@@ -336,3 +336,30 @@ def test_streamed_host_pipeline(ctx, torch_cuda):
     ref_alerts = O.verify_hits(win, O.pfac_scan(win, O.Trie(pats, 8)), pats, 8)
     assert np.array_equal(w_alerts["offset"], ref_alerts["offset"])
     assert np.array_equal(w_alerts["rule_id"], ref_alerts["rule_id"])
+
+
+def test_dpi_payloads_vs_oracle(ctx, torch_cuda):
+    """DPI configuration (configs[4]): 10,000 Snort-style contents of 8..24
+    bytes over full-byte packet payloads -- 8-byte-prefix scan (u32 table,
+    > 32K states) + stage-2 suffix verification == the oracle; device
+    payload generator == host."""
+    n = 8 << 20
+    d = torch_cuda.empty(n + 64, dtype=torch_cuda.uint8, device="cuda")
+    ctx.gen_payload_device(d.data_ptr(), n, seed=1, begin=3 << 20)
+    ctx.synchronize()
+    text = d[:n].cpu().numpy()
+    assert np.array_equal(text, glop.gen_payload_host(n, seed=1, begin=3 << 20))
+    pats = glop.gen_dpi_rules(10000, seed=606, min_len=8, max_len=24)
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    assert trie.info.state_count > 32768 and trie.info.min_depth == 8
+    rules = ctx.upload_rules(pats, 8)
+    ref_hits = O.pfac_scan(text, O.Trie(pats, 8))
+    for kernel in (glop.PFAC_PREFIX8, glop.PFAC_FILTERED):
+        hits = dev_scan(ctx, torch_cuda, trie, text, kernel)
+        assert hits.tobytes() == ref_hits.tobytes()
+    ref_alerts = O.verify_hits(text, ref_hits, pats, 8)
+    alerts, counts, s1 = ctx.run_pfac_pipeline(trie, rules, d.data_ptr(), n, True)
+    assert s1 == len(ref_hits) and len(alerts) < s1  # some prefix hits fail stage 2
+    assert np.array_equal(alerts["offset"], ref_alerts["offset"])
+    assert np.array_equal(alerts["rule_id"], ref_alerts["rule_id"])
+    assert counts.sum() == len(alerts)
