@@ -106,6 +106,7 @@ struct glop_trie {
   bool u16 = true;
   bool smem_filter = false, smem_direct = false, smem_jump = false;
   bool p8 = false;  // every output at depth >= 8: pfac8_kernel applies
+  bool p8_nibble = false;  // pfac8 d-mask layout (see pfac8.cuh)
   uint32_t max_pid = 0;
 };
 
@@ -206,8 +207,11 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
   const P8Layout L = make_p8_layout();
   auto* g = c->misc.as<unsigned long long>();
   auto launch = [&](const P8Params& p) -> glop_status {
-    auto k = t->info.max_depth > 8 ? (t->u16 ? pfac8_kernel<true, uint16_t> : pfac8_kernel<true, uint32_t>)
-                                   : (t->u16 ? pfac8_kernel<false, uint16_t> : pfac8_kernel<false, uint32_t>);
+    auto k = t->info.max_depth > 8
+                 ? (t->p8_nibble ? (t->u16 ? pfac8_kernel<true, true, uint16_t> : pfac8_kernel<true, true, uint32_t>)
+                                 : (t->u16 ? pfac8_kernel<true, false, uint16_t> : pfac8_kernel<true, false, uint32_t>))
+                 : (t->p8_nibble ? (t->u16 ? pfac8_kernel<false, true, uint16_t> : pfac8_kernel<false, true, uint32_t>)
+                                 : (t->u16 ? pfac8_kernel<false, false, uint16_t> : pfac8_kernel<false, false, uint32_t>));
     CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     CU(cudaEventRecord(c->ev0, c->stream));
     k<<<grid, kP8Threads, L.total, c->stream>>>(t->view, p, L);
@@ -817,7 +821,9 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   // pfac8 level 1 (outputs only at depth >= 8): bit d-1 of the bucket of the
   // 4-gram at offset d (1..4) of every 8-byte root path
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
+  std::vector<unsigned long long> grams8;  // (4-gram << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
+  bool nibble8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -861,14 +867,24 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       for (uint32_t x = 0; x < J; ++x) key |= (unsigned long long)path[x] << (8 * x);
       keys.push_back({key, s});
       if (p8)
-        for (uint32_t d = 1; d <= 4; ++d)
-        {
-          const uint32_t g = (uint32_t)(key >> (8 * d));
-          dmask8[p8_h1(g)] |= (uint8_t)(1u << (d - 1));
-        }
+        for (uint32_t d = 1; d <= 4; ++d) grams8.push_back(((key >> (8 * d)) & 0xFFFFFFFFull) << 2 | (d - 1));
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
     });
+    if (p8) {
+      std::sort(grams8.begin(), grams8.end());
+      grams8.erase(std::unique(grams8.begin(), grams8.end()), grams8.end());
+      nibble8 = grams8.size() > kP8NibbleGrams;
+      for (unsigned long long x : grams8) {
+        const uint32_t g = (uint32_t)(x >> 2), bit = 1u << (x & 3);
+        if (nibble8) {
+          const uint32_t h = p8_h1<true>(g);
+          dmask8[p8_dmask_byte<true>(h)] |= (uint8_t)(bit << p8_dmask_shift<true>(h));
+        } else {
+          dmask8[p8_h1<false>(g)] |= (uint8_t)bit;
+        }
+      }
+    }
     while ((1ull << cap_log2) < 2 * keys.size()) ++cap_log2;
     jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
     const uint32_t mask = (1u << cap_log2) - 1;
@@ -923,6 +939,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
+  t->p8_nibble = nibble8;
   t->view.jump_depth = J;
   t->view.jump_cap_log2 = cap_log2;
   t->view.jump_bytes = (uint32_t)jump_bytes;

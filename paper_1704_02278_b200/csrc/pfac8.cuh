@@ -35,8 +35,7 @@ constexpr uint32_t kP8Stage = kP8Tile + 16;        // + words 512..515 (halo)
 constexpr uint32_t kP8Chunk = 1024;                // bytes sampled per iteration (8 words / lane)
 constexpr uint32_t kP8Queue = 32 + kP8Chunk / 4;    // candidate words: < 32 carried + one chunk
 constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
-constexpr uint32_t kP8DmaskLog2 = 16;
-constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;
+constexpr uint32_t kP8DmaskBytes = 1u << 16;        // level-1 d-mask table (shared memory)
 
 struct P8Layout {
   uint32_t bufs, bars, queue, hits, nh, dmask, bm2, cls, total;
@@ -78,8 +77,25 @@ struct P8Params {
 // Bloom variant halved the candidate words but doubled the bank-conflicted
 // shared-memory probes, which bound the kernel (measured: 3.63 -> 3.55 ms at
 // k=1,000 and 2.46 -> 1.97 ms at k=10 without it).  Built by glop_trie_upload.
-__host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) { return (g * 0x9E3779B1u) >> (32 - kP8DmaskLog2); }
-__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) { return dm[p8_h1(g)]; }
+// Two layouts of the same 64 KB: kNibble = false, 2^16 one-byte buckets
+// (bits 0..3 used); kNibble = true, 2^17 four-bit buckets -- half the hash
+// collisions for large pattern sets (DPI: 10,000 contents, ~40K grams) at
+// two more instructions per probe.  The host picks per automaton
+// (glop_trie_upload: nibbles above kP8NibbleGrams distinct grams).
+constexpr uint32_t kP8NibbleGrams = 12000;
+template <bool kNibble>
+__host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
+  return (g * 0x9E3779B1u) >> (kNibble ? 15 : 16);
+}
+template <bool kNibble>
+__host__ __device__ __forceinline__ uint32_t p8_dmask_byte(uint32_t h) { return kNibble ? h >> 1 : h; }
+template <bool kNibble>
+__host__ __device__ __forceinline__ uint32_t p8_dmask_shift(uint32_t h) { return kNibble ? (h & 1) << 2 : 0; }
+template <bool kNibble>
+__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
+  const uint32_t h = p8_h1<kNibble>(g);
+  return kNibble ? (dm[p8_dmask_byte<kNibble>(h)] >> p8_dmask_shift<kNibble>(h)) & 15u : dm[h];
+}
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
 // valid range [a, a + n)) into dst; bytes outside 16-byte granules are copied
@@ -132,7 +148,7 @@ __device__ __noinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, u
   return nb;
 }
 
-template <bool kWalk, typename Entry>
+template <bool kWalk, bool kNibble, typename Entry>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
@@ -268,14 +284,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
         if (lane == 31) w8 = wn;
         uint32_t m[8];
-        m[0] = p8_dmask(s_dmask, va.y);
-        m[1] = p8_dmask(s_dmask, va.z);
-        m[2] = p8_dmask(s_dmask, va.w);
-        m[3] = p8_dmask(s_dmask, vb.x);
-        m[4] = p8_dmask(s_dmask, vb.y);
-        m[5] = p8_dmask(s_dmask, vb.z);
-        m[6] = p8_dmask(s_dmask, vb.w);
-        m[7] = p8_dmask(s_dmask, w8);
+        m[0] = p8_dmask<kNibble>(s_dmask, va.y);
+        m[1] = p8_dmask<kNibble>(s_dmask, va.z);
+        m[2] = p8_dmask<kNibble>(s_dmask, va.w);
+        m[3] = p8_dmask<kNibble>(s_dmask, vb.x);
+        m[4] = p8_dmask<kNibble>(s_dmask, vb.y);
+        m[5] = p8_dmask<kNibble>(s_dmask, vb.z);
+        m[6] = p8_dmask<kNibble>(s_dmask, vb.w);
+        m[7] = p8_dmask<kNibble>(s_dmask, w8);
         const uint32_t lo4 = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
         const uint32_t hi4 = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
         if (__ballot_sync(0xffffffffu, (lo4 | hi4) != 0)) {
