@@ -821,7 +821,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   // pfac8 level 1 (outputs only at depth >= 8): bit d-1 of the bucket of the
   // 4-gram at offset d (1..4) of every 8-byte root path
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
-  std::vector<unsigned long long> grams8;  // (4-gram << 2 | d-1) of every 8-byte root path
+  std::vector<unsigned long long> grams8;  // (p8_gram << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
   bool nibble8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
@@ -867,7 +867,10 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       for (uint32_t x = 0; x < J; ++x) key |= (unsigned long long)path[x] << (8 * x);
       keys.push_back({key, s});
       if (p8)
-        for (uint32_t d = 1; d <= 4; ++d) grams8.push_back(((key >> (8 * d)) & 0xFFFFFFFFull) << 2 | (d - 1));
+        for (uint32_t d = 1; d <= 4; ++d) {
+          const uint32_t g = p8_gram((uint32_t)(key >> (8 * (d - 1))) << 24, (uint32_t)(key >> (8 * d)));
+          grams8.push_back((unsigned long long)g << 2 | (d - 1));
+        }
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
     });

@@ -91,6 +91,18 @@ template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_dmask_byte(uint32_t h) { return kNibble ? h >> 1 : h; }
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_dmask_shift(uint32_t h) { return kNibble ? (h & 1) << 2 : 0; }
+// Level-1 gram of sample word i: the 5 bytes [4i-1, 4i+4) -- the aligned
+// word `cur` and the top byte of the previous word -- which for a match at
+// c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes instead of
+// four cut the candidate words by ~40% on the syslog vocabulary set for one
+// shift + one multiply-add.  (GLOP_P8_Q4: the plain aligned 4-gram.)
+__host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur) {
+#ifdef GLOP_P8_Q4
+  return cur;
+#else
+  return (prev >> 24) * 0x2545F491u + cur;
+#endif
+}
 template <bool kNibble>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
   const uint32_t h = p8_h1<kNibble>(g);
@@ -284,14 +296,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
         if (lane == 31) w8 = wn;
         uint32_t m[8];
-        m[0] = p8_dmask<kNibble>(s_dmask, va.y);
-        m[1] = p8_dmask<kNibble>(s_dmask, va.z);
-        m[2] = p8_dmask<kNibble>(s_dmask, va.w);
-        m[3] = p8_dmask<kNibble>(s_dmask, vb.x);
-        m[4] = p8_dmask<kNibble>(s_dmask, vb.y);
-        m[5] = p8_dmask<kNibble>(s_dmask, vb.z);
-        m[6] = p8_dmask<kNibble>(s_dmask, vb.w);
-        m[7] = p8_dmask<kNibble>(s_dmask, w8);
+        m[0] = p8_dmask<kNibble>(s_dmask, p8_gram(va.x, va.y));
+        m[1] = p8_dmask<kNibble>(s_dmask, p8_gram(va.y, va.z));
+        m[2] = p8_dmask<kNibble>(s_dmask, p8_gram(va.z, va.w));
+        m[3] = p8_dmask<kNibble>(s_dmask, p8_gram(va.w, vb.x));
+        m[4] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.x, vb.y));
+        m[5] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.y, vb.z));
+        m[6] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.z, vb.w));
+        m[7] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.w, w8));
         const uint32_t lo4 = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
         const uint32_t hi4 = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
         if (__ballot_sync(0xffffffffu, (lo4 | hi4) != 0)) {
