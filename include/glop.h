@@ -184,6 +184,21 @@ glop_status glop_verify_hits_device(glop_ctx* ctx, const glop_rules* rules, cons
                                     uint64_t n_hits, glop_alert* d_out, uint64_t* n_alerts,
                                     uint64_t* d_counts);
 
+/* ---- LineIndex ------------------------------------------------------------
+ * Replaces LineIndex(text).line_of(offset) (verify.hpp:40-64) for many
+ * offsets at once: line = 1 + number of LF bytes before the offset (an LF
+ * belongs to the line it ends).  One HBM pass counts LFs per 4 KB block, a
+ * device scan makes them prefixes, one warp per offset finishes the count.
+ * glop_line_numbers: host offsets/lines (offsets <= n, else GLOP_EINVAL).
+ * glop_line_numbers_device: records are `stride`-byte structs whose first 8
+ * bytes are a global offset in [base, base+n) (glop_hit / glop_alert: stride
+ * 16; plain u64: 8); d_text holds global offsets [base, base+n). */
+glop_status glop_line_numbers(glop_ctx* ctx, const uint8_t* text, uint64_t n, int text_on_device,
+                              const uint64_t* offsets, uint64_t count, uint64_t* lines);
+glop_status glop_line_numbers_device(glop_ctx* ctx, const uint8_t* d_text, uint64_t n, uint64_t base,
+                                     const void* d_records, uint32_t stride, uint64_t count,
+                                     uint64_t* d_lines);
+
 /* ---- KMP ------------------------------------------------------------------
  * Replaces kmp_search (kmp.hpp:41-69): all start offsets (ascending,
  * overlapping included) of pattern p; `failure` is the reference failure

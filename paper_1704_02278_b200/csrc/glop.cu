@@ -15,11 +15,13 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "glop.h"
 #include "glop_kernels.cuh"
 #include "pfac8.cuh"
 #include "kmp.cuh"
+#include "lines.cuh"
 #include "logtrawl/automaton.hpp"
 #include "logtrawl/detail/abi.hpp"
 #include "workload.hpp"
@@ -88,6 +90,7 @@ struct glop_ctx {
   DBuf text, staging, out, dir, prefix, misc, keys, keys_alt, cub_tmp;
   DBuf keep, bcounts, bprefix, alerts, kmp_dfa, spill;
   DBuf sbuf[2];                                  // streamed text chunks (host-text pipeline)
+  DBuf lcount, lprefix, loffs;                   // device LineIndex
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   unsigned long long* h_misc = nullptr;  // pinned readback
@@ -660,6 +663,33 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   return GLOP_OK;
 }
 
+// Device LineIndex (lines.cuh): lines[i] = line of record i's offset (u64
+// at byte 0 of each `stride`-byte record) in text d_text = global [base, base+n).
+glop_status line_numbers_impl(glop_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t base, const void* d_recs,
+                              uint32_t stride, uint64_t count, uint64_t* d_lines) {
+  if (count == 0) return GLOP_OK;
+  const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
+  const uint64_t nblocks = (n + a + kLineBlock - 1) / kLineBlock;
+  TRY(c->lcount.ensure(nblocks * 8));
+  TRY(c->lprefix.ensure(nblocks * 8));
+  const uint8_t* A = d_text - a;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((nblocks + 7) / 8, 16u * c->num_sms);
+  c->launches += 3;
+  lf_block_count_kernel<<<grid, 256, 0, c->stream>>>(A, a, n, nblocks, c->lcount.as<unsigned long long>());
+  CU(cudaGetLastError());
+  size_t tmp = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->lcount.as<unsigned long long>(),
+                                   c->lprefix.as<unsigned long long>(), (int64_t)nblocks, c->stream));
+  TRY(c->cub_tmp.ensure(tmp));
+  CU(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->lcount.as<unsigned long long>(),
+                                   c->lprefix.as<unsigned long long>(), (int64_t)nblocks, c->stream));
+  const uint32_t g2 = (uint32_t)std::min<uint64_t>((count + 7) / 8, 16u * c->num_sms);
+  lines_of_kernel<<<g2, 256, 0, c->stream>>>(A, a, base, c->lprefix.as<unsigned long long>(), d_recs, stride, count,
+                                             reinterpret_cast<unsigned long long*>(d_lines));
+  CU(cudaGetLastError());
+  return GLOP_OK;
+}
+
 }  // namespace
 
 // ============================================================== C ABI
@@ -705,7 +735,7 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
-                  &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1]})
+                  &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1], &c->lcount, &c->lprefix, &c->loffs})
     b->release();
   if (c->cstream) {
     cudaStreamSynchronize(c->cstream);
@@ -1271,6 +1301,34 @@ glop_status glop_run_pfac_pipeline_shard(glop_ctx* c, const glop_trie* t, const 
   }
   *alerts = a;
   *n_alerts = kept;
+  return GLOP_OK;
+}
+
+glop_status glop_line_numbers_device(glop_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t base,
+                                     const void* d_records, uint32_t stride, uint64_t count, uint64_t* d_lines) {
+  if (!c || (count && (!d_text || !d_records || !d_lines)) || stride < 8)
+    return fail(GLOP_EINVAL, "glop_line_numbers_device: bad argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  return line_numbers_impl(c, d_text, n, base, d_records, stride, count, d_lines);
+}
+
+glop_status glop_line_numbers(glop_ctx* c, const uint8_t* text, uint64_t n, int text_on_device,
+                              const uint64_t* offsets, uint64_t count, uint64_t* lines) {
+  if (!c || (count && (!offsets || !lines))) return fail(GLOP_EINVAL, "glop_line_numbers: null argument");
+  for (uint64_t i = 0; i < count; ++i)
+    if (offsets[i] > n) return fail(GLOP_EINVAL, "glop_line_numbers: offset past the end of text");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  if (count == 0) return GLOP_OK;
+  const uint8_t* d_text = nullptr;
+  TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  TRY(c->loffs.ensure(count * 16));
+  uint64_t* d_offs = c->loffs.as<uint64_t>();
+  CU(cudaMemcpyAsync(d_offs, offsets, count * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(line_numbers_impl(c, d_text, n, 0, d_offs, 8, count, d_offs + count));
+  CU(cudaMemcpyAsync(lines, d_offs + count, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   return GLOP_OK;
 }
 

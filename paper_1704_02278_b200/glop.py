@@ -109,6 +109,8 @@ _sig("glop_gen_syslog_device", vp, vp, C.c_uint64, C.c_uint64, C.c_uint64)
 _sig("glop_gen_syslog_host", vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint)
 _sig("glop_gen_reference_log", vp, C.c_uint64, C.c_uint32, C.c_uint64)
 _sig("glop_gen_payload_device", vp, vp, C.c_uint64, C.c_uint64, C.c_uint64)
+_sig("glop_line_numbers", vp, vp, C.c_uint64, C.c_int, u64p, C.c_uint64, u64p)
+_sig("glop_line_numbers_device", vp, vp, C.c_uint64, C.c_uint64, vp, C.c_uint32, C.c_uint64, vp)
 _sig("glop_gen_payload_host", vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint)
 _sig("glop_gen_dpi_rules", C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u8p, u64p)
 _sig("glop_gen_rules", C.c_uint32, C.c_uint32, C.c_uint32, u8p, u8p)
@@ -353,6 +355,20 @@ class Context:
                                                  1 if on_device else 0, C.byref(p), C.byref(na),
                                                  cnt.ctypes.data_as(u64p), C.byref(s1)), "run_pfac_pipeline")
         return _take(p, na.value, ALERT_DTYPE), cnt[:rules.n_patterns], s1.value
+
+    def line_numbers(self, text, offsets) -> np.ndarray:
+        """LineIndex(text).line_of(o) for every o (verify.hpp:40-64), on the device."""
+        t = _u8(text)
+        o = np.ascontiguousarray(offsets, dtype=np.uint64)
+        out = np.zeros(o.size, dtype=np.uint64)
+        _check(_lib.glop_line_numbers(self.h, _ptr(t), t.size, 0, o.ctypes.data_as(u64p), o.size,
+                                      out.ctypes.data_as(u64p)), "line_numbers")
+        return out
+
+    def line_numbers_device(self, d_text: int, n: int, d_records: int, stride: int, count: int, d_lines: int,
+                            base: int = 0):
+        _check(_lib.glop_line_numbers_device(self.h, d_text, n, base, d_records, stride, count, d_lines),
+               "line_numbers_device")
 
     def last_kernel_ms(self) -> float:
         ms = C.c_float()

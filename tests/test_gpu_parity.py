@@ -363,3 +363,47 @@ def test_dpi_payloads_vs_oracle(ctx, torch_cuda):
     assert np.array_equal(alerts["offset"], ref_alerts["offset"])
     assert np.array_equal(alerts["rule_id"], ref_alerts["rule_id"])
     assert counts.sum() == len(alerts)
+
+
+def test_device_line_index(ctx, torch_cuda):
+    """Device LineIndex (SURVEY §8f row 1) == LineIndex::line_of
+    (verify.hpp:40-64, via the oracle) and == the reference's golden alert
+    lines; offsets at LFs, block edges, 0 and n; unaligned text; the device
+    form on alert records with a shard base."""
+    t = glop.gen_syslog_host(3_000_017, seed=12)
+    rng = np.random.default_rng(4)
+    nl = np.flatnonzero(t == 10)
+    offs = np.concatenate([[0, t.size, 4095, 4096, 4097], nl[:50], nl[:50] + 1,
+                           rng.integers(0, t.size, 5000)]).astype(np.uint64)
+    want = (np.searchsorted(nl, offs.astype(np.int64), side="left") + 1).astype(np.uint64)
+    assert [O.line_of(t, int(o)) for o in offs[:60]] == want[:60].tolist()  # the oracle pins the rule
+    assert np.array_equal(ctx.line_numbers(t, offs), want)
+    t3 = t[3:]
+    o3 = offs[offs <= t3.size]
+    assert np.array_equal(ctx.line_numbers(t3, o3),
+                          np.searchsorted(np.flatnonzero(t3 == 10), o3.astype(np.int64), side="left") + 1)
+    # the reference's own alert lines (acceptance.cpp:183-206 fixture)
+    (rec,) = G.load("determinism")
+    text = bytearray(glop.gen_reference_log(10_000_000, 1111, 80).tobytes())
+    rng2 = G.MT19937(1313)
+    for _ in range(50):
+        p = rec.patterns[rng2() % len(rec.patterns)]
+        pos = rng2() % (len(text) - len(p))
+        text[pos:pos + len(p)] = p
+    text = np.frombuffer(bytes(text), np.uint8)
+    assert len(rec.alerts) > 0 and rec.alerts["line"].all()
+    assert np.array_equal(ctx.line_numbers(text, rec.alerts["offset"]), rec.alerts["line"])
+    # device form over alert records (stride 16) of a shard at global base
+    base = 7 << 30
+    pats, _ = glop.gen_rules(300, seed=9)
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    rules = ctx.upload_rules(pats, 8)
+    d = torch_cuda.from_numpy(t.copy()).cuda()
+    alerts, _, _ = ctx.run_pfac_pipeline(trie, rules, d.data_ptr(), t.size, True, base=base)
+    assert len(alerts) > 100
+    da = torch_cuda.from_numpy(alerts.view(np.uint8).copy()).cuda()
+    dl = torch_cuda.zeros(len(alerts), dtype=torch_cuda.int64, device="cuda")
+    ctx.line_numbers_device(d.data_ptr(), t.size, da.data_ptr(), 16, len(alerts), dl.data_ptr(), base=base)
+    ctx.synchronize()
+    ref = [O.line_of(t, int(o) - base) for o in alerts["offset"]]
+    assert dl.cpu().numpy().tolist() == ref
