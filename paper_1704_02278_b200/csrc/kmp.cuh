@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     s_misc[0] = 0;
+    s_misc[1] = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
     };
     auto record = [&](unsigned long long x) {  // match ending at A coordinate x
       if (p.mode == 0) {
-        const uint32_t slot = atomicAdd(&s_misc[0], 1u);
+        const uint32_t slot = atomicAdd(&s_misc[k & 1], 1u);
         if (slot < kK2HitCap) s_keys[slot] = x - tT;
       } else {
         const unsigned long long slot = atomicAdd(p.g_count, 1ull);
@@ -136,27 +137,15 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
     unsigned long long c0 = tT + (unsigned long long)tid * kK2Chunk;
     if (c0 < a) c0 = a;
     const unsigned long long c1 = min(tT + (unsigned long long)(tid + 1) * kK2Chunk, e_end);
-    // Walks end positions [from, to) (A coordinates) from state j; in state 0
-    // only p[0] bytes (found 16 at a time) step the DFA.  kCount: add the
-    // reference's comparisons and record matches (the warm-up does neither).
-    auto walk = [&](auto kCount, unsigned long long from, unsigned long long to, uint32_t& j,
-                    unsigned long long& cmp) {
-      for (unsigned long long g = from & ~15ull; g < to; g += 16) {
-        const uint32_t kb = from > g ? (uint32_t)(from - g) : 0u;
-        const uint32_t ke = to - g < 16 ? (uint32_t)(to - g) : 16u;
-        const long long y = (long long)(g - tT) + kK2Pre;
-        if (y < 0 || y + 16 > (long long)kK2Stage) {  // outside the window (long patterns)
-          for (uint32_t kk = kb; kk < ke; ++kk) {
-            const uint32_t e = D[j * 256 + abyte(g + kk)];
-            if (decltype(kCount)::value) {
-              cmp += e >> 14;
-              if (e & 0x2000u) record(g + kk);
-            }
-            j = e & 0x1FFFu;
-          }
-          continue;
-        }
-        const uint4 v = *reinterpret_cast<const uint4*>(win + y);
+    // Walks window bytes [yf, yt) from state j (window byte y is A coordinate
+    // tT - kK2Pre + y); in state 0 only p[0] bytes (found 16 at a time) step
+    // the DFA.  kCount: add the reference's comparisons and record matches
+    // (the warm-up does neither).
+    auto walk = [&](auto kCount, uint32_t yf, uint32_t yt, uint32_t& j, unsigned long long& cmp) {
+      for (uint32_t g = yf & ~15u; g < yt; g += 16) {
+        const uint32_t kb = yf > g ? yf - g : 0u;
+        const uint32_t ke = min(yt - g, 16u);
+        const uint4 v = *reinterpret_cast<const uint4*>(win + g);
         const uint32_t z0 = k2_zero_bytes(v.x, x4), z1 = k2_zero_bytes(v.y, x4), z2 = k2_zero_bytes(v.z, x4),
                        z3 = k2_zero_bytes(v.w, x4);
         if (j == 0 && !(z0 | z1 | z2 | z3)) {
@@ -177,22 +166,32 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
             if (decltype(kCount)::value) cmp += s - kk;
             kk = s;
           }
-          const uint32_t e = D[j * 256 + win[y + kk]];
+          const uint32_t e = D[j * 256 + win[g + kk]];
           if (decltype(kCount)::value) {
             cmp += e >> 14;
-            if (e & 0x2000u) record(g + kk);
+            if (e & 0x2000u) record(tT - kK2Pre + g + kk);
           }
           j = e & 0x1FFFu;
           ++kk;
         }
       }
     };
+    if (tid == 0 && p.mode == 0) s_misc[(k + 1) & 1] = 0;  // the next tile's match counter
     if (c0 < c1) {
-      // warm-up: the state at c0 from the m-1 bytes before it
+      const uint32_t y0 = (uint32_t)(c0 - tT) + kK2Pre, y1 = (uint32_t)(c1 - tT) + kK2Pre;
+      // warm-up: the state at c0 from the m-1 bytes before it (clamped to the text start)
       uint32_t j = 0;
       unsigned long long cmp = 0;
-      walk(std::false_type{}, c0 - min(c0 - a, (unsigned long long)(m - 1)), c0, j, cmp);
-      walk(std::true_type{}, c0, c1, j, cmp);
+      const unsigned long long wlo = c0 - min(c0 - a, (unsigned long long)(m - 1));
+      if (wlo + kK2Pre >= tT) {
+        walk(std::false_type{}, (uint32_t)(wlo + kK2Pre - tT), y0, j, cmp);
+      } else {  // long patterns: warm-up bytes before the window
+        for (unsigned long long x = wlo; x < c0; ++x) {
+          const uint32_t b = abyte(x);
+          if (j != 0 || b == p.p0) j = D[j * 256 + b] & 0x1FFFu;
+        }
+      }
+      walk(std::true_type{}, y0, y1, j, cmp);
       cmp_total += cmp;
     }
     __syncthreads();
@@ -204,7 +203,11 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
       }
     }
     if (p.mode != 0) continue;
-    const uint32_t nh = s_misc[0];
+    const uint32_t nh = s_misc[k & 1];
+    if (nh == 0) {  // common case: no match in the tile, no further barrier
+      if (tid == 0) p.dir[t] = TileDir{0ull, 0u, 0u};
+      continue;
+    }
     const bool over = nh > kK2HitCap;
     if (!over && nh > 1) {
       uint32_t P = 1;
@@ -224,20 +227,16 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
         }
     }
     if (tid == 0) {
-      const unsigned long long slot = nh ? atomicAdd(p.g_count, (unsigned long long)nh) : 0ull;
-      p.dir[t].slot = slot;
-      p.dir[t].count = nh;
-      p.dir[t].overflow = over;
+      const unsigned long long slot = atomicAdd(p.g_count, (unsigned long long)nh);
+      p.dir[t] = TileDir{slot, nh, over ? 1u : 0u};
       if (over) atomicOr(p.g_flags, 1u);
-      s_misc[1] = (uint32_t)slot;
-      s_misc[2] = (uint32_t)(slot >> 32);
+      s_misc[2] = (uint32_t)slot;
+      s_misc[3] = (uint32_t)(slot >> 32);
     }
     __syncthreads();
-    const unsigned long long slot = (unsigned long long)s_misc[1] | ((unsigned long long)s_misc[2] << 32);
+    const unsigned long long slot = (unsigned long long)s_misc[2] | ((unsigned long long)s_misc[3] << 32);
     if (!over && slot + nh <= p.staging_cap)
       for (uint32_t h = tid; h < nh; h += kK2Threads) p.staging[slot + h] = p.base + tT + s_keys[h] - a + 1 - m;
-    __syncthreads();
-    if (tid == 0) s_misc[0] = 0;
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) cmp_total += __shfl_xor_sync(0xffffffffu, cmp_total, o);
