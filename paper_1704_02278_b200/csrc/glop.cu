@@ -907,7 +907,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
     if (p8) {
       std::sort(grams8.begin(), grams8.end());
       grams8.erase(std::unique(grams8.begin(), grams8.end()), grams8.end());
-      nibble8 = grams8.size() > kP8NibbleGrams;
+      const char* env = getenv("GLOP_P8_NIBBLE_MIN");  // experiments: override the layout threshold
+      nibble8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8NibbleGrams);
       for (unsigned long long x : grams8) {
         const uint32_t g = (uint32_t)(x >> 2), bit = 1u << (x & 3);
         if (nibble8) {
