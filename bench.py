@@ -211,16 +211,17 @@ def run_reference(args):
 def workload_config(args, world):
     if args.config == "dpi":
         what = ("configs[4] DPI mode: PFAC, %d Snort-style contents (8..24 bytes; 8-byte prefixes + stage-2 "
-                "verify), %.0f GB synthetic packet payloads per GPU" % (args.patterns, args.bytes_per_gpu / 1e9))
+                "verify), %g GB synthetic packet payloads per GPU" % (args.patterns, args.bytes_per_gpu / 1e9))
     else:
-        what = ("configs[2]/[3]: PFAC, %d patterns (8-byte prefixes), %.0f GB synthetic RFC 5424 syslog per GPU"
+        what = ("configs[2]/[3]: PFAC, %d patterns (8-byte prefixes), %g GB synthetic RFC 5424 syslog per GPU"
                 % (args.patterns, args.bytes_per_gpu / 1e9))
     return {"workload": what,
             "bytes_per_gpu": int(args.bytes_per_gpu), "total_bytes": int(args.bytes_per_gpu) * world,
             "patterns": args.patterns, "prefix_len": args.prefix_len, "corpus_seed": args.seed,
             "rules_seed": args.rules_seed, "kernel": args.kernel,
             "parallelism": f"shard{world} (contiguous log shards, 7-byte halo)",
-            "l2": "inputs larger than L2 (>= 8 GB per GPU), no flush needed"}
+            "l2": ("inputs larger than L2 (%g GB per GPU vs 126 MB L2), no flush needed" % (args.bytes_per_gpu / 1e9)
+                   if args.bytes_per_gpu > 1e9 else "small run: inputs may be L2-resident (not a bench number)")}
 
 
 # --------------------------------------------------------------------- glop arm
@@ -233,14 +234,22 @@ def main():
     import torch.distributed as dist
 
     from paper_1704_02278_b200 import glop
-    from paper_1704_02278_b200.shards import plan_shards
+    from paper_1704_02278_b200.shards import gather_alerts_to_root, plan_shards
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GLOP_BENCH_ONE_GPU=1: functional check of the N>1 path on a one-GPU box
+    # (all ranks on cuda:0, gloo instead of NCCL); never used for numbers.
+    one_gpu = os.environ.get("GLOP_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -284,9 +293,10 @@ def main():
                                   base=sh.lo, kernel=kernel)
         na = ctx.verify_hits_device(rules, d_text.data_ptr(), sh.read, d_hits.data_ptr(), nh, d_alerts.data_ptr(),
                                     d_counts.data_ptr(), base=sh.lo)
-        if world > 1:
+        if world > 1:  # the one exchange: count all-reduce + alert gather to rank 0 (NCCL over NVLink)
             with torch.cuda.stream(stream):
                 dist.all_reduce(d_counts)
+                gather_alerts_to_root(d_alerts.view(-1, 16), na, root=0)
         return nh, na
 
     for _ in range(max(args.warmup, 3)):

@@ -71,6 +71,40 @@ def gather_alerts(alerts, n: int, group=None):
     return torch.cat([b[:s] for b, s in zip(bufs, sizes)], dim=0)
 
 
+def gather_alerts_to_root(alerts, n: int, root: int = 0, group=None):
+    """Gather each rank's first n alert rows (a 2-D torch tensor, one row per
+    alert) to `root` only, concatenated in rank order (already globally
+    sorted: owned ranges are ascending and disjoint).  One all_gather of the
+    row counts, then point-to-point sends to the root (NCCL send/recv over
+    NVLink on the B200 box; gloo in the CPU tests).  Returns the
+    concatenation on the root and None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if alerts.is_cuda and dist.get_backend(group) == "gloo":  # gloo p2p moves host memory only
+        out = gather_alerts_to_root(alerts[:n].cpu(), n, root, group)
+        return None if out is None else out.to(alerts.device)
+    cnt = torch.tensor([n], dtype=torch.int64, device=alerts.device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    sizes = [int(c.item()) for c in cnts]
+    if rank != root:
+        if n:
+            dist.send(alerts[:n].contiguous(), dst=root, group=group)
+        return None
+    parts = []
+    for r, sz in enumerate(sizes):
+        if r == root:
+            parts.append(alerts[:n])
+        elif sz:
+            buf = torch.empty((sz,) + tuple(alerts.shape[1:]), dtype=alerts.dtype, device=alerts.device)
+            dist.recv(buf, src=r, group=group)
+            parts.append(buf)
+    return torch.cat(parts, dim=0) if parts else alerts[:0]
+
+
 def merge_host(parts: list[np.ndarray]) -> np.ndarray:
     """Rank-order concatenation (globally sorted by construction)."""
     return np.concatenate(parts) if parts else np.zeros(0)

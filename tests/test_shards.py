@@ -65,7 +65,7 @@ def _worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
 
-    from paper_1704_02278_b200.shards import gather_alerts, reduce_counts
+    from paper_1704_02278_b200.shards import gather_alerts, gather_alerts_to_root, reduce_counts
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -79,6 +79,10 @@ def _worker(rank, world, port, q):
         reduce_counts(counts)
         rows = torch.from_numpy(hits.view(np.uint8).reshape(-1, 16).copy())
         allrows = gather_alerts(rows, len(hits))
+        root = gather_alerts_to_root(rows, len(hits), root=0)
+        assert (root is None) == (rank != 0)
+        if root is not None:
+            assert root.numpy().tobytes() == allrows.numpy().tobytes()
         q.put((rank, counts.numpy().tobytes(), allrows.numpy().tobytes()))
     finally:
         dist.destroy_process_group()
