@@ -22,18 +22,14 @@
 
 namespace glop {
 
-constexpr int kThreads = 512;
 constexpr uint32_t kTile = 4096;            // owned start positions per tile
 constexpr uint32_t kHalo = 64;              // bytes past the tile kept in smem
 constexpr uint32_t kStageBytes = kTile + kHalo + 16;  // +16: alignment slack
-constexpr int kStages = 4;
-constexpr uint32_t kHitCap = 2048;          // per-tile hit keys in smem
 constexpr uint32_t kDmaskBits = 15;         // level-1 q-gram d-mask: 2^15 buckets
 constexpr uint32_t kDmaskBytes = 1u << kDmaskBits;
 constexpr uint32_t kBm2Log2 = 18;
 constexpr uint32_t kBm2Bits = 1u << kBm2Log2;  // level-2 prefix bitmap
 constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
-constexpr uint32_t kQueueCap = 4096;        // per-tile filter survivors
 
 struct TileDir {
   unsigned long long slot;
@@ -57,23 +53,11 @@ struct DevTrie {
   uint32_t jump_depth, jump_cap_log2, jump_bytes;
 };
 
-struct ScanParams {
-  const uint8_t* text;
-  unsigned long long n, own, base;
-  uint32_t num_tiles;
-  int mode;  // 0: per-tile sorted staging + directory; 1: global keys
-  struct glop_hit_t {
-    unsigned long long offset;
-    uint32_t pid, len;
-  }* staging;
-  unsigned long long staging_cap;
-  unsigned long long* g_count;  // total hits (all tiles)
-  TileDir* dir;
-  unsigned int* g_flags;        // bit0: some tile overflowed its smem buffer
-  unsigned long long* keys;     // mode 1: (offset << 24) | pid
-  unsigned long long keys_cap;
+// Device twin of glop_hit / logtrawl::Hit (scan.hpp:31-41): 16 bytes.
+struct DevHit {
+  unsigned long long offset;
+  uint32_t pid, len;
 };
-using DevHit = ScanParams::glop_hit_t;
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -191,43 +175,6 @@ template <>
 struct EntryTraits<uint32_t> {
   static constexpr uint32_t kFlag = 0x80000000u, kMask = 0x7FFFFFFFu;
 };
-
-// ------------------------------------------------------------------ tile sort
-// Ascending bitonic sort of keys[0, P), P a power of two <= kHitCap.
-__device__ __forceinline__ void sort_keys(unsigned long long* keys, uint32_t P) {
-  if (P <= 1) return;
-  const int tid = threadIdx.x;
-  if (P <= 64) {
-    if (tid < 32) {
-      for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-          for (uint32_t x = tid; x < P; x += 32) {
-            uint32_t y = x ^ j;
-            if (y > x) {
-              unsigned long long u = keys[x], v = keys[y];
-              bool up = (x & k) == 0;
-              if ((u > v) == up) keys[x] = v, keys[y] = u;
-            }
-          }
-          __syncwarp();
-        }
-    }
-    __syncthreads();
-    return;
-  }
-  for (uint32_t k = 2; k <= P; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t x = tid; x < P; x += kThreads) {
-        uint32_t y = x ^ j;
-        if (y > x) {
-          unsigned long long u = keys[x], v = keys[y];
-          bool up = (x & k) == 0;
-          if ((u > v) == up) keys[x] = v, keys[y] = u;
-        }
-      }
-      __syncthreads();
-    }
-}
 
 // ------------------------------------------------------------------ K1 PFAC
 // Shared-memory layout (byte offsets), computed on the host per automaton.
