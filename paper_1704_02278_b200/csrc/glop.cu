@@ -241,6 +241,14 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
     p.g_count = g;
     p.dmask8 = t->view.dmask8;
     TRY(launch(p));
+    // ordered output, enqueued before the flags are known (see p8_gather_kernel)
+    c->launches += 2;
+    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
+                                                 c->prefix.as<unsigned long long>());
+    p8_gather_kernel<DevHit><<<(uint32_t)regions, 256, 0, c->stream>>>(
+        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
+        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out), cap);
+    CU(cudaGetLastError());
     TRY(sync_read(c, c->misc.p, 32));
     const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[2];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
@@ -284,14 +292,6 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
       continue;
     }
     if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
-    if (total == 0) return GLOP_OK;
-    c->launches += 2;
-    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
-                                                 c->prefix.as<unsigned long long>());
-    p8_gather_kernel<<<(uint32_t)regions, 256, 0, c->stream>>>(
-        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
-        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out));
-    CU(cudaGetLastError());
     return GLOP_OK;
   }
   return fail(GLOP_ECUDA, "pfac_scan: staging did not converge");
@@ -441,21 +441,24 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
   CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), dfa.size() * 4, cudaMemcpyHostToDevice, c->stream));
   const uint64_t end_lim = std::min<uint64_t>(own + m - 1, n);  // starts < own
   const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
-  const uint32_t num_tiles = (uint32_t)((end_lim + a + kK2Tile - 1) / kK2Tile);
-  TRY(c->dir.ensure(sizeof(TileDir) * num_tiles));
-  TRY(c->prefix.ensure(sizeof(unsigned long long) * num_tiles));
+  const uint32_t num_tiles = (uint32_t)((end_lim + a + kK3Tile - 1) / kK3Tile);
+  const int grid = (int)std::min<uint32_t>((num_tiles + kK3Warps - 1) / kK3Warps, (uint32_t)c->num_sms);
+  const uint32_t per = (num_tiles + grid - 1) / grid, sub = (per + kK3Warps - 1) / kK3Warps;
+  const unsigned long long regions = (unsigned long long)grid * kK3Warps;
+  TRY(c->bcounts.ensure(8 * regions));
+  TRY(c->prefix.ensure(8 * regions));
   TRY(c->misc.ensure(64));
-  size_t want = std::max<size_t>(1 << 20, own / 1024);
-  if (c->staging.bytes < want * 8) TRY(c->staging.ensure(want * 8));
-  auto* g_count = c->misc.as<unsigned long long>();
-  const bool smem_dfa = m <= kK2SmemDfaMax;
-  const size_t smem = K2Smem::kDfa + (smem_dfa ? (size_t)m * 1024 : 0);
-  const int grid = (int)std::min<uint32_t>(num_tiles, (uint32_t)c->num_sms);
-  auto launch = [&](const K2Params& p) -> glop_status {
-    auto k = smem_dfa ? kmp2_kernel<true> : kmp2_kernel<false>;
-    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  unsigned long long region = std::max<unsigned long long>(256, (own / 8192 + regions - 1) / regions);
+  if (c->staging.bytes < region * regions * 8) TRY(c->staging.ensure(region * regions * 8));
+  region = c->staging.bytes / 8 / regions;
+  auto* g = c->misc.as<unsigned long long>();
+  const bool smem_dfa = m <= kK3SmemDfaMax;
+  const K3Layout L = make_k3_layout(m, smem_dfa);
+  auto launch = [&](const K3Params& p) -> glop_status {
+    auto k = smem_dfa ? kmp3_kernel<true> : kmp3_kernel<false>;
+    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     CU(cudaEventRecord(c->ev0, c->stream));
-    k<<<grid, kK2Threads, smem, c->stream>>>(p);
+    k<<<grid, kK3Threads, L.total, c->stream>>>(p, L);
     CU(cudaGetLastError());
     CU(cudaEventRecord(c->ev1, c->stream));
     c->timed = true;
@@ -464,58 +467,58 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
   };
   for (int attempt = 0; attempt < 3; ++attempt) {
     CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
-    K2Params p{};
+    K3Params p{};
     p.text = d_text;
     p.n = n;
     p.end_lim = end_lim;
     p.base = base;
     p.m = m;
-    p.num_tiles = num_tiles;
     p.p0 = pat[0];
+    p.num_tiles = num_tiles;
+    p.per = per;
+    p.sub = sub;
     p.dfa = c->kmp_dfa.as<uint32_t>();
     p.staging = c->staging.as<unsigned long long>();
-    p.staging_cap = c->staging.bytes / 8;
-    p.g_count = g_count;
-    p.dir = c->dir.as<TileDir>();
-    p.g_flags = reinterpret_cast<unsigned int*>(g_count + 1);
-    p.comparisons = g_count + 2;
+    p.region = region;
+    p.counts = c->bcounts.as<unsigned long long>();
+    p.g_count = g;
+    p.comparisons = g + 2;
     TRY(launch(p));
-    TRY(sync_read(c, c->misc.p, 24));
-    const unsigned long long total = c->h_misc[0];
+    // ordered output, enqueued before the flags are known (see p8_gather_kernel)
+    c->launches += 2;
+    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
+                                                 c->prefix.as<unsigned long long>());
+    p8_gather_kernel<unsigned long long><<<(uint32_t)regions, 256, 0, c->stream>>>(
+        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
+        c->staging.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), cap);
+    CU(cudaGetLastError());
+    TRY(sync_read(c, c->misc.p, 32));
+    const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[3];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
     *n_offsets = total;
-    if (comparisons) *comparisons += c->h_misc[2];
     if (flags & 1u) {
-      // > kK2HitCap matches in one tile: exact fallback -- every match as a
+      // > kK3Hits matches in one warp tile: exact fallback -- every match as a
       // global key, then a device radix sort.
+      if (comparisons) *comparisons += c->h_misc[2];
       if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
       TRY(c->keys.ensure(total * 8 + 8));
       CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
       p.mode = 1;
       p.keys = c->keys.as<unsigned long long>();
       p.keys_cap = total;
-      p.comparisons = g_count + 3;  // already counted by the first pass
       TRY(launch(p));
       TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), total));
       CU(cudaStreamSynchronize(c->stream));
       return GLOP_OK;
     }
-    if (total > p.staging_cap) {
+    if (maxregion > region) {  // a warp's staging region overflowed: grow, rerun
+      region = maxregion + maxregion / 4 + 64;
       c->staging.release();
-      TRY(c->staging.ensure(total * 8 + (1 << 20)));
-      if (comparisons) *comparisons -= c->h_misc[2];
+      TRY(c->staging.ensure(region * regions * 8));
       continue;
     }
+    if (comparisons) *comparisons += c->h_misc[2];
     if (total > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
-    if (total == 0) return GLOP_OK;
-    c->launches += 2;
-    tile_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->dir.as<TileDir>(), num_tiles,
-                                                  c->prefix.as<unsigned long long>());
-    gather_kernel<unsigned long long>
-        <<<std::min<uint32_t>((num_tiles + 7) / 8, 4 * c->num_sms), 256, 0, c->stream>>>(
-            c->dir.as<TileDir>(), c->prefix.as<unsigned long long>(), num_tiles,
-            c->staging.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out));
-    CU(cudaGetLastError());
     return GLOP_OK;
   }
   return fail(GLOP_ECUDA, "kmp_search: staging did not converge");

@@ -5,7 +5,7 @@
 //                         bitmap in shared memory, then the trie walk only for
 //                         survivors (GPU analogue of RootJump, scan.hpp:81-108)
 //                         DIRECT:   one thread per start byte, literal walk
-//   tile_prefix / gather  K2  deterministic (offset, pattern_id) order
+//   seg_reduce / seg_gather  K2  deterministic (offset, pattern_id) order
 //                         (scan.hpp:197-201) without a global sort
 //   verify_*          K3  stage-2 suffix check (verify.hpp:69-105)
 //   (K4 KMP: kmp.cuh; the 8-byte-prefix PFAC fast path: pfac8.cuh)
@@ -30,12 +30,6 @@ constexpr uint32_t kDmaskBytes = 1u << kDmaskBits;
 constexpr uint32_t kBm2Log2 = 18;
 constexpr uint32_t kBm2Bits = 1u << kBm2Log2;  // level-2 prefix bitmap
 constexpr uint32_t kBm2Bytes = kBm2Bits / 8;
-
-struct TileDir {
-  unsigned long long slot;
-  uint32_t count;
-  uint32_t overflow;
-};
 
 struct JumpEntry;
 struct DevTrie {
@@ -690,45 +684,6 @@ __global__ void __launch_bounds__(1024) seg_gather_kernel(const SegDir* dir, uns
     const unsigned long long src = (unsigned long long)dir[seg].region * region + dir[seg].cursor;
     for (uint32_t h = 0; h < c[i]; ++h) out[dst + h] = staging[src + h];
     dst += c[i];
-  }
-}
-
-// Exclusive prefix of per-tile counts (single CTA, any number of tiles).
-__global__ void __launch_bounds__(1024) tile_prefix_kernel(const TileDir* dir, uint32_t num_tiles,
-                                                           unsigned long long* prefix) {
-  __shared__ unsigned long long part[1024];
-  const uint32_t tid = threadIdx.x;
-  const uint32_t per = (num_tiles + 1023) / 1024;
-  const uint32_t b = tid * per, e = min(num_tiles, b + per);
-  unsigned long long s = 0;
-  for (uint32_t i = b; i < e; ++i) s += dir[i].count;
-  part[tid] = s;
-  __syncthreads();
-  for (uint32_t off = 1; off < 1024; off <<= 1) {
-    unsigned long long v = tid >= off ? part[tid - off] : 0;
-    __syncthreads();
-    part[tid] += v;
-    __syncthreads();
-  }
-  unsigned long long run = part[tid] - s;
-  for (uint32_t i = b; i < e; ++i) {
-    prefix[i] = run;
-    run += dir[i].count;
-  }
-}
-
-// Copies each tile's sorted hits from staging to its final position (one warp
-// per tile).
-template <typename Rec>
-__global__ void gather_kernel(const TileDir* dir, const unsigned long long* prefix, uint32_t num_tiles,
-                              const Rec* staging, Rec* out) {
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t t = warp; t < num_tiles; t += nw) {
-    const uint32_t c = dir[t].count;
-    const Rec* src = staging + dir[t].slot;
-    Rec* dst = out + prefix[t];
-    for (uint32_t h = lane; h < c; h += 32) dst[h] = src[h];
   }
 }
 

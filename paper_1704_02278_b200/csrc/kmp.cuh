@@ -4,51 +4,65 @@
 // The reference's failure-function loop is replayed on the host into a DFA
 // over (state, byte): entry = next state (13 bits) | match << 13 |
 // comparisons << 14, so the sequential comparison count is reproduced step
-// by step.  Each of the 512 threads of a CTA owns 144 consecutive END
-// positions of a 73,728-byte tile (144 = 9 x 16 bytes: the 32 lanes' LDS.128
-// hit distinct banks); the state at its first position is recovered by a
-// warm-up over the previous m-1 bytes (the KMP state depends only on them).
-// In state 0 a byte other than p[0] costs exactly one comparison and keeps
-// state 0, so a thread skips 16-byte groups without p[0] (SWAR test on the
-// registers of one LDS.128) and jumps to the next p[0] inside a group; only
-// bytes after a p[0] walk the DFA.  Tiles stream HBM -> shared memory by
-// 1-D TMA (cp.async.bulk) into a 2-stage ring; matches are ordered per tile
-// (shared-memory bitonic sort of the few keys) and laid out by the tile
-// directory (tile_prefix_kernel + gather_kernel).
+// by step.  Each lane owns 144 consecutive match END positions (144 = 9 x 16
+// bytes: the warp's LDS.128 hit distinct banks); the state at its first
+// position is recovered by a warm-up over the previous m-1 bytes (the KMP
+// state depends only on them).  In state 0 a byte other than p[0] costs one
+// comparison and keeps state 0, so 16-byte groups without p[0] are skipped
+// (SWAR test on the registers of one LDS.128) and inside a group the walk
+// jumps to the next p[0]; only bytes after a p[0] walk the DFA.
+//
+// Work split as in pfac8.cuh: one 512-thread CTA per SM, each warp streams a
+// CONTIGUOUS segment of 4,608-byte warp tiles through a private
+// double-buffered TMA pipeline -- no CTA barriers.  A warp's matches come out
+// in text order tile by tile (a tile's few keys are warp-sorted in shared
+// memory), so the output is the concatenation of the per-warp staging
+// regions (u64_prefix_kernel + p8_gather_kernel).  A tile with more matches
+// than the buffer flags the exact global-key fallback (CUB radix sort).
 #pragma once
 #include <type_traits>
 
 #include "glop_kernels.cuh"
+#include "pfac8.cuh"
 
 namespace glop {
 
-constexpr int kK2Threads = 512;
-constexpr uint32_t kK2Chunk = 144;                   // end positions per thread
-constexpr uint32_t kK2Tile = kK2Chunk * kK2Threads;  // 73,728
-constexpr uint32_t kK2Pre = 64;                      // warm-up bytes kept before the tile
-constexpr uint32_t kK2Stage = kK2Pre + kK2Tile + 16;
-constexpr uint32_t kK2HitCap = 1024;                 // match keys per tile in smem
-constexpr uint32_t kK2SmemDfaMax = 48;               // patterns up to 48 bytes keep the DFA in smem
+constexpr int kK3Warps = 16;
+constexpr int kK3Threads = kK3Warps * 32;
+constexpr uint32_t kK3Chunk = 144;                 // end positions per lane
+constexpr uint32_t kK3Tile = kK3Chunk * 32;        // 4,608 per warp tile
+constexpr uint32_t kK3Pre = 64;                    // warm-up bytes kept before the tile
+constexpr uint32_t kK3Stage = kK3Pre + kK3Tile + 16;
+constexpr uint32_t kK3Hits = 64;                   // match keys per warp tile in smem
+constexpr uint32_t kK3SmemDfaMax = 48;             // patterns up to 48 bytes keep the DFA in smem
 
-struct K2Smem {
-  static constexpr uint32_t kBars = 2 * kK2Stage;
-  static constexpr uint32_t kMisc = kBars + 16;
-  static constexpr uint32_t kKeys = kMisc + 16;
-  static constexpr uint32_t kDfa = kKeys + kK2HitCap * 8;
+struct K3Layout {
+  uint32_t bufs, bars, keys, nh, dfa, total;
 };
 
-struct K2Params {
+__host__ __device__ inline K3Layout make_k3_layout(uint32_t m, bool smem_dfa) {
+  K3Layout L;
+  uint32_t o = 0;
+  L.bufs = o; o += kK3Warps * 2 * kK3Stage;
+  L.bars = o; o += kK3Warps * 2 * 8;
+  L.keys = o; o += kK3Warps * kK3Hits * 8;
+  L.nh = o; o += kK3Warps * 4;
+  L.dfa = align16(o); o = L.dfa + (smem_dfa ? m * 1024 : 0);
+  L.total = o;
+  return L;
+}
+
+struct K3Params {
   const uint8_t* text;
   unsigned long long n, end_lim, base;  // ends (last byte of a match) < end_lim
-  uint32_t m, num_tiles, p0;
+  uint32_t m, p0, num_tiles, per, sub;
   const uint32_t* dfa;                  // m x 256
-  unsigned long long* staging;
-  unsigned long long staging_cap;
-  unsigned long long* g_count;
-  TileDir* dir;
-  unsigned int* g_flags;
+  unsigned long long* staging;          // per-warp regions of start offsets
+  unsigned long long region;
+  unsigned long long* counts;           // matches per region
+  unsigned long long* g_count;          // [0] total, [1] flags, [2] comparisons, [3] max region use
   unsigned long long* comparisons;
-  int mode;                             // 0: per-tile order; 1: global keys (fallback)
+  int mode;                             // 0: per-warp ordered staging; 1: global keys (fallback)
   unsigned long long* keys;
   unsigned long long keys_cap;
 };
@@ -58,6 +72,11 @@ struct K2Params {
 __device__ __forceinline__ void k2_issue(uint8_t* dst, uint64_t* bar, const uint8_t* A, uint32_t a,
                                          unsigned long long n, long long lo, uint32_t bytes) {
   const long long hi = lo + bytes;
+  if (lo >= (long long)a && hi <= (long long)(a + n)) {  // interior: one copy
+    mbar_arrive_tx(bar, bytes);
+    bulk_g2s(dst, A + lo, bytes, bar);
+    return;
+  }
   const long long vlo = lo > (long long)a ? lo : (long long)a;
   const long long vhi = hi < (long long)(a + n) ? hi : (long long)(a + n);
   long long tlo = (vlo + 15) & ~15ll, thi = vhi & ~15ll;
@@ -83,64 +102,58 @@ __device__ __forceinline__ uint32_t k2_zero_bytes(uint32_t w, uint32_t x4) {
 __device__ __forceinline__ uint32_t k2_gather4(uint32_t z) { return (((z >> 7) * 0x00204081u) >> 21) & 15u; }
 
 template <bool kSmemDfa>
-__global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
+__global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, const K3Layout L) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t tid = threadIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K2Smem::kBars);
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + K2Smem::kMisc);
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem + K2Smem::kKeys);
-  uint32_t* s_dfa = reinterpret_cast<uint32_t*>(smem + K2Smem::kDfa);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars) + warp * 2;
+  uint8_t* bufs = smem + L.bufs + (size_t)warp * 2 * kK3Stage;
+  unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.keys) + warp * kK3Hits;
+  uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.nh) + warp;
+  uint32_t* s_dfa = reinterpret_cast<uint32_t*>(smem + L.dfa);
   if (kSmemDfa)
-    for (uint32_t i = tid; i < p.m * 64; i += kK2Threads)
+    for (uint32_t i = tid; i < p.m * 64; i += kK3Threads)
       reinterpret_cast<uint4*>(s_dfa)[i] = reinterpret_cast<const uint4*>(p.dfa)[i];
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    s_misc[0] = 0;
-    s_misc[1] = 0;
-    fence_mbar_init();
-  }
+  if (lane < 2) mbar_init(&bars[lane], 1);
+  if (lane == 0) *s_nh = 0;
+  if (tid == 0) fence_mbar_init();
   __syncthreads();
   const uint32_t* D = kSmemDfa ? s_dfa : p.dfa;
   const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
-  const uint8_t* A = p.text - a;  // 16-aligned; text position x is A[x + a]
+  const uint8_t* A = p.text - a;                   // 16-aligned; text position x is A[x + a]
   const unsigned long long e_end = p.end_lim + a;  // end positions, A coordinates
-  if (tid == 0)
-    for (uint32_t s = 0; s < 2; ++s) {
-      const uint32_t t = blockIdx.x + s * gridDim.x;
-      if (t < p.num_tiles)
-        k2_issue(smem + s * kK2Stage, &bars[s], A, a, p.n, (long long)t * kK2Tile - kK2Pre, kK2Stage);
-    }
+  const uint32_t cta_lo = min(blockIdx.x * p.per, p.num_tiles), cta_hi = min(cta_lo + p.per, p.num_tiles);
+  const uint32_t t0 = min(cta_lo + warp * p.sub, cta_hi), t1 = min(t0 + p.sub, cta_hi);
+  if (lane == 0)
+    for (uint32_t b = 0; b < 2; ++b)
+      if (t0 + b < t1)
+        k2_issue(bufs + b * kK3Stage, &bars[b], A, a, p.n, (long long)(t0 + b) * kK3Tile - kK3Pre, kK3Stage);
   const uint32_t x4 = p.p0 * 0x01010101u, m = p.m;
+  const uint32_t gw = blockIdx.x * kK3Warps + warp;
+  unsigned long long* region = p.staging + (unsigned long long)gw * p.region;
   unsigned long long cmp_total = 0;
-  for (uint32_t k = 0;; ++k) {
-    const uint32_t t = blockIdx.x + k * gridDim.x;
-    if (t >= p.num_tiles) break;
-    const uint32_t stage = k & 1;
-    mbar_wait(&bars[stage], (k >> 1) & 1);
-    const uint8_t* win = smem + stage * kK2Stage;
-    const unsigned long long tT = (unsigned long long)t * kK2Tile;
-    // window byte y holds A[tT - kK2Pre + y]
+  uint32_t cursor = 0;  // matches written to this warp's region
+
+  for (uint32_t t = t0, k = 0; t < t1; ++t, ++k) {
+    const uint32_t b = k & 1;
+    mbar_wait(&bars[b], (k >> 1) & 1);
+    const uint8_t* win = bufs + b * kK3Stage;  // window byte y holds A[tT - kK3Pre + y]
+    const unsigned long long tT = (unsigned long long)t * kK3Tile;
     auto abyte = [&](unsigned long long x) -> uint32_t {  // A coordinate, a <= x < a + n
-      const long long y = (long long)(x - tT) + kK2Pre;
-      return (y >= 0 && y < (long long)kK2Stage) ? win[y] : __ldg(A + x);
+      const long long y = (long long)(x - tT) + kK3Pre;
+      return (y >= 0 && y < (long long)kK3Stage) ? win[y] : __ldg(A + x);
     };
     auto record = [&](unsigned long long x) {  // match ending at A coordinate x
+      const unsigned long long start = p.base + x - a + 1 - m;
       if (p.mode == 0) {
-        const uint32_t slot = atomicAdd(&s_misc[k & 1], 1u);
-        if (slot < kK2HitCap) s_keys[slot] = x - tT;
+        const uint32_t slot = atomicAdd(s_nh, 1u);
+        if (slot < kK3Hits) hk[slot] = start;
       } else {
         const unsigned long long slot = atomicAdd(p.g_count, 1ull);
-        if (slot < p.keys_cap) p.keys[slot] = p.base + x - a + 1 - m;
+        if (slot < p.keys_cap) p.keys[slot] = start;
       }
     };
-    unsigned long long c0 = tT + (unsigned long long)tid * kK2Chunk;
-    if (c0 < a) c0 = a;
-    const unsigned long long c1 = min(tT + (unsigned long long)(tid + 1) * kK2Chunk, e_end);
-    // Walks window bytes [yf, yt) from state j (window byte y is A coordinate
-    // tT - kK2Pre + y); in state 0 only p[0] bytes (found 16 at a time) step
-    // the DFA.  kCount: add the reference's comparisons and record matches
-    // (the warm-up does neither).
+    // Walks window bytes [yf, yt) from state j; kCount: add the reference's
+    // comparisons and record matches (the warm-up does neither).
     auto walk = [&](auto kCount, uint32_t yf, uint32_t yt, uint32_t& j, unsigned long long& cmp) {
       for (uint32_t g = yf & ~15u; g < yt; g += 16) {
         const uint32_t kb = yf > g ? yf - g : 0u;
@@ -169,78 +182,67 @@ __global__ void __launch_bounds__(kK2Threads, 1) kmp2_kernel(const K2Params p) {
           const uint32_t e = D[j * 256 + win[g + kk]];
           if (decltype(kCount)::value) {
             cmp += e >> 14;
-            if (e & 0x2000u) record(tT - kK2Pre + g + kk);
+            if (e & 0x2000u) record(tT - kK3Pre + g + kk);
           }
           j = e & 0x1FFFu;
           ++kk;
         }
       }
     };
-    if (tid == 0 && p.mode == 0) s_misc[(k + 1) & 1] = 0;  // the next tile's match counter
+    unsigned long long c0 = tT + (unsigned long long)lane * kK3Chunk;
+    if (c0 < a) c0 = a;
+    const unsigned long long c1 = min(tT + (unsigned long long)(lane + 1) * kK3Chunk, e_end);
     if (c0 < c1) {
-      const uint32_t y0 = (uint32_t)(c0 - tT) + kK2Pre, y1 = (uint32_t)(c1 - tT) + kK2Pre;
+      const uint32_t y0 = (uint32_t)(c0 - tT) + kK3Pre, y1 = (uint32_t)(c1 - tT) + kK3Pre;
       // warm-up: the state at c0 from the m-1 bytes before it (clamped to the text start)
       uint32_t j = 0;
       unsigned long long cmp = 0;
       const unsigned long long wlo = c0 - min(c0 - a, (unsigned long long)(m - 1));
-      if (wlo + kK2Pre >= tT) {
-        walk(std::false_type{}, (uint32_t)(wlo + kK2Pre - tT), y0, j, cmp);
+      if (wlo + kK3Pre >= tT) {
+        walk(std::false_type{}, (uint32_t)(wlo + kK3Pre - tT), y0, j, cmp);
       } else {  // long patterns: warm-up bytes before the window
         for (unsigned long long x = wlo; x < c0; ++x) {
-          const uint32_t b = abyte(x);
-          if (j != 0 || b == p.p0) j = D[j * 256 + b] & 0x1FFFu;
+          const uint32_t bt = abyte(x);
+          if (j != 0 || bt == p.p0) j = D[j * 256 + bt] & 0x1FFFu;
         }
       }
       walk(std::true_type{}, y0, y1, j, cmp);
       cmp_total += cmp;
     }
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t tn = t + 2 * gridDim.x;
-      if (tn < p.num_tiles) {
-        fence_proxy_async();
-        k2_issue(smem + stage * kK2Stage, &bars[stage], A, a, p.n, (long long)tn * kK2Tile - kK2Pre, kK2Stage);
+    __syncwarp();
+    // buffer b is free: refill it with the segment's tile t + 2
+    if (lane == 0 && t + 2 < t1) {
+      fence_proxy_async();
+      k2_issue(bufs + b * kK3Stage, &bars[b], A, a, p.n, (long long)(t + 2) * kK3Tile - kK3Pre, kK3Stage);
+    }
+    if (p.mode == 0) {
+      const uint32_t nb = *s_nh;
+      if (nb) {  // this tile's matches, in order, appended to the region
+        if (nb > kK3Hits) {
+          if (lane == 0) atomicOr(reinterpret_cast<unsigned int*>(p.g_count + 1), 1u);
+        } else {
+          warp_sort_keys(hk, nb, lane);
+          if (cursor + nb <= p.region)
+            for (uint32_t h = lane; h < nb; h += 32) region[cursor + h] = hk[h];
+        }
+        cursor += nb;
+        __syncwarp();
+        if (lane == 0) *s_nh = 0;
+        __syncwarp();
       }
     }
-    if (p.mode != 0) continue;
-    const uint32_t nh = s_misc[k & 1];
-    if (nh == 0) {  // common case: no match in the tile, no further barrier
-      if (tid == 0) p.dir[t] = TileDir{0ull, 0u, 0u};
-      continue;
-    }
-    const bool over = nh > kK2HitCap;
-    if (!over && nh > 1) {
-      uint32_t P = 1;
-      while (P < nh) P <<= 1;
-      for (uint32_t y = nh + tid; y < P; y += kK2Threads) s_keys[y] = ~0ull;
-      __syncthreads();
-      for (uint32_t kk = 2; kk <= P; kk <<= 1)
-        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (uint32_t x = tid; x < P; x += kK2Threads) {
-            const uint32_t y = x ^ jj;
-            if (y > x) {
-              const unsigned long long u = s_keys[x], w = s_keys[y];
-              if ((u > w) == ((x & kk) == 0)) s_keys[x] = w, s_keys[y] = u;
-            }
-          }
-          __syncthreads();
-        }
-    }
-    if (tid == 0) {
-      const unsigned long long slot = atomicAdd(p.g_count, (unsigned long long)nh);
-      p.dir[t] = TileDir{slot, nh, over ? 1u : 0u};
-      if (over) atomicOr(p.g_flags, 1u);
-      s_misc[2] = (uint32_t)slot;
-      s_misc[3] = (uint32_t)(slot >> 32);
-    }
-    __syncthreads();
-    const unsigned long long slot = (unsigned long long)s_misc[2] | ((unsigned long long)s_misc[3] << 32);
-    if (!over && slot + nh <= p.staging_cap)
-      for (uint32_t h = tid; h < nh; h += kK2Threads) p.staging[slot + h] = p.base + tT + s_keys[h] - a + 1 - m;
-    __syncthreads();
   }
   for (int o = 16; o; o >>= 1) cmp_total += __shfl_xor_sync(0xffffffffu, cmp_total, o);
-  if ((tid & 31) == 0 && cmp_total) atomicAdd(p.comparisons, cmp_total);
+  if (lane == 0) {
+    if (cmp_total) atomicAdd(p.comparisons, cmp_total);
+    if (p.mode == 0) {
+      p.counts[gw] = cursor;
+      if (cursor) {
+        atomicAdd(p.g_count, (unsigned long long)cursor);
+        atomicMax(p.g_count + 3, (unsigned long long)cursor);
+      }
+    }
+  }
 }
 
 }  // namespace glop

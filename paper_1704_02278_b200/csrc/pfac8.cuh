@@ -410,14 +410,18 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 
 // Concatenates the per-warp regions (each already in text order) in warp
 // order: region g's hits go to out[prefix[g], prefix[g] + counts[g]).
+// Launched before the host has looked at the scan's flags (saves a round
+// trip): records past `cap` or beyond a region are not copied, and a flagged
+// scan is redone anyway.
+template <typename Rec>
 __global__ void __launch_bounds__(256) p8_gather_kernel(const unsigned long long* counts,
                                                         const unsigned long long* prefix,
-                                                        unsigned long long region, const DevHit* staging,
-                                                        DevHit* out) {
+                                                        unsigned long long region, const Rec* staging,
+                                                        Rec* out, unsigned long long cap) {
   const uint32_t g = blockIdx.x;
-  const unsigned long long c = counts[g], dst = prefix[g];
-  const DevHit* src = staging + (unsigned long long)g * region;
-  for (unsigned long long h = threadIdx.x; h < c; h += blockDim.x) out[dst + h] = src[h];
+  const unsigned long long c = min(counts[g], region), dst = prefix[g];
+  const Rec* src = staging + (unsigned long long)g * region;
+  for (unsigned long long h = threadIdx.x; h < c && dst + h < cap; h += blockDim.x) out[dst + h] = src[h];
 }
 
 // Exclusive prefix of u64 counts (single CTA, any n).

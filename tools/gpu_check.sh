@@ -15,6 +15,6 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2>&1; t
 if [ "${PROFILE:-1}" = 1 ]; then
   timeout 900 tools/profile_pfac.sh k1000
   timeout 600 tools/profile_pfac.sh k10 --patterns 10
-  KREGEX=kmp2 timeout 600 tools/profile_pfac.sh kmp --config kmp
+  KREGEX=kmp3 timeout 600 tools/profile_pfac.sh kmp --config kmp
   timeout 600 tools/profile_pfac.sh dpi --config dpi
 fi
