@@ -208,6 +208,10 @@ glop_status glop_line_numbers_device(glop_ctx* ctx, const uint8_t* d_text, uint6
 glop_status glop_kmp_search(glop_ctx* ctx, const uint8_t* p, uint32_t m, const uint32_t* failure,
                             const uint8_t* text, uint64_t n, int text_on_device, uint64_t** offsets,
                             uint64_t* n_offsets, uint64_t* comparisons);
+/* Shard form: d_text holds global offsets [base, base+n); reports the
+ * starts in [0, own) (matches may end in the halo [own, own+m-1)), adds
+ * `base` to each, and counts the comparisons the sequential scan makes at
+ * positions [0, own) -- so shards with an (m-1)-byte halo sum to the whole. */
 glop_status glop_kmp_search_device(glop_ctx* ctx, const uint8_t* p, uint32_t m,
                                    const uint32_t* failure, const uint8_t* d_text, uint64_t n,
                                    uint64_t own, uint64_t base, uint64_t* d_out, uint64_t cap,

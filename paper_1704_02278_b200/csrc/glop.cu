@@ -470,6 +470,7 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
     K3Params p{};
     p.text = d_text;
     p.n = n;
+    p.own = own;
     p.end_lim = end_lim;
     p.base = base;
     p.m = m;

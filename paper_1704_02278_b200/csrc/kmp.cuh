@@ -54,7 +54,7 @@ __host__ __device__ inline K3Layout make_k3_layout(uint32_t m, bool smem_dfa) {
 
 struct K3Params {
   const uint8_t* text;
-  unsigned long long n, end_lim, base;  // ends (last byte of a match) < end_lim
+  unsigned long long n, own, end_lim, base;  // starts < own; ends (last byte of a match) < end_lim
   uint32_t m, p0, num_tiles, per, sub;
   const uint32_t* dfa;                  // m x 256
   unsigned long long* staging;          // per-warp regions of start offsets
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
   const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
   const uint8_t* A = p.text - a;                   // 16-aligned; text position x is A[x + a]
   const unsigned long long e_end = p.end_lim + a;  // end positions, A coordinates
+  const unsigned long long o_end = p.own + a;      // comparisons counted for positions < own
   const uint32_t cta_lo = min(blockIdx.x * p.per, p.num_tiles), cta_hi = min(cta_lo + p.per, p.num_tiles);
   const uint32_t t0 = min(cta_lo + warp * p.sub, cta_hi), t1 = min(t0 + p.sub, cta_hi);
   if (lane == 0)
@@ -153,8 +154,9 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
       }
     };
     // Walks window bytes [yf, yt) from state j; kCount: add the reference's
-    // comparisons and record matches (the warm-up does neither).
-    auto walk = [&](auto kCount, uint32_t yf, uint32_t yt, uint32_t& j, unsigned long long& cmp) {
+    // comparisons, kRecord: record matches (the warm-up does neither, a
+    // shard's halo only records -- its comparisons belong to the next shard).
+    auto walk = [&](auto kCount, auto kRecord, uint32_t yf, uint32_t yt, uint32_t& j, unsigned long long& cmp) {
       for (uint32_t g = yf & ~15u; g < yt; g += 16) {
         const uint32_t kb = yf > g ? yf - g : 0u;
         const uint32_t ke = min(yt - g, 16u);
@@ -180,10 +182,8 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
             kk = s;
           }
           const uint32_t e = D[j * 256 + win[g + kk]];
-          if (decltype(kCount)::value) {
-            cmp += e >> 14;
-            if (e & 0x2000u) record(tT - kK3Pre + g + kk);
-          }
+          if (decltype(kCount)::value) cmp += e >> 14;
+          if (decltype(kRecord)::value && (e & 0x2000u)) record(tT - kK3Pre + g + kk);
           j = e & 0x1FFFu;
           ++kk;
         }
@@ -199,14 +199,20 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
       unsigned long long cmp = 0;
       const unsigned long long wlo = c0 - min(c0 - a, (unsigned long long)(m - 1));
       if (wlo + kK3Pre >= tT) {
-        walk(std::false_type{}, (uint32_t)(wlo + kK3Pre - tT), y0, j, cmp);
+        walk(std::false_type{}, std::false_type{}, (uint32_t)(wlo + kK3Pre - tT), y0, j, cmp);
       } else {  // long patterns: warm-up bytes before the window
         for (unsigned long long x = wlo; x < c0; ++x) {
           const uint32_t bt = abyte(x);
           if (j != 0 || bt == p.p0) j = D[j * 256 + bt] & 0x1FFFu;
         }
       }
-      walk(std::true_type{}, y0, y1, j, cmp);
+      if (c1 <= o_end) {
+        walk(std::true_type{}, std::true_type{}, y0, y1, j, cmp);
+      } else {  // the chunk reaches into the shard's halo
+        const uint32_t yo = c0 < o_end ? (uint32_t)(o_end - tT) + kK3Pre : y0;
+        walk(std::true_type{}, std::true_type{}, y0, yo, j, cmp);
+        walk(std::false_type{}, std::true_type{}, yo, y1, j, cmp);
+      }
       cmp_total += cmp;
     }
     __syncwarp();

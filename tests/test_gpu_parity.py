@@ -407,3 +407,26 @@ def test_device_line_index(ctx, torch_cuda):
     ctx.synchronize()
     ref = [O.line_of(t, int(o) - base) for o in alerts["offset"]]
     assert dl.cpu().numpy().tolist() == ref
+
+
+def test_kmp_shards_equal_whole(ctx, torch_cuda):
+    """KMP shard form: starts [0, own) with an (m-1)-byte halo; offsets and
+    comparison counts of the shards sum to the whole-text reference."""
+    text = glop.gen_syslog_host(3_000_000, seed=41)
+    for p in (b"Failed password", b"ab", b"session opened for user root by (uid=0)"):
+        r_offs, r_cmp = O.kmp_search(text, p)
+        m = len(p)
+        for shards in (2, 5):
+            S = -(-text.size // shards)
+            offs, cmp_total = [], 0
+            for g in range(shards):
+                lo, hi = g * S, min((g + 1) * S, text.size)
+                rd = min(hi + m - 1, text.size)
+                d = torch_cuda.from_numpy(text[lo:rd].copy()).cuda()
+                out = torch_cuda.empty(1 << 16, dtype=torch_cuda.int64, device="cuda")
+                n, c = ctx.kmp_search_device(p, d.data_ptr(), rd - lo, out.data_ptr(), 1 << 16, own=hi - lo, base=lo)
+                ctx.synchronize()
+                offs.append(out[:n].cpu().numpy())
+                cmp_total += c
+            assert np.array_equal(np.concatenate(offs), r_offs), (p, shards)
+            assert cmp_total == r_cmp, (p, shards)
