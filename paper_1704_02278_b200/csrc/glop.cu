@@ -562,10 +562,17 @@ glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* 
   const unsigned fl = (unsigned)(c->h_misc[1] & 0xffffffffu);
   if (fl & 1u) return fail(GLOP_ELOGIC, "verify_hits: hit extends past end of text");
   ++c->launches;
+  const bool hist = d_counts && r->view.n_patterns <= kHistBins;
   verify_scatter_kernel<<<nb, kVerifyBlock, 0, c->stream>>>(
       r->view, reinterpret_cast<const DevHit*>(d_hits), n_hits, c->keep.as<uint8_t>(),
       c->bprefix.as<unsigned long long>(), reinterpret_cast<DevAlert*>(d_out),
-      reinterpret_cast<unsigned long long*>(d_counts));
+      hist ? nullptr : reinterpret_cast<unsigned long long*>(d_counts));
+  if (hist && kept) {
+    ++c->launches;
+    alert_histogram_kernel<<<(uint32_t)std::min<uint64_t>((kept + 1023) / 1024, c->num_sms), 1024, 0, c->stream>>>(
+        reinterpret_cast<const DevAlert*>(d_out), kept, r->view.n_patterns,
+        reinterpret_cast<unsigned long long*>(d_counts));
+  }
   CU(cudaGetLastError());
   *n_alerts = kept;
   if ((fl & 2u) && kept > 1) {

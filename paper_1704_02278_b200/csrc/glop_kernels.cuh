@@ -815,6 +815,24 @@ __global__ void __launch_bounds__(kVerifyBlock) verify_scatter_kernel(
   }
 }
 
+// Per-pattern alert histogram (the count half of verify_hits' report):
+// grid-stride over the alerts into a shared-memory histogram per block,
+// then one global atomic per non-empty bin -- instead of one global atomic
+// per alert, which serialises on popular patterns.  k <= kHistBins.
+constexpr uint32_t kHistBins = 8192;
+__global__ void __launch_bounds__(1024) alert_histogram_kernel(const DevAlert* alerts, unsigned long long n,
+                                                               uint32_t k, unsigned long long* counts) {
+  __shared__ uint32_t h[kHistBins];
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    atomicAdd(&h[alerts[i].rule_id], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x)
+    if (h[i]) atomicAdd(counts + i, (unsigned long long)h[i]);
+}
+
 // Unsorted-input path of verify: alerts <-> (offset << 24 | rule) keys.
 __global__ void alerts_to_keys_kernel(const DevAlert* a, unsigned long long n, unsigned long long* keys) {
   for (unsigned long long h = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; h < n;
