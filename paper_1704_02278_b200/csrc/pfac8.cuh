@@ -31,11 +31,12 @@ namespace glop {
 constexpr int kP8Warps = 24;
 constexpr int kP8Threads = kP8Warps * 32;
 constexpr uint32_t kP8Tile = 2048;                 // owned starts per tile (TMA unit)
-constexpr uint32_t kP8Stage = kP8Tile + 16;        // + words 512..515 (halo)
+constexpr uint32_t kP8Stage = kP8Tile + 16;        // + the 4 words after the tile (halo)
 constexpr uint32_t kP8Chunk = 1024;                // bytes sampled per iteration (8 words / lane)
 constexpr uint32_t kP8Queue = 32 + kP8Chunk / 4;    // candidate words: < 32 carried + one chunk
 constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
-constexpr uint32_t kP8DmaskBytes = 1u << 16;        // level-1 d-mask table (shared memory)
+constexpr uint32_t kP8DmaskLog2 = 16;
+constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
 
 struct P8Layout {
   uint32_t bufs, bars, queue, hits, nh, dmask, bm2, cls, total;
@@ -85,7 +86,7 @@ struct P8Params {
 constexpr uint32_t kP8NibbleGrams = 12000;
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
-  return (g * 0x9E3779B1u) >> (kNibble ? 15 : 16);
+  return (g * 0x9E3779B1u) >> (32 - kP8DmaskLog2 - (kNibble ? 1 : 0));
 }
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_dmask_byte(uint32_t h) { return kNibble ? h >> 1 : h; }
