@@ -2,7 +2,7 @@
 
 TEST INFRASTRUCTURE ONLY.  Needs /root/reference (this build container):
   make -C oracle && python oracle/gen_golden.py
-The generator (oracle/gen_golden.cpp) replays the reference's own seeded
+The generators (oracle/gen_golden.cpp, oracle/gen_jsonl.cpp) replay the reference's own seeded
 test generators through the reference's pfac_scan / verify_hits / kmp_search
 and records the results; this script only gzips them into tests/golden/.
 """
@@ -23,6 +23,9 @@ def main() -> int:
     os.makedirs(GOLDEN, exist_ok=True)
     with tempfile.TemporaryDirectory() as tmp:
         subprocess.check_call([exe, tmp])
+        jexe = os.path.join(HERE, "_ref", "gen_jsonl")
+        if os.path.exists(jexe):  # the reference CLI's JSONL (tests/test_cli.py)
+            subprocess.check_call([jexe, tmp])
         for name in sorted(os.listdir(tmp)):
             raw = open(os.path.join(tmp, name), "rb").read()
             dst = os.path.join(GOLDEN, name + ".gz")
