@@ -363,7 +363,18 @@ def main():
 def run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, torch, dist):
     """Same metric through the public pipeline call with the shard in pinned
     host memory: H2D copy + scan + verify + D2H alerts/counts every step."""
-    host = ctx.host_alloc(sh.read)
+    try:  # pinned host copy of the shard; every rank must have one before going on
+        host, why = ctx.host_alloc(sh.read), ""
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+        host, why = None, f"pinned host allocation of {sh.read} bytes failed: {e}"
+    if world > 1:
+        ok = torch.tensor([0.0 if host is None else 1.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0 and host is not None:
+            ctx.host_free(host)
+            host, why = None, why or "another rank could not pin its shard"
+    if host is None:
+        return {"unavailable": why}
     try:
         ctx.memcpy(host, d_text.data_ptr(), sh.read, 2)
         ctx.synchronize()
