@@ -32,8 +32,7 @@ constexpr int kP8Warps = 24;
 constexpr int kP8Threads = kP8Warps * 32;
 constexpr uint32_t kP8Tile = 2048;                 // owned starts per tile (TMA unit)
 constexpr uint32_t kP8Stage = kP8Tile + 16;        // + the 4 words after the tile (halo)
-constexpr uint32_t kP8Chunk = 1024;                // bytes sampled per iteration (8 words / lane)
-constexpr uint32_t kP8Queue = 32 + kP8Chunk / 4;    // candidate words: < 32 carried + one chunk
+constexpr uint32_t kP8Queue = kP8Tile / 4;         // candidate words of one tile, worst case (u16)
 constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 constexpr uint32_t kP8DmaskLog2 = 16;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
@@ -47,7 +46,7 @@ __host__ __device__ inline P8Layout make_p8_layout() {
   uint32_t o = 0;
   L.bufs = o; o += kP8Warps * 2 * kP8Stage;
   L.bars = o; o += kP8Warps * 2 * 8;
-  L.queue = o; o += kP8Warps * kP8Queue * 4;
+  L.queue = o; o += kP8Warps * kP8Queue * 2;
   L.hits = o; o += kP8Warps * kP8Hits * 8;
   L.nh = o; o += kP8Warps * 4;
   L.dmask = align16(o); o = L.dmask + kP8DmaskBytes;
@@ -172,7 +171,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   const uint8_t* s_cls = smem + L.cls;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars) + warp * 2;
   uint8_t* bufs = smem + L.bufs + (size_t)warp * 2 * kP8Stage;
-  uint32_t* q = reinterpret_cast<uint32_t*>(smem + L.queue) + warp * kP8Queue;
+  uint16_t* q = reinterpret_cast<uint16_t*>(smem + L.queue) + warp * kP8Queue;
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.hits) + warp * kP8Hits;
   uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.nh) + warp;
 
@@ -272,31 +271,23 @@ __global__ void __launch_bounds__(kP8Threads, 1)
       }
     };
 
-    // Chunks of 1 KB: lane l samples tile words W + 8 l + 1 .. + 8 (the
-    // chunks cover candidates 0..kP8Tile-1 of the tile).  Candidate words
-    // enter the queue q in text order; full 32-entry rounds are drained after
-    // each chunk (the < 32 left over move to the front), and the pass
-    // W == kP8Tile / 4 drains the rest.
-    uint32_t qh = 0, qt = 0;
-#pragma unroll 1
-    for (uint32_t W = 0; W <= kP8Tile / 4; W += kP8Chunk / 4) {
-      const bool tail = W == kP8Tile / 4;
-      if (qh) {  // carry the < 32 undrained entries to the front
-        const uint32_t pend = qt - qh;
-        const uint32_t v = lane < pend ? q[qh + lane] : 0u;
-        __syncwarp();
-        if (lane < pend) q[lane] = v;
-        qh = 0;
-        qt = pend;
-        __syncwarp();
-      }
-      if (!tail) {
+    // Level 1 over the whole tile in one pass: lane l samples tile words
+    // 8 l + 1 .. 8 l + 8 (first half) and 256 + 8 l + 1 .. 256 + 8 l + 8 (second
+    // half), which covers candidates 0..kP8Tile-1.  Candidate words enter the
+    // queue q (u16: word << 4 | d-mask) in text order -- one packed shuffle
+    // scan gives both halves' prefixes -- and are checked 32 per round.
+    uint32_t qt = 0;
+    {
+      uint32_t lo4[2], hi4[2], mm8[2][8];
+#pragma unroll
+      for (uint32_t hf = 0; hf < 2; ++hf) {
+        const uint32_t W = hf * (kP8Tile / 8);
         const uint4 va = reinterpret_cast<const uint4*>(sw + W)[2 * lane];
         const uint4 vb = reinterpret_cast<const uint4*>(sw + W)[2 * lane + 1];
-        const uint32_t wn = sw[W + kP8Chunk / 4];
+        const uint32_t wn = sw[W + kP8Tile / 8];
         uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
         if (lane == 31) w8 = wn;
-        uint32_t m[8];
+        uint32_t* m = mm8[hf];
         m[0] = p8_dmask<kNibble>(s_dmask, p8_gram(va.x, va.y));
         m[1] = p8_dmask<kNibble>(s_dmask, p8_gram(va.y, va.z));
         m[2] = p8_dmask<kNibble>(s_dmask, p8_gram(va.z, va.w));
@@ -305,34 +296,39 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         m[5] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.y, vb.z));
         m[6] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.z, vb.w));
         m[7] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.w, w8));
-        const uint32_t lo4 = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
-        const uint32_t hi4 = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
-        if (__ballot_sync(0xffffffffu, (lo4 | hi4) != 0)) {
-          // candidate words of this lane (d-masks are < 16: adding 0x7F to a
-          // byte sets its top bit iff the byte is non-zero), bit-plane prefix
-          const uint32_t cnt =
-              __popc((lo4 + 0x7F7F7F7Fu) & 0x80808080u) + __popc((hi4 + 0x7F7F7F7Fu) & 0x80808080u);
-          uint32_t tot = 0, at = qt;
-#pragma unroll
-          for (uint32_t bit = 0; bit < 4; ++bit) {
-            const uint32_t bb = __ballot_sync(0xffffffffu, (cnt >> bit) & 1u);
-            tot += __popc(bb) << bit;
-            at += __popc(bb & ltmask) << bit;
-          }
-          const uint32_t wbase = (W + 8 * lane + 1) << 4;
-#pragma unroll
-          for (uint32_t j = 0; j < 8; ++j)
-            if (m[j]) q[at++] = wbase + 16 * j + m[j];
-          qt += tot;
-          __syncwarp();
-        }
+        lo4[hf] = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
+        hi4[hf] = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
       }
+      if (__ballot_sync(0xffffffffu, (lo4[0] | hi4[0] | lo4[1] | hi4[1]) != 0)) {
+        // candidate words per half (d-masks are < 16: adding 0x7F to a byte
+        // sets its top bit iff the byte is non-zero), packed cntA | cntB << 16
+        auto nz = [](uint32_t x) { return __popc((x + 0x7F7F7F7Fu) & 0x80808080u); };
+        const uint32_t cnt = (nz(lo4[0]) + nz(hi4[0])) | ((nz(lo4[1]) + nz(hi4[1])) << 16);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += x;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t totA = tot & 0xFFFFu;
+        uint32_t atA = (incl - cnt) & 0xFFFFu, atB = totA + ((incl - cnt) >> 16);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+          if (mm8[0][j]) q[atA++] = (uint16_t)(((8 * lane + 1 + j) << 4) | mm8[0][j]);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+          if (mm8[1][j]) q[atB++] = (uint16_t)(((kP8Tile / 8 + 8 * lane + 1 + j) << 4) | mm8[1][j]);
+        qt = totA + (tot >> 16);
+        __syncwarp();
+      }
+    }
+    {
 #pragma unroll 1
-      while (qt - qh >= 32 || (tail && qt != qh)) {
+      for (uint32_t qh = 0; qh < qt; qh += 32) {
         const uint32_t pend = qt - qh;
         // ---- 8-byte keys of up to 32 candidate words -> prefix bitmap
         const uint32_t e = lane < pend ? q[qh + lane] : 16u;  // idle lanes: word 1, no bits
-        qh += min(pend, 32u);
         const uint32_t i = e >> 4;
         uint32_t mm = e & 15u;
         const uint32_t w0 = sw[i - 1], w1 = sw[i], w2 = sw[i + 1];
