@@ -115,6 +115,21 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def settle(self, work, timeout=3.0):
+        """Run untimed `work` until nvidia-smi is producing samples (it takes a
+        moment to start), so the timed region that follows is sampled."""
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
+            work()
+
+    def hold(self, work, min_samples=5, timeout=3.0):
+        """After a short timed region: keep the same load running (untimed)
+        until a few samples under it exist."""
+        t0 = time.perf_counter()
+        n0 = len(self.rows)
+        while self.proc and len(self.rows) - n0 < min_samples and time.perf_counter() - t0 < timeout:
+            work()
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -304,6 +319,9 @@ def main():
     ctx.synchronize()
     sampler = ClockSampler(local)
     with sampler:
+        # (ranks must not run different numbers of collective steps: at N > 1
+        # the settle wait is idle)
+        sampler.settle((lambda: (step(), ctx.synchronize())) if world == 1 else (lambda: time.sleep(0.02)))
         barrier()
         l0 = ctx.launches
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -316,6 +334,8 @@ def main():
         ctx.synchronize()
         barrier()
         launches = ctx.launches - l0
+        if world == 1:
+            sampler.hold(lambda: (step(), ctx.synchronize()))
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
         kernel_ms = max_over_ranks(statistics.mean(kms))
         total_alerts = int(d_counts.sum().item())
@@ -413,19 +433,23 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
     for _ in range(max(args.warmup, 3)):
         nm, cmp_ = ctx.kmp_search_device(p, d_text.data_ptr(), S, d_out.data_ptr(), cap, base=rank * S)
     sampler = ClockSampler(local)
+    kmp_step = lambda: ctx.kmp_search_device(p, d_text.data_ptr(), S, d_out.data_ptr(), cap, base=rank * S)  # noqa: E731
     with sampler:
+        sampler.settle(kmp_step if world == 1 else (lambda: time.sleep(0.02)))
         barrier()
         l0 = ctx.launches
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         kms = []
         for _ in range(args.steps):
-            nm, cmp_ = ctx.kmp_search_device(p, d_text.data_ptr(), S, d_out.data_ptr(), cap, base=rank * S)
+            nm, cmp_ = kmp_step()
             kms.append(ctx.last_kernel_ms())
         ev1.record(stream)
         ctx.synchronize()
         barrier()
         launches = ctx.launches - l0
+        if world == 1:
+            sampler.hold(kmp_step)
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
         kernel_ms = max_over_ranks(statistics.mean(kms))
     peak, peak_src = peaks()
