@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -152,13 +153,21 @@ def pack_patterns(patterns):
 
 
 def _take(ptr: vp, n: int, dtype) -> np.ndarray:
+    """numpy view of a library-owned result array; large results are not
+    copied -- the buffer is released by glop_free once the last view is
+    gone."""
     if not n:
         _lib.glop_free(ptr)
         return np.zeros(0, dtype=dtype)
-    raw = np.ctypeslib.as_array(C.cast(ptr, u8p), shape=(n * np.dtype(dtype).itemsize,))
-    out = raw.view(dtype).copy()
-    _lib.glop_free(ptr)
-    return out
+    nbytes = n * np.dtype(dtype).itemsize
+    if nbytes < (1 << 20):
+        raw = np.ctypeslib.as_array(C.cast(ptr, u8p), shape=(nbytes,))
+        out = raw.view(dtype).copy()
+        _lib.glop_free(ptr)
+        return out
+    buf = (C.c_uint8 * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, _lib.glop_free, C.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dtype)
 
 
 # ----------------------------------------------------------------- host side
