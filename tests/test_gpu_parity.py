@@ -430,3 +430,41 @@ def test_kmp_shards_equal_whole(ctx, torch_cuda):
                 cmp_total += c
             assert np.array_equal(np.concatenate(offs), r_offs), (p, shards)
             assert cmp_total == r_cmp, (p, shards)
+
+
+def test_prefix8_small_and_ragged(ctx, torch_cuda):
+    """PREFIX8 on the edge cases the big inputs do not reach: texts of 0..5000
+    bytes (< 8, one tile, a tile + a few bytes), unaligned starts, shards
+    with tiny owned ranges, full-byte alphabets, prefixes colliding on their
+    first 8 bytes, patterns longer than the prefix (the deeper trie walk)."""
+    rng = np.random.default_rng(2024)
+    for trial in range(120):
+        alpha = 4 if trial % 3 == 0 else 256
+        n = int(rng.choice([0, 1, 7, 8, 9, 100, 2047, 2048, 2049, 2063, 4096 + 5, int(rng.integers(0, 5000))]))
+        text = (rng.integers(0, alpha, n) + (65 if alpha == 4 else 0)).astype(np.uint8)
+        k = int(rng.integers(1, 24))
+        pats = []
+        for _ in range(k):
+            ln = int(rng.integers(8, 17))
+            if n >= ln and rng.random() < 0.6:  # a window of the text: guaranteed hits
+                o = int(rng.integers(0, n - ln + 1))
+                pats.append(text[o:o + ln].tobytes())
+            else:
+                pats.append((rng.integers(0, alpha, ln) + (65 if alpha == 4 else 0)).astype(np.uint8).tobytes())
+        pats = list(dict.fromkeys(pats))
+        L = 8 if trial % 4 else 12
+        trie = ctx.upload(glop.build_failureless_trie(pats, L))
+        assert trie.info.min_depth >= 8
+        ref = O.pfac_scan(text, O.Trie(pats, L)) if n else np.zeros(0, dtype=glop.HIT_DTYPE)
+        off = int(rng.integers(0, 16))
+        padded = np.concatenate([np.zeros(off, np.uint8), text])
+        got = dev_scan(ctx, torch_cuda, trie, padded, glop.PFAC_PREFIX8, offset=off)
+        assert got.tobytes() == ref.tobytes(), (trial, n, k, L, off)
+        if n > 20:  # a shard: starts [lo, hi) of the text, reading an lmax-1 halo
+            lo = int(rng.integers(0, n - 10))
+            hi = int(rng.integers(lo + 1, n + 1))
+            rd = min(hi + trie.info.max_depth - 1, n)
+            part = dev_scan(ctx, torch_cuda, trie, text[lo:rd], glop.PFAC_PREFIX8, own=hi - lo, base=lo + (1 << 33))
+            want = ref[(ref["offset"] >= lo) & (ref["offset"] < hi)].copy()
+            want["offset"] += 1 << 33
+            assert part.tobytes() == want.tobytes(), (trial, lo, hi)
