@@ -468,3 +468,31 @@ def test_prefix8_small_and_ragged(ctx, torch_cuda):
             want = ref[(ref["offset"] >= lo) & (ref["offset"] < hi)].copy()
             want["offset"] += 1 << 33
             assert part.tobytes() == want.tobytes(), (trial, lo, hi)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_pipeline_shards_1_2_4_8(ctx, torch_cuda, world):
+    """SURVEY §8e parity: the per-rank pipeline (glop_run_pfac_pipeline_shard
+    on shards.plan_shards ranges with the halo bench.py uses) concatenated in
+    rank order, counts summed, equals the single-GPU result -- for 1, 2, 4
+    and 8 ranks (run here one after another on one GPU)."""
+    from paper_1704_02278_b200.shards import plan_shards
+
+    n = 24 << 20
+    d = torch_cuda.empty(n + 64, dtype=torch_cuda.uint8, device="cuda")
+    ctx.gen_syslog_device(d.data_ptr(), n, seed=99)
+    ctx.synchronize()
+    pats, _ = glop.gen_rules(1000, seed=606)
+    pats += [b"Failed password for invalid user", b"pam_unix(sshd:session): session opened"]
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    rules = ctx.upload_rules(pats, 8)
+    whole = ctx.run_pfac_pipeline(trie, rules, d.data_ptr(), n, True)
+    halo = max(trie.info.max_depth, max(len(p) for p in pats)) - 1
+    alerts, counts, s1 = [], np.zeros(len(pats), np.uint64), 0
+    for sh in plan_shards(n, world, halo):
+        a, c, h = ctx.run_pfac_pipeline(trie, rules, d.data_ptr() + sh.lo, sh.read, True, own=sh.own, base=sh.lo)
+        alerts.append(a)
+        counts += c
+        s1 += h
+    assert np.concatenate(alerts).tobytes() == whole[0].tobytes()
+    assert np.array_equal(counts, whole[1]) and s1 == whole[2]
