@@ -537,11 +537,46 @@ glop_status to_device_text(glop_ctx* c, const uint8_t* text, uint64_t n, int on_
   return GLOP_OK;
 }
 
+// Hits were not in (offset, id) order: order the alerts on the device, as the
+// reference sorts them (verify.hpp:100-103).  end = largest global offset + 1.
+glop_status sort_alerts(glop_ctx* c, const glop_rules* r, uint64_t end, glop_alert* d_out, uint64_t kept) {
+  if (kept < 2) return GLOP_OK;
+  if (r->view.n_patterns > (1u << 24) || end >= (1ull << 40))
+    return fail(GLOP_EINVAL, "verify_hits: unsorted hits need ids < 2^24 and offsets < 2^40");
+  TRY(c->keys.ensure(kept * 8));
+  TRY(c->keys_alt.ensure(kept * 8));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((kept + 255) / 256, 4096);
+  c->launches += 2;
+  alerts_to_keys_kernel<<<grid, 256, 0, c->stream>>>(reinterpret_cast<DevAlert*>(d_out), kept,
+                                                     c->keys.as<unsigned long long>());
+  TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), kept));
+  keys_to_alerts_kernel<<<grid, 256, 0, c->stream>>>(c->keys_alt.as<unsigned long long>(), kept, r->view,
+                                                     reinterpret_cast<DevAlert*>(d_out));
+  CU(cudaGetLastError());
+  return GLOP_OK;
+}
+
 glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* d_text, uint64_t n,
                                uint64_t base, const glop_hit* d_hits, uint64_t n_hits, glop_alert* d_out,
                                uint64_t* n_alerts, uint64_t* d_counts) {
   *n_alerts = 0;
   if (n_hits == 0) return GLOP_OK;
+  if (r->max_len <= r->view.prefix_len) {  // every hit is auto-verified: one pass
+    TRY(c->misc.ensure(64));
+    CU(cudaMemsetAsync(c->misc.p, 0, 16, c->stream));
+    auto* fl_all = reinterpret_cast<unsigned int*>(c->misc.as<unsigned long long>() + 1);
+    ++c->launches;
+    verify_all_kernel<<<(uint32_t)std::min<uint64_t>((n_hits + 1023) / 1024, 2u * c->num_sms), 1024, 0, c->stream>>>(
+        r->view, base, n, reinterpret_cast<const DevHit*>(d_hits), n_hits, reinterpret_cast<DevAlert*>(d_out),
+        reinterpret_cast<unsigned long long*>(d_counts), fl_all);
+    CU(cudaGetLastError());
+    TRY(sync_read(c, c->misc.p, 16));
+    const unsigned fl = (unsigned)(c->h_misc[1] & 0xffffffffu);
+    if (fl & 1u) return fail(GLOP_ELOGIC, "verify_hits: hit extends past end of text");
+    *n_alerts = n_hits;
+    if (fl & 2u) return sort_alerts(c, r, base + n, d_out, n_hits);
+    return GLOP_OK;
+  }
   const uint32_t nb = (uint32_t)((n_hits + kVerifyBlock - 1) / kVerifyBlock);
   TRY(c->keep.ensure(n_hits));
   TRY(c->bcounts.ensure(nb * 4));
@@ -575,22 +610,7 @@ glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* 
   }
   CU(cudaGetLastError());
   *n_alerts = kept;
-  if ((fl & 2u) && kept > 1) {
-    // hits were not in (offset, id) order: order the alerts on the device
-    // (verify.hpp:100-103)
-    if (r->view.n_patterns > (1u << 24) || base + n >= (1ull << 40))
-      return fail(GLOP_EINVAL, "verify_hits: unsorted hits need ids < 2^24 and offsets < 2^40");
-    TRY(c->keys.ensure(kept * 8));
-    TRY(c->keys_alt.ensure(kept * 8));
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((kept + 255) / 256, 4096);
-    c->launches += 2;
-    alerts_to_keys_kernel<<<grid, 256, 0, c->stream>>>(reinterpret_cast<DevAlert*>(d_out), kept,
-                                                       c->keys.as<unsigned long long>());
-    TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), kept));
-    keys_to_alerts_kernel<<<grid, 256, 0, c->stream>>>(c->keys_alt.as<unsigned long long>(), kept, r->view,
-                                                       reinterpret_cast<DevAlert*>(d_out));
-    CU(cudaGetLastError());
-  }
+  if (fl & 2u) return sort_alerts(c, r, base + n, d_out, kept);
   return GLOP_OK;
 }
 

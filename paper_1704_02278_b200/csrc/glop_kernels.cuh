@@ -833,6 +833,46 @@ __global__ void __launch_bounds__(1024) alert_histogram_kernel(const DevAlert* a
     if (h[i]) atomicAdd(counts + i, (unsigned long long)h[i]);
 }
 
+// verify_hits when every pattern is at most prefix_len long (all hits are
+// auto-verified, verify.hpp:79-81): one pass converts hits to alerts, checks
+// bounds / ids (flag 1, the reference's logic_error) and order (flag 2), and
+// builds the per-pattern histogram (shared memory when k <= kHistBins).
+__global__ void __launch_bounds__(1024) verify_all_kernel(const DevRules r, unsigned long long base,
+                                                          unsigned long long n, const DevHit* hits,
+                                                          unsigned long long n_hits, DevAlert* out,
+                                                          unsigned long long* counts, unsigned int* flags) {
+  __shared__ uint32_t h[kHistBins];
+  const bool hist = counts && r.n_patterns <= kHistBins;
+  if (hist)
+    for (uint32_t i = threadIdx.x; i < r.n_patterns; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  unsigned int fl = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n_hits;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const DevHit x = hits[i];
+    if (x.offset < base || x.offset + x.len > base + n || x.pid >= r.n_patterns) {
+      fl |= 1u;
+      continue;
+    }
+    if (i + 1 < n_hits) {
+      const DevHit y = hits[i + 1];
+      if (y.offset < x.offset || (y.offset == x.offset && y.pid < x.pid)) fl |= 2u;
+    }
+    DevAlert a;
+    a.offset = x.offset;
+    a.rule_id = x.pid;
+    a.pattern_len = (uint32_t)(r.off[x.pid + 1] - r.off[x.pid]);
+    out[i] = a;
+    if (hist) atomicAdd(&h[x.pid], 1u);
+    else if (counts) atomicAdd(counts + x.pid, 1ull);
+  }
+  if (fl) atomicOr(flags, fl);
+  __syncthreads();
+  if (hist)
+    for (uint32_t i = threadIdx.x; i < r.n_patterns; i += blockDim.x)
+      if (h[i]) atomicAdd(counts + i, (unsigned long long)h[i]);
+}
+
 // Unsorted-input path of verify: alerts <-> (offset << 24 | rule) keys.
 __global__ void alerts_to_keys_kernel(const DevAlert* a, unsigned long long n, unsigned long long* keys) {
   for (unsigned long long h = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; h < n;
