@@ -3,19 +3,21 @@
 // truncated prefixes").  Same result as pfac_scan (scan.hpp:113-202) and the
 // general kernel in glop_kernels.cuh, with far fewer instructions per byte:
 //
-//  * One 512-thread CTA per SM; each of its 16 warps streams a CONTIGUOUS
-//    segment of 4 KB tiles through a private double-buffered TMA pipeline
+//  * One 768-thread CTA per SM; each of its 24 warps streams a CONTIGUOUS
+//    segment of 2 KB tiles through a private double-buffered TMA pipeline
 //    (cp.async.bulk + mbarrier).  A warp's hits are therefore produced in text
 //    order: its staging region is already sorted, and the final output is the
 //    concatenation of the regions in warp order (no per-tile directory).
-//  * Level 1, aligned q-gram sampling: every match start c has, for the
-//    unique d in 1..4 with c + d = 0 (mod 4), the pattern's 4-gram at offset d
-//    sitting in an aligned text word.  A lane owns 8 consecutive sample words
-//    (two LDS.128); each word gets one hashed d-mask probe.
-//  * Candidate words are compacted in text order (bit-plane ballot prefix)
-//    and checked 32 per round: the 8-byte key of candidate c = 4i - d is
-//    assembled from words i-1, i, i+1 with constant funnel shifts and tested
-//    in a 2^18-bit prefix bitmap.
+//  * Level 1, aligned 5-byte grams: every match start c has, for the unique
+//    d in 1..4 with c + d = 0 (mod 4), an aligned text word i whose bytes
+//    [4i-1, 4i+4) are pattern bytes [d-1, d+4).  A lane owns 16 sample words
+//    per tile (8 consecutive in each half: two LDS.128 + a shuffle per half);
+//    each word gets one hashed d-mask probe.
+//  * Candidate words are compacted in text order into a u16 queue (one
+//    packed shuffle scan gives both halves' prefixes) and checked 32 per
+//    round: the 8-byte key of candidate c = 4i - d is assembled from words
+//    i-1, i, i+1 with constant funnel shifts and tested in a 2^18-bit prefix
+//    bitmap.
 //  * Bitmap survivors probe the exact J=8 jump table (generalised RootJump,
 //    scan.hpp:81-108) in global memory (L2-resident) and, for patterns longer
 //    than 8 bytes, continue the trie walk (scan.hpp:142-168).
