@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the Gbps-vs-pattern-count sweep (pfac, N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline work")
     a = ap.parse_args()
     if a.bytes_per_gpu is None:
@@ -369,6 +370,8 @@ def main():
                                  "table_in_smem": bool(info.table_in_smem)}}}
     if e2e is not None:
         line["e2e"] = e2e
+    if world == 1 and args.config == "pfac" and not args.no_sweep:
+        line["pattern_sweep"] = pattern_sweep(args, ctx, glop, d_text, sh, d_hits, cap, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(sh.own, 2 << 30)
         host = d_text[:sample].cpu().numpy()
@@ -378,6 +381,26 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def pattern_sweep(args, ctx, glop, d_text, sh, d_hits, cap, peak):
+    """The metric's "vs pattern count" axis: the PFAC scan of the same
+    resident shard for 10 / 100 / 1,000 / 10,000 rules (same generator, same
+    seed), mean kernel time of 5 launches after 2 warm-ups."""
+    out = []
+    for k in (10, 100, 1000, 10000):
+        pats, vocab = glop.gen_rules(k, args.rules_seed)
+        trie = ctx.upload(glop.build_failureless_trie(pats, args.prefix_len))
+        kms = []
+        for i in range(7):
+            nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), sh.read, d_hits.data_ptr(), cap, own=sh.own, base=sh.lo)
+            if i >= 2:
+                kms.append(ctx.last_kernel_ms())
+        ms = statistics.mean(kms)
+        gbs = sh.own / (ms / 1e3) / 1e9
+        out.append({"patterns": k, "kernel_ms": round(ms, 4), "gbps": round(8 * gbs, 1), "hbm_frac": round(gbs / peak, 4),
+                    "hits": int(nh), "vocab_rules": int(vocab.sum()), "trie_states": trie.info.state_count})
+    return out
 
 
 def run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, torch, dist):
