@@ -87,22 +87,24 @@ struct P8Params {
 constexpr uint32_t kP8NibbleGrams = 12000;
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
-  return (g * 0x9E3779B1u) >> (32 - kP8DmaskLog2 - (kNibble ? 1 : 0));
+  return g >> (32 - kP8DmaskLog2 - (kNibble ? 1 : 0));
 }
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_dmask_byte(uint32_t h) { return kNibble ? h >> 1 : h; }
 template <bool kNibble>
 __host__ __device__ __forceinline__ uint32_t p8_dmask_shift(uint32_t h) { return kNibble ? (h & 1) << 2 : 0; }
-// Level-1 gram of sample word i: the 5 bytes [4i-1, 4i+4) -- the aligned
+// Level-1 hash of sample word i over the 5 bytes [4i-1, 4i+4) -- the aligned
 // word `cur` and the top byte of the previous word -- which for a match at
 // c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes instead of
-// four cut the candidate words by ~40% on the syslog vocabulary set for one
-// shift + one multiply-add.  (GLOP_P8_Q4: the plain aligned 4-gram.)
+// four cut the candidate words by ~40% on the syslog vocabulary set; the
+// fifth byte is XORed (LOP3, together with its mask) into the top of the
+// multiplicative hash of `cur`, so a probe is IMAD + LOP3 + SHF + LDS.
+// p8_h1 takes the top bits.  (GLOP_P8_Q4: the plain aligned 4-gram.)
 __host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur) {
 #ifdef GLOP_P8_Q4
-  return cur;
+  return cur * 0x9E3779B1u;
 #else
-  return (prev >> 24) * 0x2545F491u + cur;
+  return (cur * 0x9E3779B1u) ^ (prev & 0xFF000000u);
 #endif
 }
 template <bool kNibble>
@@ -315,12 +317,23 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t totA = tot & 0xFFFFu;
         uint32_t atA = (incl - cnt) & 0xFFFFu, atB = totA + ((incl - cnt) >> 16);
+        // 16 predicated u16 stores through a running shared-memory address
+        // per half (value = word << 4 | d-mask; the word base is per lane)
+        uint32_t qa = smem_u32(q) + 2 * atA, qb = smem_u32(q) + 2 * atB;
+        uint32_t vb;  // opaque, so each value is one IADD3 (vb + m + const)
+        asm("mov.u32 %0, %1;" : "=r"(vb) : "r"((8 * lane + 1) << 4));
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j)
-          if (mm8[0][j]) q[atA++] = (uint16_t)(((8 * lane + 1 + j) << 4) | mm8[0][j]);
+          if (mm8[0][j]) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(vb + (j << 4) + mm8[0][j]) : "memory");
+            qa += 2;
+          }
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j)
-          if (mm8[1][j]) q[atB++] = (uint16_t)(((kP8Tile / 8 + 8 * lane + 1 + j) << 4) | mm8[1][j]);
+          if (mm8[1][j]) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qb), "r"(vb + ((kP8Tile / 8 + j) << 4) + mm8[1][j]) : "memory");
+            qb += 2;
+          }
         qt = totA + (tot >> 16);
         __syncwarp();
       }
@@ -346,8 +359,10 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         for (uint32_t d = 1; d <= 4; ++d) {
           const uint32_t x = prefix_hash32(__funnelshift_r(w0, w1, 32 - 8 * d), __funnelshift_r(w1, w2, 32 - 8 * d));
           const uint32_t word = s_bm2[x >> (32 - kBm2Log2 + 5)];
-          surv |= (__funnelshift_r(word, 0u, x >> (32 - kBm2Log2)) & (mm >> (d - 1)) & 1u) << (d - 1);
+          // rotate bit (x >> 14) & 31 of the bitmap word to position d - 1
+          surv |= __funnelshift_r(word, word, (x >> (32 - kBm2Log2)) + (33 - d)) & (1u << (d - 1));
         }
+        surv &= mm;
         const uint32_t runmask = __ballot_sync(0xffffffffu, surv != 0);
         if (!runmask) continue;
         // ---- exact check of the survivors; a pass that overflows the hit
