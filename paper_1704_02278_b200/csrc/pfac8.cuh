@@ -11,10 +11,13 @@
 //  * Level 1, aligned 5-byte grams: every match start c has, for the unique
 //    d in 1..4 with c + d = 0 (mod 4), an aligned text word i whose bytes
 //    [4i-1, 4i+4) are pattern bytes [d-1, d+4).  A lane owns 16 sample words
-//    per tile (8 consecutive in each half: two LDS.128 + a shuffle per half);
-//    each word gets one hashed d-mask probe.
+//    per tile, 4 consecutive in each 512-byte quarter, read by one
+//    conflict-free LDS.128 per quarter (consecutive lanes, consecutive 16 B:
+//    the earlier 8-consecutive-words layout was a 2-way bank conflict, and
+//    shared-memory wavefronts bound this kernel); each word gets one hashed
+//    d-mask probe.
 //  * Candidate words are compacted in text order into a u16 queue (one
-//    packed shuffle scan gives both halves' prefixes) and checked 32 per
+//    packed shuffle scan gives all four quarters' prefixes) and checked 32 per
 //    round: the 8-byte key of candidate c = 4i - d is assembled from words
 //    i-1, i, i+1 with constant funnel shifts and tested in a 2^18-bit prefix
 //    bitmap.
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint8_t* s_dmask = smem + L.dmask;
   const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
+  const uint32_t bm2_a = smem_u32(s_bm2);
   const uint8_t* s_cls = smem + L.cls;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars) + warp * 2;
   uint8_t* bufs = smem + L.bufs + (size_t)warp * 2 * kP8Stage;
@@ -282,32 +286,38 @@ __global__ void __launch_bounds__(kP8Threads, 1)
     // scan gives both halves' prefixes -- and are checked 32 per round.
     uint32_t qt = 0;
     {
-      uint32_t lo4[2], hi4[2], mm8[2][8];
+      // quarter k of the tile samples words 128 k + 1 .. 128 k + 128; lane l
+      // takes words 128 k + 4 l + 1 .. + 4 from one conflict-free LDS.128
+      // (consecutive lanes, consecutive 16 B) and the next lane's first word
+      uint32_t mq[4], mm4[4][4];
 #pragma unroll
       for (uint32_t hf = 0; hf < 2; ++hf) {
         const uint32_t W = hf * (kP8Tile / 8);
-        const uint4 va = reinterpret_cast<const uint4*>(sw + W)[2 * lane];
-        const uint4 vb = reinterpret_cast<const uint4*>(sw + W)[2 * lane + 1];
+        const uint4 va = reinterpret_cast<const uint4*>(sw + W)[lane];
+        const uint4 vb = reinterpret_cast<const uint4*>(sw + W)[32 + lane];
         const uint32_t wn = sw[W + kP8Tile / 8];
-        uint32_t w8 = __shfl_down_sync(0xffffffffu, va.x, 1);
-        if (lane == 31) w8 = wn;
-        uint32_t* m = mm8[hf];
-        m[0] = p8_dmask<kNibble>(s_dmask, p8_gram(va.x, va.y));
-        m[1] = p8_dmask<kNibble>(s_dmask, p8_gram(va.y, va.z));
-        m[2] = p8_dmask<kNibble>(s_dmask, p8_gram(va.z, va.w));
-        m[3] = p8_dmask<kNibble>(s_dmask, p8_gram(va.w, vb.x));
-        m[4] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.x, vb.y));
-        m[5] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.y, vb.z));
-        m[6] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.z, vb.w));
-        m[7] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.w, w8));
-        lo4[hf] = __byte_perm(m[0] | (m[1] << 8), m[2] | (m[3] << 8), 0x5410);
-        hi4[hf] = __byte_perm(m[4] | (m[5] << 8), m[6] | (m[7] << 8), 0x5410);
+        const uint32_t na = __shfl_sync(0xffffffffu, lane == 0 ? vb.x : va.x, (lane + 1) & 31);
+        uint32_t nb = __shfl_down_sync(0xffffffffu, vb.x, 1);
+        if (lane == 31) nb = wn;
+        uint32_t* a = mm4[2 * hf];
+        uint32_t* b = mm4[2 * hf + 1];
+        a[0] = p8_dmask<kNibble>(s_dmask, p8_gram(va.x, va.y));
+        a[1] = p8_dmask<kNibble>(s_dmask, p8_gram(va.y, va.z));
+        a[2] = p8_dmask<kNibble>(s_dmask, p8_gram(va.z, va.w));
+        a[3] = p8_dmask<kNibble>(s_dmask, p8_gram(va.w, na));
+        b[0] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.x, vb.y));
+        b[1] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.y, vb.z));
+        b[2] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.z, vb.w));
+        b[3] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.w, nb));
+        mq[2 * hf] = __byte_perm(a[0] | (a[1] << 8), a[2] | (a[3] << 8), 0x5410);
+        mq[2 * hf + 1] = __byte_perm(b[0] | (b[1] << 8), b[2] | (b[3] << 8), 0x5410);
       }
-      if (__ballot_sync(0xffffffffu, (lo4[0] | hi4[0] | lo4[1] | hi4[1]) != 0)) {
-        // candidate words per half (d-masks are < 16: adding 0x7F to a byte
-        // sets its top bit iff the byte is non-zero), packed cntA | cntB << 16
+      if (__ballot_sync(0xffffffffu, (mq[0] | mq[1] | mq[2] | mq[3]) != 0)) {
+        // candidate words per quarter (d-masks are < 16: adding 0x7F to a
+        // byte sets its top bit iff the byte is non-zero), packed 8 bits per
+        // quarter (<= 128 each): one shuffle scan gives all four prefixes
         auto nz = [](uint32_t x) { return __popc((x + 0x7F7F7F7Fu) & 0x80808080u); };
-        const uint32_t cnt = (nz(lo4[0]) + nz(hi4[0])) | ((nz(lo4[1]) + nz(hi4[1])) << 16);
+        const uint32_t cnt = nz(mq[0]) | (nz(mq[1]) << 8) | (nz(mq[2]) << 16) | (nz(mq[3]) << 24);
         uint32_t incl = cnt;
 #pragma unroll
         for (uint32_t o = 1; o < 32; o <<= 1) {
@@ -315,26 +325,38 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           if (lane >= o) incl += x;
         }
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t totA = tot & 0xFFFFu;
-        uint32_t atA = (incl - cnt) & 0xFFFFu, atB = totA + ((incl - cnt) >> 16);
+        const uint32_t ex = incl - cnt;
         // 16 predicated u16 stores through a running shared-memory address
-        // per half (value = word << 4 | d-mask; the word base is per lane)
-        uint32_t qa = smem_u32(q) + 2 * atA, qb = smem_u32(q) + 2 * atB;
-        uint32_t vb;  // opaque, so each value is one IADD3 (vb + m + const)
-        asm("mov.u32 %0, %1;" : "=r"(vb) : "r"((8 * lane + 1) << 4));
+        // per quarter (value = word << 4 | d-mask; the word base is per lane)
+        uint32_t vl;  // opaque, so each value is one IADD3 (vl + m + const)
+        asm("mov.u32 %0, %1;" : "=r"(vl) : "r"((4 * lane + 1) << 4));
+        uint32_t base = smem_u32(q);
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j)
-          if (mm8[0][j]) {
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(vb + (j << 4) + mm8[0][j]) : "memory");
+        for (uint32_t k = 0; k < 4; ++k) {
+          uint32_t qa = base + 2 * ((ex >> (8 * k)) & 0xFFu);
+#ifdef GLOP_P8_LOOPQ4
+          // one store per set byte (loop count = the warp's max per lane)
+          uint32_t bits = ((((mq[k] + 0x7F7F7F7Fu) & 0x80808080u) >> 7) * 0x01020408u) >> 24;
+          while (bits) {
+            const uint32_t j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa),
+                         "r"(vl + ((128 * k) << 4) + (j << 4) + (__byte_perm(mq[k], 0, j) & 15u)) : "memory");
             qa += 2;
           }
+#else
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j)
-          if (mm8[1][j]) {
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qb), "r"(vb + ((kP8Tile / 8 + j) << 4) + mm8[1][j]) : "memory");
-            qb += 2;
+          for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t m = mm4[k][j];
+            if (m) {
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(vl + ((128 * k + j) << 4) + m) : "memory");
+              qa += 2;
+            }
           }
-        qt = totA + (tot >> 16);
+#endif
+          base += 2 * ((tot >> (8 * k)) & 0xFFu);
+        }
+        qt = (tot & 0xFFu) + ((tot >> 8) & 0xFFu) + ((tot >> 16) & 0xFFu) + (tot >> 24);
         __syncwarp();
       }
     }
@@ -358,7 +380,12 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 #pragma unroll
         for (uint32_t d = 1; d <= 4; ++d) {
           const uint32_t x = prefix_hash32(__funnelshift_r(w0, w1, 32 - 8 * d), __funnelshift_r(w1, w2, 32 - 8 * d));
-          const uint32_t word = s_bm2[x >> (32 - kBm2Log2 + 5)];
+          // probe only for the d-mask's offsets: predicated-off lanes take no
+          // shared-memory bank slot (fewer conflicts)
+          uint32_t word = x;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.shared.b32 %0, [%1];\n}"
+                       : "+r"(word)
+                       : "r"(bm2_a + ((x >> (32 - kBm2Log2 + 5)) << 2)), "r"(mm & (1u << (d - 1))));
           // rotate bit (x >> 14) & 31 of the bitmap word to position d - 1
           surv |= __funnelshift_r(word, word, (x >> (32 - kBm2Log2)) + (33 - d)) & (1u << (d - 1));
         }
