@@ -109,7 +109,7 @@ struct glop_trie {
   bool u16 = true;
   bool smem_filter = false, smem_direct = false, smem_jump = false;
   bool p8 = false;  // every output at depth >= 8: pfac8_kernel applies
-  bool p8_nibble = false;  // pfac8 d-mask layout (see pfac8.cuh)
+  bool p8_bits = false;  // pfac8 d-mask layout (see pfac8.cuh)
   uint32_t max_pid = 0;
 };
 
@@ -211,9 +211,9 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
   auto* g = c->misc.as<unsigned long long>();
   auto launch = [&](const P8Params& p) -> glop_status {
     auto k = t->info.max_depth > 8
-                 ? (t->p8_nibble ? (t->u16 ? pfac8_kernel<true, true, uint16_t> : pfac8_kernel<true, true, uint32_t>)
+                 ? (t->p8_bits ? (t->u16 ? pfac8_kernel<true, true, uint16_t> : pfac8_kernel<true, true, uint32_t>)
                                  : (t->u16 ? pfac8_kernel<true, false, uint16_t> : pfac8_kernel<true, false, uint32_t>))
-                 : (t->p8_nibble ? (t->u16 ? pfac8_kernel<false, true, uint16_t> : pfac8_kernel<false, true, uint32_t>)
+                 : (t->p8_bits ? (t->u16 ? pfac8_kernel<false, true, uint16_t> : pfac8_kernel<false, true, uint32_t>)
                                  : (t->u16 ? pfac8_kernel<false, false, uint16_t> : pfac8_kernel<false, false, uint32_t>));
     CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     CU(cudaEventRecord(c->ev0, c->stream));
@@ -884,7 +884,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
   std::vector<unsigned long long> grams8;  // (p8_gram << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
-  bool nibble8 = false;
+  bool bits8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -938,13 +938,13 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
     if (p8) {
       std::sort(grams8.begin(), grams8.end());
       grams8.erase(std::unique(grams8.begin(), grams8.end()), grams8.end());
-      const char* env = getenv("GLOP_P8_NIBBLE_MIN");  // experiments: override the layout threshold
-      nibble8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8NibbleGrams);
+      const char* env = getenv("GLOP_P8_BITS_MIN");  // experiments: override the layout threshold
+      bits8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8BitsGrams);
       for (unsigned long long x : grams8) {
         const uint32_t g = (uint32_t)(x >> 2), bit = 1u << (x & 3);
-        if (nibble8) {
+        if (bits8) {
           const uint32_t h = p8_h1<true>(g);
-          dmask8[p8_dmask_byte<true>(h)] |= (uint8_t)(bit << p8_dmask_shift<true>(h));
+          dmask8[h >> 3] |= (uint8_t)(1u << (h & 7));  // little-endian bit h of the u32 words
         } else {
           dmask8[p8_h1<false>(g)] |= (uint8_t)bit;
         }
@@ -1004,7 +1004,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
-  t->p8_nibble = nibble8;
+  t->p8_bits = bits8;
   t->view.jump_depth = J;
   t->view.jump_cap_log2 = cap_log2;
   t->view.jump_bytes = (uint32_t)jump_bytes;

@@ -82,20 +82,19 @@ struct P8Params {
 // Bloom variant halved the candidate words but doubled the bank-conflicted
 // shared-memory probes, which bound the kernel (measured: 3.63 -> 3.55 ms at
 // k=1,000 and 2.46 -> 1.97 ms at k=10 without it).  Built by glop_trie_upload.
-// Two layouts of the same 64 KB: kNibble = false, 2^16 one-byte buckets
-// (bits 0..3 used); kNibble = true, 2^17 four-bit buckets -- half the hash
-// collisions for large pattern sets (DPI: 10,000 contents, ~40K grams) at
-// two more instructions per probe.  The host picks per automaton
-// (glop_trie_upload: nibbles above kP8NibbleGrams distinct grams).
-constexpr uint32_t kP8NibbleGrams = 12000;
-template <bool kNibble>
+// Two layouts of the same 64 KB: kBits = false, 2^16 one-byte buckets
+// holding the d-mask (bits 0..3); kBits = true, 2^19 one-bit buckets
+// ("some offset d may match": the drain tests all four).  Above ~1,000
+// distinct grams hash collisions dominate the candidate words and the 8x
+// finer bit table wins despite two more instructions per probe (measured:
+// k=1,000 2.76 -> 2.60 ms, DPI 10,000 contents 3.40 -> 2.87 ms, syslog
+// k=10,000 6.04 -> 4.03 ms; an intermediate 2^17 x 4-bit layout sat between).
+// The host picks per automaton (glop_trie_upload: bits above kP8BitsGrams).
+constexpr uint32_t kP8BitsGrams = 1024;
+template <bool kBits>
 __host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
-  return g >> (32 - kP8DmaskLog2 - (kNibble ? 1 : 0));
+  return g >> (32 - kP8DmaskLog2 - (kBits ? 3 : 0));
 }
-template <bool kNibble>
-__host__ __device__ __forceinline__ uint32_t p8_dmask_byte(uint32_t h) { return kNibble ? h >> 1 : h; }
-template <bool kNibble>
-__host__ __device__ __forceinline__ uint32_t p8_dmask_shift(uint32_t h) { return kNibble ? (h & 1) << 2 : 0; }
 // Level-1 hash of sample word i over the 5 bytes [4i-1, 4i+4) -- the aligned
 // word `cur` and the top byte of the previous word -- which for a match at
 // c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes instead of
@@ -110,10 +109,14 @@ __host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur
   return (cur * 0x9E3779B1u) ^ (prev & 0xFF000000u);
 #endif
 }
-template <bool kNibble>
+template <bool kBits>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
-  const uint32_t h = p8_h1<kNibble>(g);
-  return kNibble ? (dm[p8_dmask_byte<kNibble>(h)] >> p8_dmask_shift<kNibble>(h)) & 15u : dm[h];
+  const uint32_t h = p8_h1<kBits>(g);
+  if (kBits) {
+    const uint32_t w = reinterpret_cast<const uint32_t*>(dm)[h >> 5];
+    return __funnelshift_r(w, w, h) & 1u;  // bit h & 31
+  }
+  return dm[h];
 }
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
@@ -167,7 +170,7 @@ __device__ __noinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, u
   return nb;
 }
 
-template <bool kWalk, bool kNibble, typename Entry>
+template <bool kWalk, bool kBits, typename Entry>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
@@ -301,14 +304,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (lane == 31) nb = wn;
         uint32_t* a = mm4[2 * hf];
         uint32_t* b = mm4[2 * hf + 1];
-        a[0] = p8_dmask<kNibble>(s_dmask, p8_gram(va.x, va.y));
-        a[1] = p8_dmask<kNibble>(s_dmask, p8_gram(va.y, va.z));
-        a[2] = p8_dmask<kNibble>(s_dmask, p8_gram(va.z, va.w));
-        a[3] = p8_dmask<kNibble>(s_dmask, p8_gram(va.w, na));
-        b[0] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.x, vb.y));
-        b[1] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.y, vb.z));
-        b[2] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.z, vb.w));
-        b[3] = p8_dmask<kNibble>(s_dmask, p8_gram(vb.w, nb));
+        a[0] = p8_dmask<kBits>(s_dmask, p8_gram(va.x, va.y));
+        a[1] = p8_dmask<kBits>(s_dmask, p8_gram(va.y, va.z));
+        a[2] = p8_dmask<kBits>(s_dmask, p8_gram(va.z, va.w));
+        a[3] = p8_dmask<kBits>(s_dmask, p8_gram(va.w, na));
+        b[0] = p8_dmask<kBits>(s_dmask, p8_gram(vb.x, vb.y));
+        b[1] = p8_dmask<kBits>(s_dmask, p8_gram(vb.y, vb.z));
+        b[2] = p8_dmask<kBits>(s_dmask, p8_gram(vb.z, vb.w));
+        b[3] = p8_dmask<kBits>(s_dmask, p8_gram(vb.w, nb));
         mq[2 * hf] = __byte_perm(a[0] | (a[1] << 8), a[2] | (a[3] << 8), 0x5410);
         mq[2 * hf + 1] = __byte_perm(b[0] | (b[1] << 8), b[2] | (b[3] << 8), 0x5410);
       }
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         // ---- 8-byte keys of up to 32 candidate words -> prefix bitmap
         const uint32_t e = lane < pend ? q[qh + lane] : 16u;  // idle lanes: word 1, no bits
         const uint32_t i = e >> 4;
-        uint32_t mm = e & 15u;
+        uint32_t mm = kBits ? (e & 1u) * 15u : e & 15u;  // bit layout: all four offsets
         const uint32_t w0 = sw[i - 1], w1 = sw[i], w2 = sw[i + 1];
         if (edge) {
 #pragma unroll

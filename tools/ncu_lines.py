@@ -25,3 +25,17 @@ it = nbytes / 512
 print(f"total warp-inst {tot} = {tot/it:.1f} per 512B")
 for o in sorted(out, key=lambda x: -x[0])[:top]:
     print(f"{o[0]/it:7.2f}/512B {o[1]/ts*100:5.1f}%stall {o[2]}:{o[3]:5s} {o[4]}")
+# shared-memory wavefronts per source line (actual vs ideal): what bounds an smem-bound kernel
+wf = []
+for r in csv.reader(io.StringIO(src)):
+    if len(r) == 2 and r[0] == "File Path": fname = r[1].split("/")[-1]
+    if len(r) > 20 and r[0] not in ("", "Line No") and r[2] == "-":
+        try:
+            a, i = float(r[19] or 0), float(r[20] or 0)
+        except ValueError:
+            continue
+        if a: wf.append((a, i, fname, r[0], r[1][:70]))
+ta = sum(w[0] for w in wf) or 1
+print(f"shared wavefronts {ta:.0f} = {ta/it:.1f} per 512B")
+for w in sorted(wf, key=lambda x: -x[0])[:16]:
+    print(f"{w[0]/it:7.2f}/512B (ideal {w[1]/it:6.2f}) {w[2]}:{w[3]:5s} {w[4]}")
