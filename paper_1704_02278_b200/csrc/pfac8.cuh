@@ -112,9 +112,9 @@ __host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur
 template <bool kBits>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
   const uint32_t h = p8_h1<kBits>(g);
-  if (kBits) {
+  if (kBits) {  // bit h & 31 of the word, in bit 0 (bits 1..31: don't care)
     const uint32_t w = reinterpret_cast<const uint32_t*>(dm)[h >> 5];
-    return __funnelshift_r(w, w, h) & 1u;  // bit h & 31
+    return __funnelshift_r(w, w, h);
   }
   return dm[h];
 }
@@ -312,14 +312,20 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         b[1] = p8_dmask<kBits>(s_dmask, p8_gram(vb.y, vb.z));
         b[2] = p8_dmask<kBits>(s_dmask, p8_gram(vb.z, vb.w));
         b[3] = p8_dmask<kBits>(s_dmask, p8_gram(vb.w, nb));
-        mq[2 * hf] = __byte_perm(a[0] | (a[1] << 8), a[2] | (a[3] << 8), 0x5410);
-        mq[2 * hf + 1] = __byte_perm(b[0] | (b[1] << 8), b[2] | (b[3] << 8), 0x5410);
+        if (kBits) {  // byte j = probe j's bit 0
+          mq[2 * hf] = __byte_perm(__byte_perm(a[0], a[1], 0x40), __byte_perm(a[2], a[3], 0x40), 0x5410) & 0x01010101u;
+          mq[2 * hf + 1] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410) & 0x01010101u;
+        } else {
+          mq[2 * hf] = __byte_perm(a[0] | (a[1] << 8), a[2] | (a[3] << 8), 0x5410);
+          mq[2 * hf + 1] = __byte_perm(b[0] | (b[1] << 8), b[2] | (b[3] << 8), 0x5410);
+        }
       }
       if (__ballot_sync(0xffffffffu, (mq[0] | mq[1] | mq[2] | mq[3]) != 0)) {
         // candidate words per quarter (d-masks are < 16: adding 0x7F to a
-        // byte sets its top bit iff the byte is non-zero), packed 8 bits per
-        // quarter (<= 128 each): one shuffle scan gives all four prefixes
-        auto nz = [](uint32_t x) { return __popc((x + 0x7F7F7F7Fu) & 0x80808080u); };
+        // byte sets its top bit iff the byte is non-zero; bit layout: bytes
+        // are 0/1), packed 8 bits per quarter (<= 128 each): one shuffle scan
+        // gives all four prefixes
+        auto nz = [](uint32_t x) { return kBits ? __popc(x) : __popc((x + 0x7F7F7F7Fu) & 0x80808080u); };
         const uint32_t cnt = nz(mq[0]) | (nz(mq[1]) << 8) | (nz(mq[2]) << 16) | (nz(mq[3]) << 24);
         uint32_t incl = cnt;
 #pragma unroll
@@ -337,26 +343,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 #pragma unroll
         for (uint32_t k = 0; k < 4; ++k) {
           uint32_t qa = base + 2 * ((ex >> (8 * k)) & 0xFFu);
-#ifdef GLOP_P8_LOOPQ4
-          // one store per set byte (loop count = the warp's max per lane)
-          uint32_t bits = ((((mq[k] + 0x7F7F7F7Fu) & 0x80808080u) >> 7) * 0x01020408u) >> 24;
-          while (bits) {
-            const uint32_t j = __ffs(bits) - 1;
-            bits &= bits - 1;
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa),
-                         "r"(vl + ((128 * k) << 4) + (j << 4) + (__byte_perm(mq[k], 0, j) & 15u)) : "memory");
-            qa += 2;
-          }
-#else
 #pragma unroll
           for (uint32_t j = 0; j < 4; ++j) {
-            const uint32_t m = mm4[k][j];
+            const uint32_t m = kBits ? (mq[k] >> (8 * j)) & 1u : mm4[k][j];
             if (m) {
               asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(vl + ((128 * k + j) << 4) + m) : "memory");
               qa += 2;
             }
           }
-#endif
           base += 2 * ((tot >> (8 * k)) & 0xFFu);
         }
         qt = (tot & 0xFFu) + ((tot >> 8) & 0xFFu) + ((tot >> 16) & 0xFFu) + (tot >> 24);
