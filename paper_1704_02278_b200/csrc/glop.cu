@@ -109,7 +109,7 @@ struct glop_trie {
   bool u16 = true;
   bool smem_filter = false, smem_direct = false, smem_jump = false;
   bool p8 = false;  // every output at depth >= 8: pfac8_kernel applies
-  bool p8_bits = false;  // pfac8 d-mask layout (see pfac8.cuh)
+  int p8_l1 = 0;  // pfac8 level-1/2 layout (kL1, see pfac8.cuh)
   uint32_t max_pid = 0;
 };
 
@@ -210,11 +210,15 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
   const P8Layout L = make_p8_layout();
   auto* g = c->misc.as<unsigned long long>();
   auto launch = [&](const P8Params& p) -> glop_status {
-    auto k = t->info.max_depth > 8
-                 ? (t->p8_bits ? (t->u16 ? pfac8_kernel<true, true, uint16_t> : pfac8_kernel<true, true, uint32_t>)
-                                 : (t->u16 ? pfac8_kernel<true, false, uint16_t> : pfac8_kernel<true, false, uint32_t>))
-                 : (t->p8_bits ? (t->u16 ? pfac8_kernel<false, true, uint16_t> : pfac8_kernel<false, true, uint32_t>)
-                                 : (t->u16 ? pfac8_kernel<false, false, uint16_t> : pfac8_kernel<false, false, uint32_t>));
+    using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
+    static const KF table[2][3][2] = {
+        {{pfac8_kernel<false, 0, uint16_t>, pfac8_kernel<false, 0, uint32_t>},
+         {pfac8_kernel<false, 1, uint16_t>, pfac8_kernel<false, 1, uint32_t>},
+         {pfac8_kernel<false, 2, uint16_t>, pfac8_kernel<false, 2, uint32_t>}},
+        {{pfac8_kernel<true, 0, uint16_t>, pfac8_kernel<true, 0, uint32_t>},
+         {pfac8_kernel<true, 1, uint16_t>, pfac8_kernel<true, 1, uint32_t>},
+         {pfac8_kernel<true, 2, uint16_t>, pfac8_kernel<true, 2, uint32_t>}}};
+    const KF k = table[t->info.max_depth > 8][t->p8_l1][t->u16 ? 0 : 1];
     CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     CU(cudaEventRecord(c->ev0, c->stream));
     k<<<grid, kP8Threads, L.total, c->stream>>>(t->view, p, L);
@@ -884,7 +888,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
   std::vector<unsigned long long> grams8;  // (p8_gram << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
-  bool bits8 = false;
+  bool bits8 = false, bloom2 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -950,6 +954,15 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         }
       }
     }
+    if (p8) {  // large prefix sets: a second level-2 bit per prefix
+      const char* env = getenv("GLOP_P8_BLOOM2_MIN");  // experiments: override the threshold
+      bloom2 = bits8 && keys.size() > (env ? (size_t)atoll(env) : (size_t)kP8Bloom2Keys);
+      if (bloom2)
+        for (const auto& kv : keys) {
+          const uint32_t bit = prefix_bit2(kv.first);
+          bm2[bit >> 5] |= 1u << (bit & 31);
+        }
+    }
     while ((1ull << cap_log2) < 2 * keys.size()) ++cap_log2;
     jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
     const uint32_t mask = (1u << cap_log2) - 1;
@@ -1004,7 +1017,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
-  t->p8_bits = bits8;
+  t->p8_l1 = bloom2 ? 2 : bits8 ? 1 : 0;
   t->view.jump_depth = J;
   t->view.jump_cap_log2 = cap_log2;
   t->view.jump_bytes = (uint32_t)jump_bytes;

@@ -110,6 +110,12 @@ __host__ __device__ __forceinline__ uint32_t prefix_bit32(uint32_t lo, uint32_t 
 __host__ __device__ __forceinline__ uint32_t prefix_bit(unsigned long long key) {
   return prefix_bit32((uint32_t)key, (uint32_t)(key >> 32));
 }
+// Second level-2 bit of a prefix (PREFIX8 kernel, large prefix sets): the top
+// bits of a remultiplied 32-bit hash, independent of prefix_bit's slice.
+__host__ __device__ __forceinline__ uint32_t prefix_hash2(uint32_t x) { return x * 0x2C1B3C6Du; }
+__host__ __device__ __forceinline__ uint32_t prefix_bit2(unsigned long long key) {
+  return prefix_hash2(prefix_hash32((uint32_t)key, (uint32_t)(key >> 32))) >> (32 - kBm2Log2);
+}
 __host__ __device__ __forceinline__ unsigned long long low_bytes_mask(uint32_t k) {
   return k >= 8 ? ~0ull : ((1ull << (8 * k)) - 1);
 }

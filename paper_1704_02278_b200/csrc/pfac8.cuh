@@ -91,6 +91,9 @@ struct P8Params {
 // k=10,000 6.04 -> 4.03 ms; an intermediate 2^17 x 4-bit layout sat between).
 // The host picks per automaton (glop_trie_upload: bits above kP8BitsGrams).
 constexpr uint32_t kP8BitsGrams = 1024;
+// Above this many 8-byte prefixes the 2^18-bit level-2 bitmap passes too many
+// (word, d) pairs to the exact L2 probe: set and test a second bit per prefix.
+constexpr uint32_t kP8Bloom2Keys = 3000;
 template <bool kBits>
 __host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
   return g >> (32 - kP8DmaskLog2 - (kBits ? 3 : 0));
@@ -170,10 +173,13 @@ __device__ __noinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, u
   return nb;
 }
 
-template <bool kWalk, bool kBits, typename Entry>
+// kL1: 0 byte d-mask buckets; 1 one-bit buckets; 2 one-bit buckets and a
+// second level-2 bitmap probe (prefix_bit2_32) for large prefix sets.
+template <bool kWalk, int kL1, typename Entry>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
+  constexpr bool kBits = kL1 != 0, kB2 = kL1 == 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint8_t* s_dmask = smem + L.dmask;
@@ -385,6 +391,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
                        : "r"(bm2_a + ((x >> (32 - kBm2Log2 + 5)) << 2)), "r"(mm & (1u << (d - 1))));
           // rotate bit (x >> 14) & 31 of the bitmap word to position d - 1
           surv |= __funnelshift_r(word, word, (x >> (32 - kBm2Log2)) + (33 - d)) & (1u << (d - 1));
+          if (kB2) {  // second, independent 18-bit slice of the same key hash
+            const uint32_t x2 = prefix_hash2(x);
+            uint32_t word2 = x2;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.shared.b32 %0, [%1];\n}"
+                         : "+r"(word2)
+                         : "r"(bm2_a + ((x2 >> (32 - kBm2Log2 + 5)) << 2)), "r"(surv & (1u << (d - 1))));
+            surv &= ~(1u << (d - 1)) | __funnelshift_r(word2, word2, (x2 >> (32 - kBm2Log2)) + (33 - d));
+          }
         }
         surv &= mm;
         const uint32_t runmask = __ballot_sync(0xffffffffu, surv != 0);

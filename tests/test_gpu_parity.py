@@ -193,15 +193,17 @@ def test_large_syslog_vs_oracle(ctx, torch_cuda, k):
 
 # level-1 table layouts of the PREFIX8 kernel (pfac8.cuh): the host picks
 # one-byte d-mask buckets or one-bit buckets by gram count; force each
-P8_LAYOUTS = {"auto": None, "bytes": "1000000000", "bits": "0"}
+P8_LAYOUTS = {"auto": {}, "bytes": {"GLOP_P8_BITS_MIN": "1000000000"},
+              "bits": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "1000000000"},
+              "bits+bloom2": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "0"}}
 
 
 @pytest.mark.parametrize("layout", list(P8_LAYOUTS))
 def test_prefix8_shards_and_dense(ctx, torch_cuda, layout, monkeypatch):
     """PREFIX8 kernel: shards with halo == whole == oracle; colliding
     prefixes (several ids per state); a hit-dense text (exact fallback)."""
-    if P8_LAYOUTS[layout] is not None:
-        monkeypatch.setenv("GLOP_P8_BITS_MIN", P8_LAYOUTS[layout])
+    for k, v in P8_LAYOUTS[layout].items():
+        monkeypatch.setenv(k, v)
     text = glop.gen_syslog_host(6 << 20, seed=31)
     pats, _ = glop.gen_rules(300, seed=5)
     pats += [b"Failed password", b"Failed passwd", b"<38>1 2026-", b"\n<38>1 20"]
@@ -440,14 +442,14 @@ def test_kmp_shards_equal_whole(ctx, torch_cuda):
             assert cmp_total == r_cmp, (p, shards)
 
 
-@pytest.mark.parametrize("layout", ["auto", "bits"])
+@pytest.mark.parametrize("layout", ["auto", "bits", "bits+bloom2"])
 def test_prefix8_small_and_ragged(ctx, torch_cuda, layout, monkeypatch):
     """PREFIX8 on the edge cases the big inputs do not reach: texts of 0..5000
     bytes (< 8, one tile, a tile + a few bytes), unaligned starts, shards
     with tiny owned ranges, full-byte alphabets, prefixes colliding on their
     first 8 bytes, patterns longer than the prefix (the deeper trie walk)."""
-    if P8_LAYOUTS[layout] is not None:
-        monkeypatch.setenv("GLOP_P8_BITS_MIN", P8_LAYOUTS[layout])
+    for k, v in P8_LAYOUTS[layout].items():
+        monkeypatch.setenv(k, v)
     rng = np.random.default_rng(2024)
     for trial in range(120):
         alpha = 4 if trial % 3 == 0 else 256
