@@ -9,7 +9,7 @@ tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 3000 gpurun_out/bench.json
 timeout 600 python bench.py --config kmp > gpurun_out/bench_kmp.json 2> gpurun_out/bench_kmp.err; tail -c 1500 gpurun_out/bench_kmp.json
-timeout 300 python bench.py --patterns 10 --no-cpu --no-e2e > gpurun_out/bench_k10.json 2>&1; tail -c 1200 gpurun_out/bench_k10.json
+timeout 300 python bench.py --patterns 10 --no-cpu --no-e2e --no-sweep > gpurun_out/bench_k10.json 2>&1; tail -c 1200 gpurun_out/bench_k10.json
 timeout 600 python bench.py --config dpi > gpurun_out/bench_dpi.json 2>&1; tail -c 1500 gpurun_out/bench_dpi.json
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2>&1; tail -c 800 gpurun_out/bench_ref.json
 if [ "${PROFILE:-1}" = 1 ]; then
