@@ -159,7 +159,9 @@ __device__ __noinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, u
     }
     return 0;
   }
-  warp_sort_keys(hk, nb, lane);
+  // batches are usually already in text order (a lane emits its candidates
+  // in ascending offset, rounds and tiles ascend): sort only when needed
+  if (!__all_sync(0xffffffffu, lane + 1 >= nb || hk[lane] < hk[lane + 1])) warp_sort_keys(hk, nb, lane);
   if (dst)
     for (uint32_t h = lane; h < nb; h += 32) {
       const unsigned long long key = hk[h];
@@ -413,8 +415,8 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           if ((mask >> lane) & 1u) {
             uint32_t sv = surv;
             while (sv) {
-              const uint32_t d = __ffs(sv);  // 1..4
-              sv &= sv - 1;
+              const uint32_t d = 32 - __clz(sv);  // 4..1: ascending candidate offsets
+              sv &= ~(1u << (d - 1));
               const uint32_t sh = 32 - 8 * d;
               exact(4 * i - d, __funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh));
             }
