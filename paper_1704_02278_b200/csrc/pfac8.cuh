@@ -168,7 +168,7 @@ __device__ __noinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, u
       DevHit out;
       out.offset = key >> 24;
       out.pid = (uint32_t)key & 0xFFFFFFu;
-      out.len = __ldg(pid_len + out.pid);
+      out.len = pid_len ? __ldg(pid_len + out.pid) : 8u;  // nullptr: every output at depth 8
       dst[h] = out;
     }
   __syncwarp();
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 
   auto flush = [&](uint32_t nb) {
     const bool fits = cursor + nb <= p.region;
-    cursor += p8_flush(hk, nb, lane, fits ? region + cursor : nullptr, tr.pid_len, p.g_count);
+    cursor += p8_flush(hk, nb, lane, fits ? region + cursor : nullptr, kWalk ? tr.pid_len : nullptr, p.g_count);
     if (lane == 0) *s_nh = 0;
     __syncwarp();
   };
@@ -337,10 +337,13 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         const uint32_t cnt = nz(mq[0]) | (nz(mq[1]) << 8) | (nz(mq[2]) << 16) | (nz(mq[3]) << 24);
         uint32_t incl = cnt;
 #pragma unroll
-        for (uint32_t o = 1; o < 32; o <<= 1) {
-          const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += x;
-        }
+        for (uint32_t o = 1; o < 32; o <<= 1)  // the shuffle's own in-range predicate guards the add
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t.reg .b32 x;\n\t"
+              "shfl.sync.up.b32 x|p, %0, %1, 0, 0xffffffff;\n\t"
+              "@p add.u32 %0, %0, x;\n}"
+              : "+r"(incl)
+              : "r"(o));
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t ex = incl - cnt;
         // 16 predicated u16 stores through a running shared-memory address
@@ -353,8 +356,8 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           uint32_t qa = base + 2 * ((ex >> (8 * k)) & 0xFFu);
 #pragma unroll
           for (uint32_t j = 0; j < 4; ++j) {
-            const uint32_t m = kBits ? (mq[k] >> (8 * j)) & 1u : mm4[k][j];
-            if (m) {
+            if (kBits ? (mq[k] & (1u << (8 * j))) != 0 : mm4[k][j] != 0) {
+              const uint32_t m = kBits ? 1u : mm4[k][j];
               asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa), "r"(vl + ((128 * k + j) << 4) + m) : "memory");
               qa += 2;
             }
