@@ -33,13 +33,19 @@
 
 namespace glop {
 
-constexpr int kP8Warps = 24;
+#ifndef GLOP_P8_WARPS
+#define GLOP_P8_WARPS 24
+#endif
+#ifndef GLOP_P8_DMASK_LOG2
+#define GLOP_P8_DMASK_LOG2 16
+#endif
+constexpr int kP8Warps = GLOP_P8_WARPS;
 constexpr int kP8Threads = kP8Warps * 32;
 constexpr uint32_t kP8Tile = 2048;                 // owned starts per tile (TMA unit)
 constexpr uint32_t kP8Stage = kP8Tile + 16;        // + the 4 words after the tile (halo)
 constexpr uint32_t kP8Queue = kP8Tile / 4;         // candidate words of one tile, worst case (u16)
 constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
-constexpr uint32_t kP8DmaskLog2 = 16;
+constexpr uint32_t kP8DmaskLog2 = GLOP_P8_DMASK_LOG2;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
 
 struct P8Layout {
