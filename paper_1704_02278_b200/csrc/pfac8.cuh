@@ -15,17 +15,20 @@
 //    conflict-free LDS.128 per quarter (consecutive lanes, consecutive 16 B:
 //    the earlier 8-consecutive-words layout was a 2-way bank conflict, and
 //    shared-memory wavefronts bound this kernel); each word gets one hashed
-//    d-mask probe.
+//    probe of a 64 KB table: d-mask bytes for small gram sets, single bits
+//    (2^19 buckets) above kP8BitsGrams.
 //  * Candidate words are compacted in text order into a u16 queue (one
 //    packed shuffle scan gives all four quarters' prefixes) and checked 32 per
 //    round: the 8-byte key of candidate c = 4i - d is assembled from words
 //    i-1, i, i+1 with constant funnel shifts and tested in a 2^18-bit prefix
-//    bitmap.
+//    bitmap (one bit per prefix; two above kP8Bloom2Keys prefixes).
 //  * Bitmap survivors probe the exact J=8 jump table (generalised RootJump,
 //    scan.hpp:81-108) in global memory (L2-resident) and, for patterns longer
 //    than 8 bytes, continue the trie walk (scan.hpp:142-168).
 //  * Hits are buffered as (offset, id) keys in shared memory and flushed in
-//    sorted batches; a round that overflows the buffer is replayed lane by
+//    sorted batches (a lane emits its candidates in ascending offset, so a
+//    batch is usually in order already and the warp sort is skipped); a
+//    round that overflows the buffer is replayed lane by
 //    lane, and a single lane that overflows it flags the exact global-key
 //    fallback (radix sort), so any hit density is handled exactly.
 #pragma once
