@@ -509,3 +509,25 @@ def test_pipeline_shards_1_2_4_8(ctx, torch_cuda, world):
         s1 += h
     assert np.concatenate(alerts).tobytes() == whole[0].tobytes()
     assert np.array_equal(counts, whole[1]) and s1 == whole[2]
+
+
+@pytest.mark.parametrize("layout", list(P8_LAYOUTS))
+def test_prefix8_hit_density_sweep(ctx, torch_cuda, layout, monkeypatch):
+    """PREFIX8 over 4-letter texts where most 8-byte windows are patterns:
+    hit densities from sparse to several per word, several ids per prefix,
+    so the hit buffer's in-order batches, the out-of-order sort, the
+    overflow replay and the staging-region growth all run -- each result
+    bit-exact with the oracle."""
+    for k, v in P8_LAYOUTS[layout].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(77)
+    for trial, (n, k) in enumerate([(1 << 20, 50), (1 << 20, 2000), (3 << 19, 20000)]):
+        text = (rng.integers(0, 4, n) + 65).astype(np.uint8)
+        starts = rng.integers(0, n - 16, k)
+        pats = [text[s:s + int(rng.integers(8, 13))].tobytes() for s in starts]
+        pats += [p[:8] + b"Z" for p in pats[:k // 4]]  # colliding 8-byte prefixes
+        pats = list(dict.fromkeys(pats))
+        trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+        ref = O.pfac_scan(text, O.Trie(pats, 8))
+        got = dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_PREFIX8)
+        assert got.tobytes() == ref.tobytes(), (layout, trial, len(got), len(ref))
