@@ -134,12 +134,12 @@ __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
 // valid range [a, a + n)) into dst; bytes outside 16-byte granules are copied
 // by the issuing lane.  One arrival (with tx bytes) on bar.
-__device__ __forceinline__ void p8_issue(uint8_t* dst, uint64_t* bar, const uint8_t* A, uint32_t a,
+__device__ __forceinline__ void p8_issue(uint8_t* dst, uint32_t dst_a, uint32_t bar_a, const uint8_t* A, uint32_t a,
                                          unsigned long long n, unsigned long long lo) {
   const unsigned long long hi = lo + kP8Stage;
   if (lo >= a && hi <= a + n) {  // interior: one copy
-    mbar_arrive_tx(bar, kP8Stage);
-    bulk_g2s(dst, A + lo, kP8Stage, bar);
+    mbar_arrive_tx_a(bar_a, kP8Stage);
+    bulk_g2s_a(dst_a, A + lo, kP8Stage, bar_a);
     return;
   }
   const unsigned long long vlo = lo > a ? lo : a, vhi = hi < a + n ? hi : a + n;
@@ -148,10 +148,10 @@ __device__ __forceinline__ void p8_issue(uint8_t* dst, uint64_t* bar, const uint
   for (unsigned long long x = vlo; x < tlo && x < vhi; ++x) dst[x - lo] = A[x];
   for (unsigned long long x = thi > vlo ? thi : vlo; x < vhi; ++x) dst[x - lo] = A[x];
   if (thi > tlo) {
-    mbar_arrive_tx(bar, (uint32_t)(thi - tlo));
-    bulk_g2s(dst + (tlo - lo), A + tlo, (uint32_t)(thi - tlo), bar);
+    mbar_arrive_tx_a(bar_a, (uint32_t)(thi - tlo));
+    bulk_g2s_a(dst_a + (uint32_t)(tlo - lo), A + tlo, (uint32_t)(thi - tlo), bar_a);
   } else {
-    mbar_arrive(bar);
+    mbar_arrive_a(bar_a);
   }
 }
 
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   const uint8_t* s_cls = smem + L.cls;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars) + warp * 2;
   uint8_t* bufs = smem + L.bufs + (size_t)warp * 2 * kP8Stage;
+  const uint32_t bufs_a = smem_u32(bufs), bars_a = smem_u32(bars);  // shared-window addresses
   uint16_t* q = reinterpret_cast<uint16_t*>(smem + L.queue) + warp * kP8Queue;
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.hits) + warp * kP8Hits;
   uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.nh) + warp;
@@ -223,7 +224,9 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   const uint8_t* A = p.text - a;
   if (lane == 0)
     for (uint32_t b = 0; b < 2; ++b)
-      if (t0 + b < t1) p8_issue(bufs + b * kP8Stage, &bars[b], A, a, p.n, (unsigned long long)(t0 + b) * kP8Tile);
+      if (t0 + b < t1)
+        p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
+                 (unsigned long long)(t0 + b) * kP8Tile);
   const unsigned long long own_end = p.own + a, n_end = p.n + a;  // aligned coordinates
   // interior tiles: t >= 1, all kP8Tile starts owned, the whole stage inside
   // the text -- no range masks
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 
   for (uint32_t t = t0, k = 0; t < t1; ++t, ++k) {
     const uint32_t b = k & 1;
-    mbar_wait(&bars[b], (k >> 1) & 1);
+    mbar_wait_a(bars_a + 8 * b, (k >> 1) & 1);
     const uint8_t* sb = bufs + b * kP8Stage;
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
     const unsigned long long tA = (unsigned long long)t * kP8Tile;
@@ -456,7 +459,8 @@ __global__ void __launch_bounds__(kP8Threads, 1)
     __syncwarp();
     if (lane == 0 && t + 2 < t1) {
       fence_proxy_async();
-      p8_issue(bufs + b * kP8Stage, &bars[b], A, a, p.n, (unsigned long long)(t + 2) * kP8Tile);
+      p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
+               (unsigned long long)(t + 2) * kP8Tile);
     }
   }
   if (p.mode == 0) {
