@@ -49,10 +49,11 @@ constexpr uint32_t kP8Stage = kP8Tile + 16;        // + the 4 words after the ti
 constexpr uint32_t kP8Queue = kP8Tile / 4;         // candidate words of one tile, worst case (u16)
 constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 // Flush the hit buffer once a round leaves more keys than this (a later round
-// that overflows the remaining slots is replayed lane by lane).  24 of 32:
-// DPI 2.06 -> 1.84 ms against 16, k=1,000 unchanged.
+// that overflows the remaining slots is replayed lane by lane; a single lane
+// overflowing them takes the exact global-key fallback).  Higher thresholds
+// send DPI lanes with several ids per prefix to that fallback.
 #ifndef GLOP_P8_FLUSH_AT
-#define GLOP_P8_FLUSH_AT 24
+#define GLOP_P8_FLUSH_AT 16
 #endif
 constexpr uint32_t kP8DmaskLog2 = GLOP_P8_DMASK_LOG2;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
@@ -165,7 +166,7 @@ __device__ __forceinline__ void p8_issue(uint8_t* dst, uint32_t dst_a, uint32_t 
 // and writes them as hits to dst (nullptr: the warp's staging region is full;
 // the host grows it and reruns).  nb > kP8Hits means keys were dropped: the
 // scan is flagged for the exact global-key fallback.  Whole warp.
-// (inlined: as a real call it cost 5% at k=1,000 and 7% on the DPI set)
+// (inlined: as a real call it cost 5% at k=1,000 and 6% on the DPI set)
 __device__ __forceinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb, uint32_t lane, DevHit* dst,
                                           const uint32_t* pid_len, unsigned long long* g_count) {
   if (nb > kP8Hits) {
