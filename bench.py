@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the Gbps-vs-pattern-count sweep (pfac, N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline work")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size result digests")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the configs[0]/[1]/[4] sub-blocks of the default line")
     a = ap.parse_args()
     if a.bytes_per_gpu is None:
         a.bytes_per_gpu = {"pfac": 8e9, "kmp": 1e9, "dpi": 4e9}[a.config]
@@ -172,56 +175,138 @@ def cpu_baseline_pfac(text_host, pats, L, target_s):
 
 
 # --------------------------------------------------------------------- reference arm
+# Sub-configurations carried by the default (configs[2]) line besides its
+# headline: BASELINE.json configs[0], [1] and configs[4]'s per-GPU shard.
+SUB_CONFIGS = [
+    {"config": "configs[0]", "kind": "pfac", "corpus": "syslog", "bytes": 256_000_000, "patterns": 10,
+     "workload": "PFAC, 10 patterns (8-byte prefixes), 256 MB synthetic RFC 5424 syslog"},
+    {"config": "configs[1]", "kind": "kmp", "corpus": "syslog", "bytes": 1_000_000_000, "patterns": 1,
+     "workload": "KMP single pattern 'Failed password' over 1 GB synthetic syslog"},
+    {"config": "configs[4]", "kind": "pfac", "corpus": "payload", "bytes": 4_000_000_000, "patterns": 10000,
+     "workload": "DPI: PFAC, 10,000 Snort-style contents (8..24 B) over one GPU's 4 GB payload shard "
+                 "(32 GB over 8 GPUs)"},
+]
+KMP_PATTERN = b"Failed password"
+
+
+def ref_rules(args, O, corpus=None, k=None):
+    """The config's pattern set and host text generator, from oracle/_ref (the
+    reference arm never maps libglop.so)."""
+    corpus = corpus or ("payload" if args.config == "dpi" else "syslog")
+    k = k or args.patterns
+    if corpus == "payload":
+        return O.ref_gen_dpi_rules(k, args.rules_seed, 8, 24), O.ref_gen_payload
+    return O.ref_gen_rules(k, args.rules_seed), O.ref_gen_syslog
+
+
+def ref_parity_pfac(O, text, own, pats, L):
+    """Digest of the reference pfac_scan + verify_hits over text (starts
+    < own reported, the shard ownership rule of scan.hpp:230-232)."""
+    from paper_1704_02278_b200.parity import digest
+
+    if O.ref() is not None:
+        hits, alerts = O.ref_pfac_verify(text, pats, L, compact=True, workers=0)
+    else:
+        hits, alerts = O.pfac_verify(text, pats, L)
+    hits, alerts = hits[hits["offset"] < own], alerts[alerts["offset"] < own]
+    return digest(hits, alerts, len(pats))
+
+
+def ref_parity_kmp(O, text):
+    from paper_1704_02278_b200.parity import offsets_digest
+
+    offs, cmp_ = O.kmp_search(text, KMP_PATTERN) if O.ref() is None else ref_kmp(O, text)
+    return offsets_digest(offs, cmp_)
+
+
+def ref_kmp(O, text):
+    import ctypes as C
+
+    import numpy as np
+
+    r = O.ref()
+    op, no, rc = C.c_void_p(), C.c_uint64(), C.c_uint64()
+    pa = np.frombuffer(KMP_PATTERN, np.uint8).copy()
+    r.ref_kmp_search(text.ctypes.data_as(O.u8p), len(text), pa.ctypes.data_as(O.u8p), len(pa), C.byref(op),
+                     C.byref(no), C.byref(rc))
+    return O._take(op, no.value, np.uint64, r.ref_free), rc.value
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import numpy as np
-
     import oracle_ffi as O
-    from paper_1704_02278_b200 import glop
+
+    from paper_1704_02278_b200.shards import plan_shards  # pure Python
 
     ref = O.ref()
     kind = "reference" if ref is not None else "port"
     budget = 120.0  # seconds for warmup + steps
+    S = int(args.bytes_per_gpu)
     if args.config == "kmp":
-        p = b"Failed password"
-        probe = glop.gen_syslog_host(64 << 20, args.seed)
+        p = KMP_PATTERN
+        probe = O.ref_gen_syslog(64 << 20, args.seed)
         secs, _ = (O.ref_time_kmp(probe, p, 0, 1) if ref is not None else ([time.perf_counter()], 0))
         per_byte = max(secs[0], 1e-6) / probe.size
-        sample = int(min(args.bytes_per_gpu, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
-        text = glop.gen_syslog_host(sample, args.seed)
+        sample = int(min(S, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
+        full = O.ref_gen_syslog(S, args.seed)
+        text = full[:sample]
         secs, nm = O.ref_time_kmp(text, p, args.warmup, args.steps)
         cores, metric = 1, KMP_METRIC
-        config = {"workload": "configs[1]: KMP 'Failed password' over synthetic RFC 5424 syslog",
-                  "bytes": int(args.bytes_per_gpu), "sample_bytes": sample}
+        config = {"workload": "configs[1]: KMP single pattern 'Failed password' over 1 GB synthetic syslog",
+                  "bytes_per_gpu": S, "l2": "inputs larger than L2"}
         desc = f"kmp_multi (kmp.hpp:74) single-threaded by design on the first {sample} bytes"
+        parity = ref_parity_kmp(O, full) if not args.no_parity else None
     else:
-        pats, gen_host, _ = workload_rules(args, glop)
+        pats, gen_host = ref_rules(args, O)
         probe = gen_host(64 << 20, args.seed)
         timer = O.ref_time_pfac if ref is not None else (lambda t, q, l, w, r: O.port_time_pfac(t, q, l, w, r))
         secs, _ = timer(probe, pats, args.prefix_len, 0, 1)
         per_byte = max(secs[0], 1e-6) / probe.size
-        sample = int(min(args.bytes_per_gpu, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
-        text = gen_host(sample, args.seed)
+        sample = int(min(S, max(probe.size, budget / (args.warmup + args.steps) / per_byte)))
+        halo = max(len(q) for q in pats) - 1
+        sh = plan_shards(S * args.gpus, args.gpus, max(halo, args.prefix_len - 1))[0]
+        full = gen_host(sh.read, args.seed)  # rank 0's shard (the whole text at N = 1)
+        text = full[:sample]
         secs, na = timer(text, pats, args.prefix_len, args.warmup, args.steps)
         cores = int(ref.ref_default_workers()) if ref is not None else 1
         metric = METRIC
-        config = workload_config(args, 1)
-        config["sample_bytes"] = sample
+        config = workload_config(args, args.gpus)
         desc = (f"reference pfac_scan + verify_hits (oracle/_ref built from /root/reference), workers={cores}, "
                 f"on the first {sample} bytes of the same corpus and rules")
+        parity = ref_parity_pfac(O, full, sh.own, pats, args.prefix_len) if not args.no_parity else None
+    del full, text
     mean = statistics.mean(secs)
     value = 8 * sample / mean / 1e9
     line = {"impl": "reference", "metric": metric, "value": round(value, 3), "unit": "Gbps", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic RFC 5424 syslog (csrc/corpus.h)", "config": config,
-            "cpu_baseline": {"value": round(value, 3), "unit": "Gbps", "cores": cores, "kind": kind, "sample": desc},
+            "data": "synthetic RFC 5424 syslog (csrc/corpus.h)" if args.config != "dpi" else
+                    "synthetic packet payloads (csrc/payload.h)", "config": config,
+            "cpu_baseline": {"value": round(value, 3), "unit": "Gbps", "cores": cores, "kind": kind, "sample": desc,
+                             "sample_bytes": sample, "cpu_model": O.cpu_model()},
             "e2e": {"value": round(value, 3), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if parity is not None:
+        parity["scope"] = f"rank 0's shard: starts [0, {S}) of the config's text, full size (untimed)"
+        line["parity"] = parity
+    if args.config == "pfac" and not args.no_configs and not args.no_parity:
+        line["configs"] = [dict(c0, parity=ref_sub_parity(args, O, c0)) for c0 in
+                           ({"config": c["config"], "workload": c["workload"], "bytes": c["bytes"]}
+                            for c in SUB_CONFIGS)]
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ref_sub_parity(args, O, cfg):
+    c = next(x for x in SUB_CONFIGS if x["config"] == cfg["config"])
+    gen = O.ref_gen_payload if c["corpus"] == "payload" else O.ref_gen_syslog
+    text = gen(c["bytes"], args.seed)
+    if c["kind"] == "kmp":
+        return ref_parity_kmp(O, text)
+    pats, _ = ref_rules(args, O, c["corpus"], c["patterns"])
+    return ref_parity_pfac(O, text, c["bytes"], pats, args.prefix_len)
 
 
 def workload_config(args, world):
@@ -370,8 +455,18 @@ def main():
                                  "table_in_smem": bool(info.table_in_smem)}}}
     if e2e is not None:
         line["e2e"] = e2e
+    if not args.no_parity:  # rank 0's full-size result, for the driver to compare with the reference arm
+        from paper_1704_02278_b200.parity import digest
+
+        hits = d_hits[: nh * 16].cpu().numpy().view(glop.HIT_DTYPE)
+        alerts = d_alerts[: na * 16].cpu().numpy().view(glop.ALERT_DTYPE)
+        line["parity"] = dict(digest(hits, alerts, args.patterns),
+                              scope=f"rank 0's shard: starts [0, {S}) of the config's text, full size (untimed)")
     if world == 1 and args.config == "pfac" and not args.no_sweep:
         line["pattern_sweep"] = pattern_sweep(args, ctx, glop, d_text, sh, d_hits, cap, peak)
+    if world == 1 and args.config == "pfac" and not args.no_configs:
+        line["configs"] = [sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak)
+                           for c in SUB_CONFIGS]
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(sh.own, 2 << 30)
         host = d_text[:sample].cpu().numpy()
@@ -400,6 +495,69 @@ def pattern_sweep(args, ctx, glop, d_text, sh, d_hits, cap, peak):
         gbs = sh.own / (ms / 1e3) / 1e9
         out.append({"patterns": k, "kernel_ms": round(ms, 4), "gbps": round(8 * gbs, 1), "hbm_frac": round(gbs / peak, 4),
                     "hits": int(nh), "vocab_rules": int(vocab.sum()), "trie_states": trie.info.state_count})
+    return out
+
+
+def sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak):
+    """One of BASELINE.json's other configs on this GPU, device-resident:
+    3 warm-ups + min(steps, 10) timed steps (CUDA events on the library
+    stream), the dominant kernel's mean time, and the full-size result digest."""
+    import torch
+
+    from paper_1704_02278_b200.parity import digest, offsets_digest
+
+    n = c["bytes"]
+    gen = ctx.gen_payload_device if c["corpus"] == "payload" else ctx.gen_syslog_device
+    gen(d_text.data_ptr(), n, args.seed)
+    ctx.synchronize()
+    steps = max(1, min(args.steps, 10))
+    if c["kind"] == "kmp":
+        kcap = min(cap * 2, 1 << 24)
+
+        def step():
+            return ctx.kmp_search_device(KMP_PATTERN, d_text.data_ptr(), n, d_hits.data_ptr(), kcap)
+        kname = "kmp3_kernel"
+    else:
+        pats = glop.gen_dpi_rules(c["patterns"], args.rules_seed, 8, 24) if c["corpus"] == "payload" else \
+            glop.gen_rules(c["patterns"], args.rules_seed)[0]
+        trie = ctx.upload(glop.build_failureless_trie(pats, args.prefix_len))
+        rules = ctx.upload_rules(pats, args.prefix_len)
+        d_counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+
+        def step():
+            with torch.cuda.stream(stream):
+                d_counts.zero_()
+            nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), n, d_hits.data_ptr(), cap)
+            na = ctx.verify_hits_device(rules, d_text.data_ptr(), n, d_hits.data_ptr(), nh, d_alerts.data_ptr(),
+                                        d_counts.data_ptr())
+            return nh, na
+        kname = "pfac8_kernel" if trie.info.min_depth >= 8 else "pfac_warp_kernel"
+    for _ in range(3):
+        r = step()
+    ctx.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    kms = []
+    for _ in range(steps):
+        r = step()
+        kms.append(ctx.last_kernel_ms())
+    ev1.record(stream)
+    ctx.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    kernel_ms = statistics.mean(kms)
+    gbs = n / (kernel_ms / 1e3) / 1e9
+    out = {"config": c["config"], "workload": c["workload"], "bytes": n, "steps": steps, "kernel": kname,
+           "kernel_ms": round(kernel_ms, 4), "ms_per_step": round(ms, 4), "gbps": round(8 * n / (ms / 1e3) / 1e9, 1),
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(gbs / peak, 4)}}
+    if not args.no_parity:
+        if c["kind"] == "kmp":
+            nm, cmp_ = r
+            out["parity"] = offsets_digest(d_hits[: nm * 8].cpu().numpy().view("<u8"), cmp_)
+        else:
+            nh, na = r
+            out["parity"] = digest(d_hits[: nh * 16].cpu().numpy().view(glop.HIT_DTYPE),
+                                   d_alerts[: na * 16].cpu().numpy().view(glop.ALERT_DTYPE), len(pats))
     return out
 
 

@@ -7,6 +7,7 @@
 // ("kind": "reference") in bench.py: the timed call is the reference's own
 // measure() harness (bench.hpp:64-113) over pfac_scan + verify_hits.
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +17,7 @@
 #include "logtrawl/bench.hpp"
 #include "logtrawl/kmp.hpp"
 #include "logtrawl/pipeline.hpp"
+#include "workload.hpp"  // synthetic inputs (paper_1704_02278_b200/csrc), not the matching path
 
 using namespace logtrawl;
 
@@ -160,6 +162,58 @@ int ref_kmp_search(const uint8_t* text, uint64_t n, const uint8_t* p, uint32_t m
 }
 
 unsigned ref_default_workers(void) { return default_workers(); }
+
+// ---- synthetic workloads for the reference arm, so it never maps the
+// product library (the same header-only generators libglop exports).
+int ref_gen_syslog(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads) {
+  glop_workload::gen_syslog(out, begin, n, seed, threads);
+  return 0;
+}
+int ref_gen_payload(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads) {
+  glop_workload::gen_payload(out, begin, n, seed, threads);
+  return 0;
+}
+int ref_gen_rules(uint32_t k, uint32_t seed, uint32_t len, uint8_t* bytes, uint8_t* is_vocab) {
+  auto rules = glop_workload::synthetic_rules(k, seed, len);
+  for (uint32_t i = 0; i < k; ++i) {
+    memcpy(bytes + (size_t)i * len, rules[i].bytes.data(), len);
+    if (is_vocab) is_vocab[i] = rules[i].name.rfind("vocab-", 0) == 0;
+  }
+  return 0;
+}
+int ref_gen_dpi_rules(uint32_t k, uint32_t seed, uint32_t min_len, uint32_t max_len, uint8_t* bytes,
+                      uint64_t* off) {
+  const auto rules = glop_workload::dpi_rules(k, seed, min_len, max_len);
+  uint64_t o = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    off[i] = o;
+    memcpy(bytes + o, rules[i].data(), rules[i].size());
+    o += rules[i].size();
+  }
+  off[k] = o;
+  return 0;
+}
+
+// The CPU model of this host (cpu_baseline), from /proc/cpuinfo.
+int ref_cpu_model(char* out, uint64_t cap) {
+  std::string model = "unknown";
+  if (FILE* f = fopen("/proc/cpuinfo", "r")) {
+    char line[512];
+    while (fgets(line, sizeof line, f))
+      if (!strncmp(line, "model name", 10)) {
+        const char* c = strchr(line, ':');
+        if (c) {
+          model = c + 1;
+          while (!model.empty() && (model.front() == ' ' || model.front() == '\t')) model.erase(0, 1);
+          while (!model.empty() && (model.back() == '\n' || model.back() == ' ')) model.pop_back();
+        }
+        break;
+      }
+    fclose(f);
+  }
+  snprintf(out, cap, "%s", model.c_str());
+  return 0;
+}
 
 void ref_free(void* p) { free(p); }
 }

@@ -292,3 +292,62 @@ def port_time_pfac(text, patterns, L, warmup=1, runs=3):
         if i >= warmup:
             secs.append(time.perf_counter() - t0)
     return secs, na
+
+
+# ------------------------------------------------------------------ workloads (reference arm)
+# The same header-only generators libglop exports (csrc/workload.hpp), built
+# into oracle/_ref/libref_logtrawl.so so the reference arm of bench.py never
+# maps the product library.
+def _ref_gen():
+    r = ref()
+    if r is None:
+        raise RuntimeError("reference shim not built")
+    if not getattr(r, "_gen_sigs", False):
+        r.ref_gen_syslog.argtypes = [u8p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint]
+        r.ref_gen_payload.argtypes = [u8p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint]
+        r.ref_gen_rules.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, u8p, u8p]
+        r.ref_gen_dpi_rules.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u8p, u64p]
+        r.ref_cpu_model.argtypes = [C.c_char_p, C.c_uint64]
+        r._gen_sigs = True
+    return r
+
+
+def ref_gen_syslog(n: int, seed: int, begin: int = 0, threads: int = 0) -> np.ndarray:
+    out = np.empty(max(n, 1), dtype=np.uint8)
+    _ref_gen().ref_gen_syslog(out.ctypes.data_as(u8p), begin, n, seed, threads)
+    return out[:n]
+
+
+def ref_gen_payload(n: int, seed: int, begin: int = 0, threads: int = 0) -> np.ndarray:
+    out = np.empty(max(n, 1), dtype=np.uint8)
+    _ref_gen().ref_gen_payload(out.ctypes.data_as(u8p), begin, n, seed, threads)
+    return out[:n]
+
+
+def ref_gen_rules(k: int, seed: int, length: int = 8) -> list[bytes]:
+    b = np.zeros(max(k * length, 1), dtype=np.uint8)
+    _ref_gen().ref_gen_rules(k, seed, length, b.ctypes.data_as(u8p), None)
+    return [bytes(b[i * length:(i + 1) * length]) for i in range(k)]
+
+
+def ref_gen_dpi_rules(k: int, seed: int, min_len: int = 8, max_len: int = 24) -> list[bytes]:
+    b = np.zeros(max(k * max_len, 1), dtype=np.uint8)
+    off = np.zeros(k + 1, dtype=np.uint64)
+    _ref_gen().ref_gen_dpi_rules(k, seed, min_len, max_len, b.ctypes.data_as(u8p), off.ctypes.data_as(u64p))
+    return [bytes(b[int(off[i]):int(off[i + 1])]) for i in range(k)]
+
+
+def cpu_model() -> str:
+    r = ref()
+    if r is not None:
+        buf = C.create_string_buffer(256)
+        _ref_gen().ref_cpu_model(buf, 256)
+        return buf.value.decode(errors="replace")
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

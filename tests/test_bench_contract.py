@@ -46,3 +46,16 @@ def test_reference_arm_line(config):
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+@pytest.mark.skipif(not os.path.exists(REF_LIB), reason="oracle/_ref not built (build() compiles it)")
+def test_reference_arm_never_maps_libglop():
+    """The reference arm generates its corpus and rules through oracle/_ref:
+    with GLOP_LIB pointing nowhere, importing the product binding would fail."""
+    env = dict(os.environ, GLOP_LIB="/nonexistent/libglop.so")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                          "--bytes-per-gpu", "1e6", "--no-configs"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["parity"]["sha"] and d["cpu_baseline"]["cpu_model"]
