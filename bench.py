@@ -7,7 +7,9 @@ Workload (configs[2] / configs[3] of BASELINE.json): synthetic RFC 5424 syslog,
 8e9 bytes per GPU (weak scaling; 64e9 at 8 GPUs), 1,000 8-byte patterns
 (half reference random_rules, half incident vocabulary), prefix L = 8.
 A step = one pass of the hot path over the GPU's shard: device PFAC scan +
-stage-2 verify + per-pattern counts (+ the NCCL count all-reduce at N > 1).
+ordering + stage-2 verify + per-pattern counts, through the fused device
+pipeline (glop_run_pfac_pipeline_device: one host wait per step), plus the
+NCCL count all-reduce and alert gather at N > 1.
 `value` has the text already in HBM; `e2e` goes through the public pipeline
 call with the text in pinned HOST memory (H2D + scan + verify + D2H of alerts
 inside the timed region).  The 8 GB shard is larger than L2, so no flush.
@@ -388,12 +390,16 @@ def main():
     d_counts = torch.zeros(args.patterns, dtype=torch.int64, device="cuda")
 
     def step():
-        with torch.cuda.stream(stream):
-            d_counts.zero_()
-        nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), sh.read, d_hits.data_ptr(), cap, own=sh.own,
-                                  base=sh.lo, kernel=kernel)
-        na = ctx.verify_hits_device(rules, d_text.data_ptr(), sh.read, d_hits.data_ptr(), nh, d_alerts.data_ptr(),
-                                    d_counts.data_ptr(), base=sh.lo)
+        if kernel == glop.PFAC_AUTO:  # the fused device pipeline: one host wait per step
+            nh, na = ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), sh.read, d_alerts.data_ptr(), cap,
+                                                  d_counts.data_ptr(), own=sh.own, base=sh.lo)
+        else:
+            with torch.cuda.stream(stream):
+                d_counts.zero_()
+            nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), sh.read, d_hits.data_ptr(), cap, own=sh.own,
+                                      base=sh.lo, kernel=kernel)
+            na = ctx.verify_hits_device(rules, d_text.data_ptr(), sh.read, d_hits.data_ptr(), nh,
+                                        d_alerts.data_ptr(), d_counts.data_ptr(), base=sh.lo)
         if world > 1:  # the one exchange: count all-reduce + alert gather to rank 0 (NCCL over NVLink)
             with torch.cuda.stream(stream):
                 dist.all_reduce(d_counts)
@@ -429,6 +435,8 @@ def main():
         e2e = None
         if not args.no_e2e:
             e2e = run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, torch, dist)
+            if world == 1 and args.config != "kmp":
+                e2e["dropin"] = run_e2e_dropin(args, glop, d_text, sh, pats)
     clocks = sampler.summary()
 
     value = 8 * total / (ms / 1e3) / 1e9
@@ -458,6 +466,9 @@ def main():
     if not args.no_parity:  # rank 0's full-size result, for the driver to compare with the reference arm
         from paper_1704_02278_b200.parity import digest
 
+        nh, na = ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), sh.read, d_alerts.data_ptr(), cap,
+                                              d_counts.data_ptr(), own=sh.own, base=sh.lo, d_hits=d_hits.data_ptr(),
+                                              hit_cap=cap)
         hits = d_hits[: nh * 16].cpu().numpy().view(glop.HIT_DTYPE)
         alerts = d_alerts[: na * 16].cpu().numpy().view(glop.ALERT_DTYPE)
         line["parity"] = dict(digest(hits, alerts, args.patterns),
@@ -525,12 +536,8 @@ def sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak):
         d_counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
 
         def step():
-            with torch.cuda.stream(stream):
-                d_counts.zero_()
-            nh = ctx.pfac_scan_device(trie, d_text.data_ptr(), n, d_hits.data_ptr(), cap)
-            na = ctx.verify_hits_device(rules, d_text.data_ptr(), n, d_hits.data_ptr(), nh, d_alerts.data_ptr(),
-                                        d_counts.data_ptr())
-            return nh, na
+            return ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), n, d_alerts.data_ptr(), cap,
+                                                d_counts.data_ptr())
         kname = "pfac8_kernel" if trie.info.min_depth >= 8 else "pfac_warp_kernel"
     for _ in range(3):
         r = step()
@@ -555,7 +562,8 @@ def sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak):
             nm, cmp_ = r
             out["parity"] = offsets_digest(d_hits[: nm * 8].cpu().numpy().view("<u8"), cmp_)
         else:
-            nh, na = r
+            nh, na = ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), n, d_alerts.data_ptr(), cap,
+                                                  d_counts.data_ptr(), d_hits=d_hits.data_ptr(), hit_cap=cap)
             out["parity"] = digest(d_hits[: nh * 16].cpu().numpy().view(glop.HIT_DTYPE),
                                    d_alerts[: na * 16].cpu().numpy().view(glop.ALERT_DTYPE), len(pats))
     return out
@@ -597,6 +605,29 @@ def run_e2e(args, ctx, trie, rules, d_text, sh, world, barrier, max_over_ranks, 
     return {"value": round(8 * sh.own * world / dt / 1e9, 2), "unit": "Gbps", "h2d_bytes_per_step": sh.read,
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 3),
             "api": "glop_run_pfac_pipeline_shard (pinned host text)"}
+
+
+def run_e2e_dropin(args, glop, d_text, sh, pats):
+    """The reference caller's path: logtrawl::run_engine_scan (the drop-in
+    C++ header API, pfac_compact engine, the reference default) on the text in
+    PAGEABLE host memory, as a std::string would hold it -- upload, scan,
+    verify and the alert report back, per call, wall-clock."""
+    try:
+        eng = glop.Engine(pats)
+    except ImportError as e:
+        return {"unavailable": str(e)}
+    host = d_text[: sh.read].cpu().numpy()  # pageable
+    eng.run(host.ctypes.data, sh.read)  # warm-up: builds + uploads the cached trie / rules
+    steps = max(1, min(args.e2e_steps or args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        alerts, _, s1 = eng.run(host.ctypes.data, sh.read)
+    dt = (time.perf_counter() - t0) / steps
+    eng.close()
+    return {"value": round(8 * sh.own / dt / 1e9, 2), "unit": "Gbps", "h2d_bytes_per_step": sh.read,
+            "d2h_bytes_per_step": int(alerts.nbytes), "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "api": "logtrawl::run_engine_scan (include/logtrawl/pipeline.hpp, pfac_compact) via libglop_engine.so, "
+                   "text in pageable host memory"}
 
 
 def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):

@@ -131,6 +131,21 @@ glop_status glop_pfac_scan_device(glop_ctx* ctx, const glop_trie* trie, const ui
                                   uint64_t n, uint64_t own, uint64_t base, glop_pfac_kernel kernel,
                                   glop_hit* d_out, uint64_t cap, uint64_t* n_hits);
 
+/* ---- chunked full Aho-Corasick --------------------------------------------
+ * Replaces chunked_ac_scan (scan.hpp:207-243): chunk k owns starts
+ * [k*c, (k+1)*c) (c = chunk_size, 0 = the whole text) and is scanned from the
+ * root over [k*c, min(k*c + c + overlap, n)); a match is reported iff the
+ * chunk owning its start also reaches its end -- so an overlap below
+ * max_len - 1 loses boundary-straddling matches exactly as the reference does.
+ * `trie` is the GOTO trie of the AC automaton (its dense table) with only each
+ * pattern's own output (matched_len == depth); the device enumerates every
+ * occurrence with the PFAC kernel and keeps the owned, reached ones.  Result:
+ * (offset, pattern_id, matched_len) records sorted by (offset, pattern_id),
+ * library-owned (glop_free). */
+glop_status glop_chunked_ac_scan(glop_ctx* ctx, const glop_trie* trie, const uint8_t* text, uint64_t n,
+                                 int text_on_device, uint64_t chunk_size, uint64_t overlap, glop_hit** matches,
+                                 uint64_t* n_matches);
+
 /* ---- end-to-end PFAC pipeline --------------------------------------------
  * The device half of run_engine_scan's PFAC branch (pipeline.hpp:86-97):
  * text (host or device) -> pfac_scan -> verify_hits -> alerts + per-pattern
@@ -149,12 +164,38 @@ glop_status glop_run_pfac_pipeline_shard(glop_ctx* ctx, const glop_trie* trie,
                                          glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
                                          uint64_t* stage1_hits);
 
+/* With a LineIndex (run_engine_scan's `lines` argument, pipeline.hpp:49 /
+ * verify.hpp:40-64): also lines[i] = LineIndex(text).line_of(alerts[i].offset)
+ * (library-owned, glop_free) and *line_count = LineIndex(text).line_count()
+ * (1 + LF bytes of text), computed on the device from the same upload. */
+glop_status glop_run_pfac_pipeline_lines(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules,
+                                         const uint8_t* text, uint64_t n, int text_on_device, glop_alert** alerts,
+                                         uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits,
+                                         uint64_t** lines, uint64_t* line_count);
+
+/* Fully device-resident form (the bench step): d_text holds global offsets
+ * [base, base+n); starts [base, base+own) are scanned.  Writes the sorted
+ * alerts to d_alerts[0, alert_cap), the per-pattern alert counts to d_counts
+ * (n_patterns u64, OVERWRITTEN; may be NULL) and, when d_hits is not NULL,
+ * the sorted stage-1 hits to d_hits[0, hit_cap).  For 8-byte-prefix automata
+ * every kernel is enqueued back to back and the host waits once, at the end.
+ * GLOP_ECAPACITY (with *n_hits / *n_alerts set to the totals) when a buffer
+ * is too small. */
+glop_status glop_run_pfac_pipeline_device(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules,
+                                          const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                          glop_hit* d_hits, uint64_t hit_cap, glop_alert* d_alerts,
+                                          uint64_t alert_cap, uint64_t* d_counts, uint64_t* n_hits,
+                                          uint64_t* n_alerts);
+
 /* ---- measurement ----------------------------------------------------------
  * Device time of the most recent PFAC / KMP scan kernel on this context,
  * from CUDA events recorded on the context stream around the launch. */
 glop_status glop_last_kernel_ms(glop_ctx* ctx, float* ms);
 /* Number of kernels this context has launched so far. */
 uint64_t glop_ctx_launch_count(glop_ctx* ctx);
+/* Number of PFAC scans on this context that needed the exact global-key
+ * fallback (one lane emitting more hits than a warp's hit buffer holds). */
+uint64_t glop_ctx_fallback_count(glop_ctx* ctx);
 
 /* ---- stage-2 verification ------------------------------------------------
  * Patterns for verify_hits (verify.hpp:69-105): bytes of pattern i are

@@ -1,9 +1,11 @@
 #pragma once
 // Drop-in for logtrawl/verify.hpp (reference: /root/reference/proj/include/
 // logtrawl/verify.hpp).  verify_hits runs the stage-2 suffix compare and the
-// order-preserving compaction on the B200; Alert names and line numbers are
-// attached on the host (LineIndex stays a host index, as in the reference).
+// order-preserving compaction on the B200; Alert names are attached on the
+// host.  LineIndex stays the reference's host index; run_engine_scan computes
+// the alert lines on the device from the same upload (pipeline.hpp).
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -60,50 +62,54 @@ class LineIndex {
 
 namespace detail {
 
-struct DeviceRules {
-  glop_rules* r = nullptr;
-  explicit DeviceRules(const RuleSet& rules, std::size_t prefix_len) {
-    std::string blob;
-    std::vector<std::uint64_t> off{0};
-    for (std::size_t i = 0; i < rules.patterns.size(); ++i) {
-      if (rules.patterns[i].id != i) throw std::invalid_argument("verify_hits: pattern ids must be dense 0..k-1");
-      blob += rules.patterns[i].bytes;
-      off.push_back(blob.size());
+// Device alerts -> reference Alerts.  The device reports the POSITION of the
+// pattern (hits name patterns by position: rules.patterns.at(pattern_id),
+// verify.hpp:78); the Alert carries that pattern's id and name, sorted by
+// (offset, rule_id) (verify.hpp:100-103) -- only a RuleSet whose ids are not
+// their positions changes the device's (offset, position) order.
+inline std::vector<Alert> to_alerts(const glop_alert* a, std::uint64_t na, const RuleSet& rules,
+                                    const LineIndex* lines, const std::uint64_t* dev_lines) {
+  for (std::uint64_t i = 0; i < na; ++i)  // rules.patterns.at() (verify.hpp:78) throws before any work
+    if (a[i].rule_id >= rules.patterns.size()) (void)rules.patterns.at(a[i].rule_id);
+  std::vector<Alert> out(na);
+  std::atomic<bool> dense_ids{true};
+  parallel_for(na, [&](std::size_t lo, std::size_t hi) {
+    bool dense = true;
+    for (std::size_t i = lo; i < hi; ++i) {
+      const Pattern& p = rules.patterns[a[i].rule_id];
+      dense = dense && p.id == a[i].rule_id;
+      Alert& al = out[i];
+      al.offset = a[i].offset;
+      al.line = dev_lines ? dev_lines[i] : (lines ? lines->line_of(a[i].offset) : 0);
+      al.rule_id = p.id;
+      al.rule_name = p.name;
+      al.pattern_len = a[i].pattern_len;
+      al.verified = true;
     }
-    check(glop_rules_upload(context(), reinterpret_cast<const std::uint8_t*>(blob.data()), off.data(),
-                            static_cast<std::uint32_t>(rules.patterns.size()), prefix_len, &r),
-          "verify_hits");
-  }
-  ~DeviceRules() { glop_rules_destroy(r); }
-  DeviceRules(const DeviceRules&) = delete;
-  DeviceRules& operator=(const DeviceRules&) = delete;
-};
+    if (!dense) dense_ids = false;
+  });
+  if (!dense_ids)
+    std::stable_sort(out.begin(), out.end(), [](const Alert& x, const Alert& y) {
+      return x.offset != y.offset ? x.offset < y.offset : x.rule_id < y.rule_id;
+    });
+  return out;
+}
 
 }  // namespace detail
 
-// verify.hpp:69-105 on the B200: alerts sorted by (offset, rule_id).
+// verify.hpp:69-105 on the B200: alerts sorted by (offset, rule_id).  The
+// rule set's device copy is cached by content (detail::device_rules).
 inline std::vector<Alert> verify_hits(std::string_view text, const std::vector<Hit>& hits, const PrefixSet& prefixes,
                                       const RuleSet& rules, const LineIndex* lines = nullptr) {
-  std::vector<Alert> out;
-  if (hits.empty()) return out;
-  detail::DeviceRules dr(rules, prefixes.prefix_len);
+  if (hits.empty()) return {};
+  const auto dr = detail::device_rules(rules, prefixes.prefix_len);
   glop_alert* a = nullptr;
   std::uint64_t na = 0;
-  detail::check(glop_verify_hits(detail::context(), dr.r, reinterpret_cast<const std::uint8_t*>(text.data()),
+  detail::check(glop_verify_hits(detail::context(), dr->rules, reinterpret_cast<const std::uint8_t*>(text.data()),
                                  text.size(), 0, reinterpret_cast<const glop_hit*>(hits.data()), hits.size(), 0, &a,
                                  &na, nullptr),
                 "verify_hits");
-  out.reserve(na);
-  for (std::uint64_t i = 0; i < na; ++i) {
-    Alert al;
-    al.offset = a[i].offset;
-    al.line = lines ? lines->line_of(a[i].offset) : 0;
-    al.rule_id = a[i].rule_id;
-    al.rule_name = rules.patterns[a[i].rule_id].name;
-    al.pattern_len = a[i].pattern_len;
-    al.verified = true;
-    out.push_back(std::move(al));
-  }
+  std::vector<Alert> out = detail::to_alerts(a, na, rules, lines, nullptr);
   glop_free(a);
   return out;
 }

@@ -12,16 +12,19 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include "glop.h"
 #include "glop_kernels.cuh"
 #include "pfac8.cuh"
 #include "kmp.cuh"
 #include "lines.cuh"
+#include "pipeline.cuh"
 #include "logtrawl/automaton.hpp"
 #include "logtrawl/detail/abi.hpp"
 #include "workload.hpp"
@@ -91,12 +94,16 @@ struct glop_ctx {
   DBuf keep, bcounts, bprefix, alerts, kmp_dfa, spill;
   DBuf sbuf[2];                                  // streamed text chunks (host-text pipeline)
   DBuf lcount, lprefix, loffs;                   // device LineIndex
+  DBuf hprefix, kcounts, kprefix, keep8, counts_tmp;  // fused pipeline (pipeline.cuh)
+  DBuf palerts, plines;                          // alerts (+ lines) of the host-facing pipeline calls
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
+  void* pin[2] = {nullptr, nullptr};             // pinned staging of pageable host text
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   unsigned long long* h_misc = nullptr;  // pinned readback
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
   bool timed = false;
   uint64_t launches = 0;
+  uint64_t fallbacks = 0;  // scans that took the exact global-key fallback
   std::mutex mu;
 };
 
@@ -110,6 +117,8 @@ struct glop_trie {
   bool smem_filter = false, smem_direct = false, smem_jump = false;
   bool p8 = false;  // every output at depth >= 8: pfac8_kernel applies
   int p8_l1 = 0;  // pfac8 level-1/2 layout (kL1, see pfac8.cuh)
+  mutable bool p8_careful = false;  // kCareful pfac8 kernel (set at upload; sticky after a fallback)
+  uint32_t p8_lane_emits = 0;       // most hits one start position can emit
   uint32_t max_pid = 0;
 };
 
@@ -190,95 +199,118 @@ glop_status radix_sort_keys(glop_ctx* c, unsigned long long* in, unsigned long l
   return GLOP_OK;
 }
 
+// pfac8 launch geometry: one CTA per SM, kP8Warps contiguous warp segments
+// per CTA, one staging region per warp.
+struct P8Geom {
+  uint32_t num_tiles, per, sub;
+  int grid;
+  unsigned long long regions, region;
+};
+
+glop_status p8_geometry(glop_ctx* c, const uint8_t* d_text, uint64_t own, P8Geom* G) {
+  const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
+  G->num_tiles = (uint32_t)((own + a + kP8Tile - 1) / kP8Tile);
+  G->grid = (int)std::min<uint32_t>((G->num_tiles + kP8Warps - 1) / kP8Warps, (uint32_t)c->num_sms);
+  G->per = (G->num_tiles + G->grid - 1) / G->grid;
+  G->sub = (G->per + kP8Warps - 1) / kP8Warps;
+  G->regions = (unsigned long long)G->grid * kP8Warps;
+  TRY(c->bcounts.ensure(8 * G->regions));
+  TRY(c->prefix.ensure(8 * G->regions));
+  TRY(c->misc.ensure(64));
+  unsigned long long region =
+      std::max<unsigned long long>(256, (std::max<uint64_t>(1 << 20, own / 512) + G->regions - 1) / G->regions);
+  if (c->staging.bytes < region * G->regions * sizeof(glop_hit))
+    TRY(c->staging.ensure(region * G->regions * sizeof(glop_hit)));
+  G->region = c->staging.bytes / sizeof(glop_hit) / G->regions;
+  return GLOP_OK;
+}
+
+glop_status launch_pfac8(glop_ctx* c, const glop_trie* t, const P8Geom& G, const P8Params& p) {
+  using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
+#define GLOP_P8_K(w, l, c) {pfac8_kernel<w, l, uint16_t, c>, pfac8_kernel<w, l, uint32_t, c>}
+  static const KF table[2][2][3][2] = {
+      {{GLOP_P8_K(false, 0, false), GLOP_P8_K(false, 1, false), GLOP_P8_K(false, 2, false)},
+       {GLOP_P8_K(true, 0, false), GLOP_P8_K(true, 1, false), GLOP_P8_K(true, 2, false)}},
+      {{GLOP_P8_K(false, 0, true), GLOP_P8_K(false, 1, true), GLOP_P8_K(false, 2, true)},
+       {GLOP_P8_K(true, 0, true), GLOP_P8_K(true, 1, true), GLOP_P8_K(true, 2, true)}}};
+#undef GLOP_P8_K
+  const P8Layout L = make_p8_layout();
+  const KF k = table[t->p8_careful][t->info.max_depth > 8][t->p8_l1][t->u16 ? 0 : 1];
+  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  CU(cudaEventRecord(c->ev0, c->stream));
+  k<<<G.grid, kP8Threads, L.total, c->stream>>>(t->view, p, L);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(c->ev1, c->stream));
+  c->timed = true;
+  ++c->launches;
+  return GLOP_OK;
+}
+
+P8Params p8_params(glop_ctx* c, const glop_trie* t, const P8Geom& G, const uint8_t* d_text, uint64_t n, uint64_t own,
+                   uint64_t base) {
+  P8Params p{};
+  p.text = d_text;
+  p.n = n;
+  p.own = own;
+  p.base = base;
+  p.num_tiles = G.num_tiles;
+  p.per = G.per;
+  p.sub = G.sub;
+  p.mode = 0;
+  p.staging = reinterpret_cast<DevHit*>(c->staging.p);
+  p.region = G.region;
+  p.counts = c->bcounts.as<unsigned long long>();
+  p.g_count = c->misc.as<unsigned long long>();
+  p.dmask8 = t->view.dmask8;
+  return p;
+}
+
 // pfac8 path (every output at depth >= 8), same contract as below.
 glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_text, uint64_t n,
                             uint64_t own, uint64_t base, glop_hit* d_out, uint64_t cap, uint64_t* n_hits) {
-  const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
-  const uint32_t num_tiles = (uint32_t)((own + a + kP8Tile - 1) / kP8Tile);
-  const int grid = (int)std::min<uint32_t>((num_tiles + kP8Warps - 1) / kP8Warps, (uint32_t)c->num_sms);
-  const uint32_t per = (num_tiles + grid - 1) / grid;
-  const uint32_t sub = (per + kP8Warps - 1) / kP8Warps;
-  const unsigned long long regions = (unsigned long long)grid * kP8Warps;
-  TRY(c->bcounts.ensure(8 * regions));
-  TRY(c->prefix.ensure(8 * regions));
-  TRY(c->misc.ensure(64));
-  unsigned long long region =
-      std::max<unsigned long long>(256, (std::max<uint64_t>(1 << 20, own / 512) + regions - 1) / regions);
-  if (c->staging.bytes < region * regions * sizeof(glop_hit))
-    TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
-  region = c->staging.bytes / sizeof(glop_hit) / regions;
-  const P8Layout L = make_p8_layout();
+  P8Geom G;
+  TRY(p8_geometry(c, d_text, own, &G));
   auto* g = c->misc.as<unsigned long long>();
-  auto launch = [&](const P8Params& p) -> glop_status {
-    using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
-    static const KF table[2][3][2] = {
-        {{pfac8_kernel<false, 0, uint16_t>, pfac8_kernel<false, 0, uint32_t>},
-         {pfac8_kernel<false, 1, uint16_t>, pfac8_kernel<false, 1, uint32_t>},
-         {pfac8_kernel<false, 2, uint16_t>, pfac8_kernel<false, 2, uint32_t>}},
-        {{pfac8_kernel<true, 0, uint16_t>, pfac8_kernel<true, 0, uint32_t>},
-         {pfac8_kernel<true, 1, uint16_t>, pfac8_kernel<true, 1, uint32_t>},
-         {pfac8_kernel<true, 2, uint16_t>, pfac8_kernel<true, 2, uint32_t>}}};
-    const KF k = table[t->info.max_depth > 8][t->p8_l1][t->u16 ? 0 : 1];
-    CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    CU(cudaEventRecord(c->ev0, c->stream));
-    k<<<grid, kP8Threads, L.total, c->stream>>>(t->view, p, L);
-    CU(cudaGetLastError());
-    CU(cudaEventRecord(c->ev1, c->stream));
-    c->timed = true;
-    ++c->launches;
-    return GLOP_OK;
-  };
   for (int attempt = 0; attempt < 3; ++attempt) {
-    CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
-    P8Params p{};
-    p.text = d_text;
-    p.n = n;
-    p.own = own;
-    p.base = base;
-    p.num_tiles = num_tiles;
-    p.per = per;
-    p.sub = sub;
-    p.mode = 0;
-    p.staging = reinterpret_cast<DevHit*>(c->staging.p);
-    p.region = region;
-    p.counts = c->bcounts.as<unsigned long long>();
-    p.g_count = g;
-    p.dmask8 = t->view.dmask8;
-    TRY(launch(p));
+    CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
+    P8Params p = p8_params(c, t, G, d_text, n, own, base);
+    TRY(launch_pfac8(c, t, G, p));
     // ordered output, enqueued before the flags are known (see p8_gather_kernel)
     c->launches += 2;
-    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
+    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)G.regions,
                                                  c->prefix.as<unsigned long long>());
-    p8_gather_kernel<DevHit><<<(uint32_t)regions, 256, 0, c->stream>>>(
-        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
+    p8_gather_kernel<DevHit><<<(uint32_t)G.regions, 256, 0, c->stream>>>(
+        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), G.region,
         reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out), cap);
     CU(cudaGetLastError());
     TRY(sync_read(c, c->misc.p, 32));
-    const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[2];
-    const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
+    const unsigned long long total = c->h_misc[kStTotal], maxregion = c->h_misc[kStMaxRegion];
+    const unsigned flags = (unsigned)(c->h_misc[kStFlags] & 0xffffffffu);
     if (getenv("GLOP_DEBUG"))
       fprintf(stderr, "pfac8: tiles %u grid %d per %u sub %u region %llu -> total %llu flags %u maxregion %llu\n",
-              num_tiles, grid, per, sub, region, total, flags, maxregion);
+              G.num_tiles, G.grid, G.per, G.sub, G.region, total, flags, maxregion);
     *n_hits = total;
     if (flags & 1u) {
+      ++c->fallbacks;
+      t->p8_careful = true;  // later scans of this automaton replay lanes from an empty buffer
       // one lane of a drain round produced more hits than the warp's buffer
       // holds: exact fallback -- global keys, device radix sort.  A counting
       // pass (keys_cap = 0) sizes the key buffer.
-      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+      CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
       p.mode = 1;
       p.keys = nullptr;
       p.keys_cap = 0;
-      TRY(launch(p));
+      TRY(launch_pfac8(c, t, G, p));
       TRY(sync_read(c, c->misc.p, 32));
-      const unsigned long long exact_total = c->h_misc[3];
+      const unsigned long long exact_total = c->h_misc[kStKeys];
       *n_hits = exact_total;
       if (exact_total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
       TRY(c->keys.ensure(exact_total * 8 + 8));
       TRY(c->keys_alt.ensure(exact_total * 8 + 8));
-      CU(cudaMemsetAsync(c->misc.p, 0, 32, c->stream));
+      CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
       p.keys = c->keys.as<unsigned long long>();
       p.keys_cap = exact_total;
-      TRY(launch(p));
+      TRY(launch_pfac8(c, t, G, p));
       if (exact_total == 0) return GLOP_OK;
       TRY(radix_sort_keys(c, c->keys.as<unsigned long long>(), c->keys_alt.as<unsigned long long>(), exact_total));
       c->launches += 2;
@@ -289,15 +321,17 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
       CU(cudaStreamSynchronize(c->stream));
       return GLOP_OK;
     }
-    if (maxregion > region) {  // a warp's staging region overflowed: grow, rerun
-      region = maxregion + maxregion / 4 + 64;
+    if (maxregion > G.region) {  // a warp's staging region overflowed: grow, rerun
+      const unsigned long long region = maxregion + maxregion / 4 + 64;
       c->staging.release();
-      TRY(c->staging.ensure(region * regions * sizeof(glop_hit)));
+      TRY(c->staging.ensure(region * G.regions * sizeof(glop_hit)));
+      G.region = region;
       continue;
     }
     if (total > cap) return fail(GLOP_ECAPACITY, "pfac_scan: output capacity");
     return GLOP_OK;
   }
+  (void)g;
   return fail(GLOP_ECUDA, "pfac_scan: staging did not converge");
 }
 
@@ -352,6 +386,7 @@ glop_status pfac_scan_device_impl(glop_ctx* c, const glop_trie* t, const uint8_t
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
     *n_hits = total;
     if (flags & 1u) {
+      ++c->fallbacks;
       // a slice produced more hits than its shared-memory buffer holds:
       // exact fallback -- global keys, device radix sort
       if (t->max_pid >= (1u << 24) || base + n >= (1ull << 40))
@@ -421,6 +456,9 @@ void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::
     }
 }
 
+glop_status kmp_seq_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab, const uint8_t* d_text,
+                         uint64_t n, uint64_t* d_out, uint64_t cap, uint64_t* n_offsets, uint64_t* comparisons);
+
 glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab,
                             const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
                             uint64_t* d_out, uint64_t cap, uint64_t* n_offsets,
@@ -428,16 +466,21 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
   *n_offsets = 0;
   if (own > n) return fail(GLOP_EINVAL, "kmp_search: own > n");
   if (m == 0 || n < m || own == 0) return GLOP_OK;  // kmp.hpp:50
-  if (m >= 8192) return fail(GLOP_EINVAL, "kmp_search: pattern longer than 8191 bytes");
   // chunks resynchronise from the previous m-1 bytes, which is exact for the
-  // pattern's own prefix function (kmp.hpp:25-36); reject any other table
-  for (uint32_t i = 0, k = 0; i < m; ++i) {
+  // pattern's own prefix function (kmp.hpp:25-36); any other table (or a
+  // pattern too long for the DFA) runs the sequential walk, whole texts only
+  bool canonical = m < 8192;
+  for (uint32_t i = 0, k = 0; i < m && canonical; ++i) {
     if (i > 0) {
       while (k > 0 && pat[i] != pat[k]) k = fail_tab[k - 1];
       if (pat[i] == pat[k]) ++k;
     }
-    if (fail_tab[i] != (i ? k : 0u))
-      return fail(GLOP_EINVAL, "kmp_search: failure table is not the pattern's prefix function");
+    canonical = fail_tab[i] == (i ? k : 0u);
+  }
+  if (!canonical) {
+    if (own != n || base != 0)
+      return fail(GLOP_EINVAL, "kmp_search: shards need the pattern's own prefix function and m < 8192");
+    return kmp_seq_impl(c, pat, m, fail_tab, d_text, n, d_out, cap, n_offsets, comparisons);
   }
   std::vector<uint32_t> dfa;
   build_kmp_dfa(pat, m, fail_tab, dfa);
@@ -618,98 +661,295 @@ glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* 
   return GLOP_OK;
 }
 
+// Device-resident scan + verify + counts (the device half of run_engine_scan's
+// PFAC branch).  pfac8 automata take the fused path of pipeline.cuh: every
+// kernel is enqueued back to back and the host reads one status block at the
+// end.  A scan that needs the exact fallback or a larger staging region, and
+// non-pfac8 automata, go through pfac_scan_device_impl + verify_device_impl.
+// d_hits (optional) receives the ordered hits (hit_cap records); d_counts
+// (optional) the per-pattern alert counts (overwritten, not accumulated).
+glop_status pipeline_device_impl(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* d_text,
+                                 uint64_t n, uint64_t own, uint64_t base, glop_hit* d_hits, uint64_t hit_cap,
+                                 glop_alert* d_alerts, uint64_t alert_cap, uint64_t* d_counts, uint64_t* n_hits,
+                                 uint64_t* n_alerts) {
+  *n_hits = *n_alerts = 0;
+  if (own > n) return fail(GLOP_EINVAL, "run_pfac_pipeline: own > n");
+  const uint32_t k = r->view.n_patterns;
+  if (!d_counts) {
+    TRY(c->counts_tmp.ensure((size_t)(k + 1) * 8));
+    d_counts = c->counts_tmp.as<uint64_t>();
+  }
+  const bool fused = t->p8 && !t->empty && own > 0 && t->max_pid < (1u << 24) && base + n < (1ull << 40) &&
+                     !getenv("GLOP_NO_FUSED");
+  if (fused) {
+    P8Geom G;
+    TRY(p8_geometry(c, d_text, own, &G));
+    const bool stage2 = r->max_len > r->view.prefix_len;
+    TRY(c->hprefix.ensure(8 * G.regions));
+    if (stage2) {
+      TRY(c->kcounts.ensure(8 * G.regions));
+      TRY(c->kprefix.ensure(8 * G.regions));
+      TRY(c->keep8.ensure(G.regions * G.region));
+    }
+    auto* g = c->misc.as<unsigned long long>();
+    CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
+    const P8Params p = p8_params(c, t, G, d_text, n, own, base);
+    TRY(launch_pfac8(c, t, G, p));
+    const auto* cnt = c->bcounts.as<unsigned long long>();
+    p8_prefix_kernel<<<1, 1024, 0, c->stream>>>(cnt, (uint32_t)G.regions, G.region,
+                                                c->hprefix.as<unsigned long long>(), g + kStHits,
+                                                reinterpret_cast<unsigned long long*>(d_counts), k);
+    const uint32_t egrid = (uint32_t)std::min<unsigned long long>(G.regions, 2ull * c->num_sms);
+    const uint32_t hist_bins = (size_t)k * 4 <= kSmemMax - 1024 ? k : 0;
+    const size_t hist_bytes = (size_t)hist_bins * 4;
+    if (stage2) {
+      c->launches += 2;
+      p8_keep_kernel<<<(uint32_t)std::min<unsigned long long>(G.regions, 8ull * c->num_sms), 256, 0, c->stream>>>(
+          r->view, d_text, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
+          c->keep8.as<uint8_t>(), c->kcounts.as<unsigned long long>(), g + kStVerify);
+      p8_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->kcounts.as<unsigned long long>(), (uint32_t)G.regions,
+                                                  G.region, c->kprefix.as<unsigned long long>(), g + kStKept,
+                                                  nullptr, 0);
+      CU(cudaFuncSetAttribute(p8_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_bytes));
+      p8_emit_kernel<true><<<egrid, 1024, hist_bytes, c->stream>>>(
+          r->view, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
+          c->keep8.as<uint8_t>(), c->hprefix.as<unsigned long long>(), c->kprefix.as<unsigned long long>(),
+          reinterpret_cast<DevHit*>(d_hits), d_hits ? hit_cap : 0, reinterpret_cast<DevAlert*>(d_alerts), alert_cap,
+          reinterpret_cast<unsigned long long*>(d_counts), hist_bins, g + kStVerify);
+    } else {
+      CU(cudaFuncSetAttribute(p8_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_bytes));
+      p8_emit_kernel<false><<<egrid, 1024, hist_bytes, c->stream>>>(
+          r->view, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
+          nullptr, c->hprefix.as<unsigned long long>(), nullptr, reinterpret_cast<DevHit*>(d_hits),
+          d_hits ? hit_cap : 0, reinterpret_cast<DevAlert*>(d_alerts), alert_cap,
+          reinterpret_cast<unsigned long long*>(d_counts), hist_bins, g + kStVerify);
+    }
+    c->launches += 2;
+    CU(cudaGetLastError());
+    TRY(sync_read(c, c->misc.p, 64));
+    const unsigned long long* h = c->h_misc;
+    const unsigned flags = (unsigned)(h[kStFlags] & 0xffffffffu);
+    if (!(flags & 1u) && h[kStMaxRegion] <= G.region) {
+      if (h[kStVerify] & 1u) return fail(GLOP_ELOGIC, "verify_hits: hit extends past end of text");
+      *n_hits = h[kStTotal];
+      *n_alerts = stage2 ? h[kStKept] : h[kStTotal];
+      if ((d_hits && *n_hits > hit_cap) || *n_alerts > alert_cap)
+        return fail(GLOP_ECAPACITY, "run_pfac_pipeline: output capacity");
+      return GLOP_OK;
+    }
+    // overflow: the general path below handles the exact fallback / regrowth
+  }
+  glop_hit* hits = d_hits;
+  uint64_t cap = hit_cap;
+  if (!hits) {
+    cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
+    TRY(c->out.ensure(cap * sizeof(glop_hit)));
+    hits = c->out.as<glop_hit>();
+  }
+  uint64_t nh = 0;
+  glop_status s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, hits, cap, &nh);
+  if (s == GLOP_ECAPACITY && !d_hits && nh > cap) {
+    c->out.release();
+    cap = nh;
+    TRY(c->out.ensure(cap * sizeof(glop_hit)));
+    hits = c->out.as<glop_hit>();
+    s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, hits, cap, &nh);
+  }
+  *n_hits = nh;
+  if (s != GLOP_OK) return s;
+  if (nh > alert_cap) {  // alerts <= hits; only a short alert buffer can overflow
+    TRY(c->alerts.ensure(nh * sizeof(glop_alert)));
+    CU(cudaMemsetAsync(d_counts, 0, (size_t)k * 8, c->stream));
+    uint64_t kept = 0;
+    TRY(verify_device_impl(c, r, d_text, n, base, hits, nh, c->alerts.as<glop_alert>(), &kept, d_counts));
+    *n_alerts = kept;
+    if (kept > alert_cap) return fail(GLOP_ECAPACITY, "run_pfac_pipeline: output capacity");
+    CU(cudaMemcpyAsync(d_alerts, c->alerts.p, kept * sizeof(glop_alert), cudaMemcpyDeviceToDevice, c->stream));
+    return GLOP_OK;
+  }
+  CU(cudaMemsetAsync(d_counts, 0, (size_t)k * 8, c->stream));
+  return verify_device_impl(c, r, d_text, n, base, hits, nh, d_alerts, n_alerts, d_counts);
+}
+
 // Host-text pipeline for large inputs (streaming ingest):
 // the text is copied in kStreamChunk pieces (+ a halo for the trie walk and
 // the stage-2 suffix compare) on a copy stream into two device buffers, so
 // the H2D copy of chunk i+1 overlaps the scan + verify of chunk i.  Chunk
 // results are exact and ordered (ownership of starts, scan.hpp:230-232), so
 // the alerts are the concatenation of the chunks' alerts.
+glop_status line_numbers_impl(glop_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t base, const void* d_recs,
+                              uint32_t stride, uint64_t count, uint64_t* d_lines, const uint64_t* d_line_base,
+                              uint64_t* d_lf_acc);
+
+// memcpy on up to 16 host threads (pageable -> pinned staging).
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned T = (unsigned)std::min<size_t>(std::min(hw, 16u), std::max<size_t>(1, bytes >> 22));
+  if (T <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t per = (bytes / T + 4095) & ~size_t(4095);
+  for (unsigned t = 0; t < T; ++t) {
+    const size_t lo = std::min(bytes, t * per), hi = std::min(bytes, lo + per);
+    if (lo < hi)
+      pool.emplace_back([=] { memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Grows a device buffer to `want` bytes keeping its first `keep` bytes.
+glop_status grow_keep(glop_ctx* c, DBuf& b, size_t want, size_t keep) {
+  if (want <= b.bytes) return GLOP_OK;
+  DBuf bigger;
+  TRY(bigger.ensure(std::max<size_t>(want, 2 * b.bytes)));
+  if (keep) CU(cudaMemcpyAsync(bigger.p, b.p, keep, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  b.release();
+  b = bigger;
+  bigger.p = nullptr;
+  return GLOP_OK;
+}
+
+// Copies the n_alerts alerts (+ lines when wanted) and the counts to
+// library-owned host arrays.
+glop_status alerts_to_host(glop_ctx* c, const glop_alert* d_alerts, uint64_t n_alerts, const uint64_t* d_counts,
+                           uint32_t k, uint64_t* counts, glop_alert** alerts, const uint64_t* d_lines, uint64_t** lines,
+                           const uint64_t* d_lf, uint64_t* line_count) {
+  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(n_alerts, 1) * sizeof(glop_alert)));
+  uint64_t* l = lines ? static_cast<uint64_t*>(malloc(std::max<uint64_t>(n_alerts, 1) * 8)) : nullptr;
+  cudaError_t e = a && (!lines || l) ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess && n_alerts)
+    e = cudaMemcpyAsync(a, d_alerts, n_alerts * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && counts) e = cudaMemcpyAsync(counts, d_counts, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && lines && n_alerts)
+    e = cudaMemcpyAsync(l, d_lines, n_alerts * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && line_count) e = cudaMemcpyAsync(c->h_misc + 7, d_lf, 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(a);
+    free(l);
+    return fail(e == cudaErrorMemoryAllocation ? GLOP_ENOMEM : GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  if (line_count) *line_count = c->h_misc[7] + 1;  // LineIndex::line_count() = 1 + LF bytes
+  *alerts = a;
+  if (lines) *lines = l;
+  return GLOP_OK;
+}
+
 glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* h_text,
                                   uint64_t n, uint64_t own, uint64_t base, glop_alert** alerts,
-                                  uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits) {
+                                  uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits,
+                                  uint64_t** lines = nullptr, uint64_t* line_count = nullptr) {
   const uint64_t halo = std::max<uint64_t>(std::max<uint64_t>(t->info.max_depth, r->max_len), 1) - 1;
   const uint64_t chunks = (own + kStreamChunk - 1) / kStreamChunk;
   for (int b = 0; b < 2; ++b) TRY(c->sbuf[b].ensure(kStreamChunk + halo + 64));
   const uint32_t k = r->view.n_patterns;
-  TRY(c->spill.ensure((size_t)(k + 1) * 8));
-  uint64_t* d_counts = c->spill.as<uint64_t>();
-  CU(cudaMemsetAsync(d_counts, 0, (size_t)(k + 1) * 8, c->stream));
-  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
-  TRY(c->out.ensure(cap * sizeof(glop_hit)));
-  DBuf& acc = c->alerts;  // accumulated alerts (device); grows rarely, kept across calls
+  TRY(c->spill.ensure((size_t)(2 * k + 3) * 8));
+  uint64_t* d_counts = c->spill.as<uint64_t>();          // accumulated over chunks
+  uint64_t* d_chunk_counts = d_counts + k + 1;           // one chunk's counts
+  uint64_t* d_lf = d_chunk_counts + k + 1;               // LF bytes of the chunks so far
+  CU(cudaMemsetAsync(d_counts, 0, (size_t)(2 * k + 3) * 8, c->stream));
+  const bool want_lines = lines || line_count;
+  DBuf& acc = c->palerts;  // accumulated alerts (device); grows rarely, kept across calls
+  TRY(acc.ensure(std::max<size_t>(acc.bytes, (1 << 16) * sizeof(glop_alert))));
   uint64_t total = 0, hits = 0;
+  // Pageable text (a std::string, a file read into memory): the driver would
+  // stage it through its own pinned buffers on one thread; instead host
+  // threads copy each chunk into one of two pinned staging buffers while the
+  // DMA of the previous chunk runs.
+  cudaPointerAttributes pa{};
+  const bool pageable = cudaPointerGetAttributes(&pa, h_text) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered;
+  cudaGetLastError();  // (older drivers report unregistered memory as an error)
+  if (pageable)
+    for (int b = 0; b < 2; ++b)
+      if (!c->pin[b]) CU(cudaMallocHost(&c->pin[b], kStreamChunk + halo + 64));
   auto copy = [&](uint64_t i) -> glop_status {
     const uint64_t lo = i * kStreamChunk;
     const uint64_t rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - lo) + halo, n - lo);
+    const uint8_t* src = h_text + lo;
+    if (pageable) {  // the DMA out of pin[b] two chunks ago must be done
+      CU(cudaEventSynchronize(c->ev_copied[i & 1]));
+      parallel_memcpy(c->pin[i & 1], src, rd);
+      src = static_cast<const uint8_t*>(c->pin[i & 1]);
+    }
     CU(cudaStreamWaitEvent(c->cstream, c->ev_free[i & 1], 0));
-    CU(cudaMemcpyAsync(c->sbuf[i & 1].p, h_text + lo, rd, cudaMemcpyHostToDevice, c->cstream));
+    CU(cudaMemcpyAsync(c->sbuf[i & 1].p, src, rd, cudaMemcpyHostToDevice, c->cstream));
     CU(cudaEventRecord(c->ev_copied[i & 1], c->cstream));
     return GLOP_OK;
   };
   // ev_free[b]: buffer b may be overwritten (recorded after its chunk's work)
   CU(cudaEventRecord(c->ev_free[0], c->stream));
   CU(cudaEventRecord(c->ev_free[1], c->stream));
-  glop_status st = copy(0);
-  for (uint64_t i = 0; i < chunks && st == GLOP_OK; ++i) {
+  TRY(copy(0));
+  for (uint64_t i = 0; i < chunks; ++i) {
     if (i + 1 < chunks) TRY(copy(i + 1));
     const uint64_t lo = i * kStreamChunk, own_i = std::min<uint64_t>(kStreamChunk, own - lo);
     const uint64_t rd = std::min<uint64_t>(own_i + halo, n - lo);
     const uint8_t* d_text = c->sbuf[i & 1].as<uint8_t>();
     CU(cudaStreamWaitEvent(c->stream, c->ev_copied[i & 1], 0));
-    uint64_t nh = 0;
-    glop_status s = pfac_scan_device_impl(c, t, d_text, rd, own_i, base + lo, GLOP_PFAC_AUTO, c->out.as<glop_hit>(),
-                                          cap, &nh);
-    if (s == GLOP_ECAPACITY && nh > cap) {
-      c->out.release();
-      cap = nh;
-      TRY(c->out.ensure(cap * sizeof(glop_hit)));
-      s = pfac_scan_device_impl(c, t, d_text, rd, own_i, base + lo, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
+    uint64_t nh = 0, kept = 0;
+    for (;;) {
+      const uint64_t room = acc.bytes / sizeof(glop_alert) - total;
+      glop_status s = pipeline_device_impl(c, t, r, d_text, rd, own_i, base + lo, nullptr, 0,
+                                           acc.as<glop_alert>() + total, room, d_chunk_counts, &nh, &kept);
+      if (s == GLOP_ECAPACITY && kept > room) {  // grow, keeping the alerts so far; redo the chunk
+        DBuf bigger;
+        TRY(bigger.ensure(std::max<uint64_t>(2 * acc.bytes, (total + kept + (1 << 16)) * sizeof(glop_alert))));
+        if (total) CU(cudaMemcpyAsync(bigger.p, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        acc.release();
+        acc = bigger;
+        bigger.p = nullptr;
+        continue;
+      }
+      if (s != GLOP_OK) return s;
+      break;
     }
-    if (s != GLOP_OK) return s;
-    hits += nh;
-    if ((total + nh) * sizeof(glop_alert) > acc.bytes) {  // grow, keeping the alerts so far
-      DBuf bigger;
-      TRY(bigger.ensure(std::max<uint64_t>(2 * acc.bytes, (total + nh + (1 << 16)) * sizeof(glop_alert))));
-      if (total) CU(cudaMemcpyAsync(bigger.p, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToDevice, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
-      acc.release();
-      acc = bigger;
-      bigger.p = nullptr;
+    if (want_lines) {  // LineIndex over the owned bytes of this chunk, offset by the earlier chunks' LFs
+      TRY(grow_keep(c, c->plines, (total + kept) * 8 + 8, total * 8));
+      TRY(line_numbers_impl(c, d_text, own_i, base + lo, acc.as<glop_alert>() + total, sizeof(glop_alert), kept,
+                            c->plines.as<uint64_t>() + total, d_lf, d_lf));
     }
-    uint64_t kept = 0;
-    TRY(verify_device_impl(c, r, d_text, rd, base + lo, c->out.as<glop_hit>(), nh, acc.as<glop_alert>() + total,
-                           &kept, d_counts));
+    ++c->launches;
+    add_u64_kernel<<<(k + 255) / 256 + 1, 256, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<const unsigned long long*>(d_chunk_counts), k);
+    CU(cudaGetLastError());
     CU(cudaEventRecord(c->ev_free[i & 1], c->stream));
+    hits += nh;
     total += kept;
   }
   if (stage1_hits) *stage1_hits = hits;
-  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(total, 1) * sizeof(glop_alert)));
-  cudaError_t e = a ? cudaSuccess : cudaErrorMemoryAllocation;
-  if (e == cudaSuccess && total)
-    e = cudaMemcpyAsync(a, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess && counts) e = cudaMemcpyAsync(counts, d_counts, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-  if (e != cudaSuccess) {
-    free(a);
-    return fail(e == cudaErrorMemoryAllocation ? GLOP_ENOMEM : GLOP_ECUDA, cudaGetErrorString(e));
-  }
-  *alerts = a;
+  TRY(alerts_to_host(c, acc.as<glop_alert>(), total, d_counts, k, counts, alerts, c->plines.as<uint64_t>(), lines,
+                     d_lf, line_count));
   *n_alerts = total;
   return GLOP_OK;
 }
 
 // Device LineIndex (lines.cuh): lines[i] = line of record i's offset (u64
-// at byte 0 of each `stride`-byte record) in text d_text = global [base, base+n).
+// at byte 0 of each `stride`-byte record) in text d_text = global [base, base+n),
+// plus *d_line_base when given (lines of earlier streamed chunks).  d_lf_acc
+// (optional) is incremented by the number of LF bytes in text[0, n).
 glop_status line_numbers_impl(glop_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t base, const void* d_recs,
-                              uint32_t stride, uint64_t count, uint64_t* d_lines) {
-  if (count == 0) return GLOP_OK;
+                              uint32_t stride, uint64_t count, uint64_t* d_lines,
+                              const uint64_t* d_line_base, uint64_t* d_lf_acc) {
+  if (count == 0 && !d_lf_acc) return GLOP_OK;
+  if (n == 0) {
+    if (count) {
+      ++c->launches;
+      lines_fill_kernel<<<1, 256, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(d_lines), count,
+                                                  reinterpret_cast<const unsigned long long*>(d_line_base));
+      CU(cudaGetLastError());
+    }
+    return GLOP_OK;
+  }
   const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
   const uint64_t nblocks = (n + a + kLineBlock - 1) / kLineBlock;
   TRY(c->lcount.ensure(nblocks * 8));
   TRY(c->lprefix.ensure(nblocks * 8));
   const uint8_t* A = d_text - a;
   const uint32_t grid = (uint32_t)std::min<uint64_t>((nblocks + 7) / 8, 16u * c->num_sms);
-  c->launches += 3;
+  c->launches += 2;
   lf_block_count_kernel<<<grid, 256, 0, c->stream>>>(A, a, n, nblocks, c->lcount.as<unsigned long long>());
   CU(cudaGetLastError());
   size_t tmp = 0;
@@ -718,12 +958,124 @@ glop_status line_numbers_impl(glop_ctx* c, const uint8_t* d_text, uint64_t n, ui
   TRY(c->cub_tmp.ensure(tmp));
   CU(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, c->lcount.as<unsigned long long>(),
                                    c->lprefix.as<unsigned long long>(), (int64_t)nblocks, c->stream));
-  const uint32_t g2 = (uint32_t)std::min<uint64_t>((count + 7) / 8, 16u * c->num_sms);
-  lines_of_kernel<<<g2, 256, 0, c->stream>>>(A, a, base, c->lprefix.as<unsigned long long>(), d_recs, stride, count,
-                                             reinterpret_cast<unsigned long long*>(d_lines));
-  CU(cudaGetLastError());
+  if (count) {
+    ++c->launches;
+    const uint32_t g2 = (uint32_t)std::min<uint64_t>((count + 7) / 8, 16u * c->num_sms);
+    lines_of_kernel<<<g2, 256, 0, c->stream>>>(A, a, base, c->lprefix.as<unsigned long long>(), d_recs, stride, count,
+                                               reinterpret_cast<unsigned long long*>(d_lines),
+                                               reinterpret_cast<const unsigned long long*>(d_line_base));
+    CU(cudaGetLastError());
+  }
+  if (d_lf_acc) {
+    ++c->launches;
+    lf_total_add_kernel<<<1, 1, 0, c->stream>>>(c->lcount.as<unsigned long long>(), c->lprefix.as<unsigned long long>(),
+                                                nblocks, reinterpret_cast<unsigned long long*>(d_lf_acc));
+    CU(cudaGetLastError());
+  }
   return GLOP_OK;
 }
+
+// chunked_ac_scan's result (scan.hpp:207-243) from the exact occurrence
+// list: chunk k = [k*c, (k+1)*c) is walked from the root over
+// [k*c, min(k*c + c + overlap, n)), so it reports exactly the occurrences
+// whose start it owns and whose end it reaches.
+struct AcOwned {
+  unsigned long long c, overlap, n;
+  __host__ __device__ bool operator()(const DevHit& h) const {
+    const unsigned long long own_begin = h.offset / c * c;
+    const unsigned long long scan_end = own_begin + c + overlap < n ? own_begin + c + overlap : n;
+    return h.offset + h.len <= scan_end;
+  }
+};
+
+glop_status chunked_ac_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_text, uint64_t n, uint64_t chunk,
+                            uint64_t overlap, glop_hit* d_out, uint64_t cap, uint64_t* n_out) {
+  *n_out = 0;
+  if (n == 0 || t->empty) return GLOP_OK;
+  uint64_t hcap = std::max<uint64_t>(1 << 16, c->keys_alt.bytes / sizeof(glop_hit));
+  TRY(c->keys_alt.ensure(hcap * sizeof(glop_hit)));
+  uint64_t nh = 0;
+  glop_status s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->keys_alt.as<glop_hit>(), hcap, &nh);
+  if (s == GLOP_ECAPACITY && nh > hcap) {
+    c->keys_alt.release();
+    hcap = nh;
+    TRY(c->keys_alt.ensure(hcap * sizeof(glop_hit)));
+    s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->keys_alt.as<glop_hit>(), hcap, &nh);
+  }
+  if (s != GLOP_OK) return s;
+  if (nh == 0) return GLOP_OK;
+  if (nh > cap) {  // the selection is <= nh: size the output for the worst case
+    *n_out = nh;
+    return fail(GLOP_ECAPACITY, "chunked_ac_scan: output capacity");
+  }
+  const AcOwned pred{chunk ? chunk : std::max<uint64_t>(n, 1), overlap, n};
+  TRY(c->misc.ensure(64));
+  auto* d_sel = c->misc.as<unsigned long long>() + 7;
+  const auto* in = reinterpret_cast<const DevHit*>(c->keys_alt.p);
+  auto* out = reinterpret_cast<DevHit*>(d_out);
+  size_t tmp = 0;
+  CU(cub::DeviceSelect::If(nullptr, tmp, in, out, d_sel, (int64_t)nh, pred, c->stream));
+  TRY(c->cub_tmp.ensure(tmp));
+  CU(cub::DeviceSelect::If(c->cub_tmp.p, tmp, in, out, d_sel, (int64_t)nh, pred, c->stream));
+  ++c->launches;
+  TRY(sync_read(c, d_sel, 8));
+  *n_out = c->h_misc[0];
+  return GLOP_OK;
+}
+
+// The reference's kmp_search loop verbatim on one device thread (kmp.hpp:41-69)
+// for inputs the chunk-parallel DFA cannot take: a failure table that is not
+// the pattern's prefix function, or a pattern of 8,192 bytes or more.
+__global__ void kmp_seq_kernel(const uint8_t* text, unsigned long long n, const uint8_t* p, uint32_t m,
+                               const uint32_t* table, unsigned long long* out, unsigned long long cap,
+                               unsigned long long* status) {
+  unsigned long long found = 0, cmp = 0;
+  uint32_t j = 0;
+  for (unsigned long long i = 0; i < n; ++i) {
+    const uint8_t b = text[i];
+    for (;;) {
+      ++cmp;
+      if (b == p[j]) {
+        ++j;
+        if (j == m) {
+          if (found < cap) out[found] = i + 1 - m;
+          ++found;
+          j = table[m - 1];
+        }
+        break;
+      }
+      if (j == 0) break;
+      j = table[j - 1];
+    }
+  }
+  status[0] = found;
+  status[1] = cmp;
+}
+
+glop_status kmp_seq_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab, const uint8_t* d_text,
+                         uint64_t n, uint64_t* d_out, uint64_t cap, uint64_t* n_offsets, uint64_t* comparisons) {
+  for (uint32_t i = 0; i < m; ++i)
+    if (fail_tab[i] >= m) return fail(GLOP_EINVAL, "kmp_search: failure table entry out of range");
+  TRY(c->kmp_dfa.ensure((size_t)m * 4 + m + 16));
+  auto* d_tab = c->kmp_dfa.as<uint32_t>();
+  auto* d_pat = reinterpret_cast<uint8_t*>(d_tab + m);
+  CU(cudaMemcpyAsync(d_tab, fail_tab, (size_t)m * 4, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(d_pat, pat, m, cudaMemcpyHostToDevice, c->stream));
+  TRY(c->misc.ensure(64));
+  ++c->launches;
+  kmp_seq_kernel<<<1, 1, 0, c->stream>>>(d_text, n, d_pat, m, d_tab, reinterpret_cast<unsigned long long*>(d_out),
+                                         cap, c->misc.as<unsigned long long>());
+  CU(cudaGetLastError());
+  TRY(sync_read(c, c->misc.p, 16));
+  *n_offsets = c->h_misc[0];
+  if (comparisons) *comparisons += c->h_misc[1];
+  if (*n_offsets > cap) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
+  return GLOP_OK;
+}
+
+glop_status pipeline_host(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text, uint64_t n,
+                          uint64_t own, uint64_t base, int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                          uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count);
 
 }  // namespace
 
@@ -770,7 +1122,8 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
-                  &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1], &c->lcount, &c->lprefix, &c->loffs})
+                  &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1], &c->lcount, &c->lprefix, &c->loffs,
+                  &c->hprefix, &c->kcounts, &c->kprefix, &c->keep8, &c->counts_tmp, &c->palerts, &c->plines})
     b->release();
   if (c->cstream) {
     cudaStreamSynchronize(c->cstream);
@@ -781,6 +1134,8 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
     if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
   }
   cudaFreeHost(c->h_misc);
+  for (void* p : c->pin)
+    if (p) cudaFreeHost(p);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   cudaStreamDestroy(c->stream);
@@ -855,10 +1210,33 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         return fail(GLOP_EINVAL, "glop_trie_upload: pattern id with two lengths");
       L = out_flat[o].matched_len;
     }
+  // most hits one start position emits: outputs summed along a root path
+  // (BFS order visits parents first); a pfac8 lane checks up to 4 starts
+  uint32_t max_emits = 0;
+  {
+    std::vector<uint32_t> cum(Q, 0);
+    for (size_t h = 0; h < order.size(); ++h) {
+      const uint32_t s = order[h];
+      max_emits = std::max(max_emits, cum[s]);
+      for (int b = 0; b < 256; ++b) {
+        const int32_t t2 = dense[(size_t)s * 256 + b];
+        if (t2 > 0) cum[t2] = cum[s] + (off2[t2 + 1] - off2[t2]);
+      }
+    }
+  }
   // --- alphabet classes (ascending byte order; class 0 = no edge anywhere)
+  // (all 256 bytes on edges: the identity map, 256 classes -- no byte needs
+  // the "no edge" class, and 257 classes would not fit the u8 map)
   uint8_t cls[256];
   uint32_t C = 1;
-  for (int b = 0; b < 256; ++b) cls[b] = used[b] ? (uint8_t)C++ : 0;
+  for (int b = 0; b < 256; ++b) C += used[b];
+  if (C == 257) {
+    C = 256;
+    for (int b = 0; b < 256; ++b) cls[b] = (uint8_t)b;
+  } else {
+    C = 1;
+    for (int b = 0; b < 256; ++b) cls[b] = used[b] ? (uint8_t)C++ : 0;
+  }
   const bool u16 = Q < 0x8000u;
   const size_t eb = u16 ? 2 : 4;
   const size_t table_bytes = up16((size_t)Q * C * eb);
@@ -1018,6 +1396,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
   t->p8_l1 = bloom2 ? 2 : bits8 ? 1 : 0;
+  t->p8_lane_emits = 4 * max_emits;
+  t->p8_careful = t->p8_lane_emits > kP8Hits - GLOP_P8_FLUSH_AT || getenv("GLOP_P8_CAREFUL");
   t->view.jump_depth = J;
   t->view.jump_cap_log2 = cap_log2;
   t->view.jump_bytes = (uint32_t)jump_bytes;
@@ -1293,6 +1673,7 @@ glop_status glop_last_kernel_ms(glop_ctx* c, float* ms) {
 }
 
 uint64_t glop_ctx_launch_count(glop_ctx* c) { return c ? c->launches : 0; }
+uint64_t glop_ctx_fallback_count(glop_ctx* c) { return c ? c->fallbacks : 0; }
 
 glop_status glop_run_pfac_pipeline(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text,
                                    uint64_t n, int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
@@ -1305,6 +1686,60 @@ glop_status glop_run_pfac_pipeline_shard(glop_ctx* c, const glop_trie* t, const 
                                          const uint8_t* text, uint64_t n, uint64_t own, uint64_t base,
                                          int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
                                          uint64_t* counts, uint64_t* stage1_hits) {
+  return pipeline_host(c, t, r, text, n, own, base, text_on_device, alerts, n_alerts, counts, stage1_hits, nullptr,
+                       nullptr);
+}
+
+glop_status glop_run_pfac_pipeline_lines(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text,
+                                         uint64_t n, int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                                         uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines,
+                                         uint64_t* line_count) {
+  if (!lines || !line_count) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline_lines: null argument");
+  return pipeline_host(c, t, r, text, n, n, 0, text_on_device, alerts, n_alerts, counts, stage1_hits, lines,
+                       line_count);
+}
+
+glop_status glop_chunked_ac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n,
+                                 int text_on_device, uint64_t chunk_size, uint64_t overlap, glop_hit** matches,
+                                 uint64_t* n_matches) {
+  if (!c || !t || !matches || !n_matches) return fail(GLOP_EINVAL, "glop_chunked_ac_scan: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  *matches = nullptr;
+  *n_matches = 0;
+  const uint8_t* d_text = nullptr;
+  TRY(to_device_text(c, text, n, text_on_device, &d_text));
+  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
+  TRY(c->out.ensure(cap * sizeof(glop_hit)));
+  uint64_t total = 0;
+  glop_status s = chunked_ac_impl(c, t, d_text, n, chunk_size, overlap, c->out.as<glop_hit>(), cap, &total);
+  if (s == GLOP_ECAPACITY && total > cap) {
+    c->out.release();
+    cap = total;
+    TRY(c->out.ensure(cap * sizeof(glop_hit)));
+    s = chunked_ac_impl(c, t, d_text, n, chunk_size, overlap, c->out.as<glop_hit>(), cap, &total);
+  }
+  if (s != GLOP_OK) return s;
+  glop_hit* h = static_cast<glop_hit*>(malloc(std::max<uint64_t>(total, 1) * sizeof(glop_hit)));
+  if (!h) return fail(GLOP_ENOMEM, "glop_chunked_ac_scan: host allocation");
+  cudaError_t e = cudaSuccess;
+  if (total) e = cudaMemcpyAsync(h, c->out.p, total * sizeof(glop_hit), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free(h);
+    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  }
+  *matches = h;
+  *n_matches = total;
+  return GLOP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+glop_status pipeline_host(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text, uint64_t n,
+                          uint64_t own, uint64_t base, int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                          uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count) {
   if (!c || !t || !r || !alerts || !n_alerts) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline: null argument");
   if (own > n) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline: own > n");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1312,41 +1747,53 @@ glop_status glop_run_pfac_pipeline_shard(glop_ctx* c, const glop_trie* t, const 
   *alerts = nullptr;
   *n_alerts = 0;
   if (!text_on_device && own > kStreamChunk)
-    return run_pipeline_streamed(c, t, r, text, n, own, base, alerts, n_alerts, counts, stage1_hits);
+    return run_pipeline_streamed(c, t, r, text, n, own, base, alerts, n_alerts, counts, stage1_hits, lines,
+                                 line_count);
   const uint8_t* d_text = nullptr;
   TRY(to_device_text(c, text, n, text_on_device, &d_text));
-  uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
-  TRY(c->out.ensure(cap * sizeof(glop_hit)));
-  uint64_t nh = 0;
-  glop_status s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
-  if (s == GLOP_ECAPACITY && nh > cap) {
-    c->out.release();
-    cap = nh;
-    TRY(c->out.ensure(cap * sizeof(glop_hit)));
-    s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &nh);
+  const uint32_t k = r->view.n_patterns;
+  TRY(c->spill.ensure((size_t)(k + 1) * 8));
+  uint64_t* d_counts = c->spill.as<uint64_t>();
+  TRY(c->palerts.ensure(std::max<size_t>(c->palerts.bytes, (1 << 16) * sizeof(glop_alert))));
+  uint64_t nh = 0, kept = 0, acap = c->palerts.bytes / sizeof(glop_alert);
+  glop_status s = pipeline_device_impl(c, t, r, d_text, n, own, base, nullptr, 0, c->palerts.as<glop_alert>(), acap,
+                                       d_counts, &nh, &kept);
+  if (s == GLOP_ECAPACITY && kept > acap) {
+    c->palerts.release();
+    TRY(c->palerts.ensure(kept * sizeof(glop_alert)));
+    s = pipeline_device_impl(c, t, r, d_text, n, own, base, nullptr, 0, c->palerts.as<glop_alert>(), kept, d_counts,
+                             &nh, &kept);
   }
   if (s != GLOP_OK) return s;
   if (stage1_hits) *stage1_hits = nh;
-  const uint32_t k = r->view.n_patterns;
-  TRY(c->alerts.ensure(std::max<uint64_t>(nh, 1) * sizeof(glop_alert) + (size_t)(k + 1) * 8));
-  glop_alert* d_alerts = c->alerts.as<glop_alert>();
-  uint64_t* d_counts = reinterpret_cast<uint64_t*>(d_alerts + std::max<uint64_t>(nh, 1));
-  CU(cudaMemsetAsync(d_counts, 0, (size_t)k * 8 + 8, c->stream));
-  uint64_t kept = 0;
-  TRY(verify_device_impl(c, r, d_text, n, base, c->out.as<glop_hit>(), nh, d_alerts, &kept, d_counts));
-  glop_alert* a = static_cast<glop_alert*>(malloc(std::max<uint64_t>(kept, 1) * sizeof(glop_alert)));
-  if (!a) return fail(GLOP_ENOMEM, "glop_run_pfac_pipeline: host allocation");
-  cudaError_t e = cudaSuccess;
-  if (kept) e = cudaMemcpyAsync(a, d_alerts, kept * sizeof(glop_alert), cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess && counts) e = cudaMemcpyAsync(counts, d_counts, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-  if (e != cudaSuccess) {
-    free(a);
-    return fail(GLOP_ECUDA, cudaGetErrorString(e));
+  uint64_t* d_lf = nullptr;
+  if (lines || line_count) {  // LineIndex(text) on the device (own == n, base == 0 here)
+    TRY(c->plines.ensure(kept * 8 + 16));
+    d_lf = c->plines.as<uint64_t>() + kept + 1;
+    CU(cudaMemsetAsync(d_lf, 0, 8, c->stream));
+    TRY(line_numbers_impl(c, d_text, n, base, c->palerts.p, sizeof(glop_alert), kept, c->plines.as<uint64_t>(),
+                          nullptr, d_lf));
   }
-  *alerts = a;
+  TRY(alerts_to_host(c, c->palerts.as<glop_alert>(), kept, d_counts, k, counts, alerts, c->plines.as<uint64_t>(),
+                     lines, d_lf, line_count));
   *n_alerts = kept;
   return GLOP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+glop_status glop_run_pfac_pipeline_device(glop_ctx* c, const glop_trie* t, const glop_rules* r,
+                                          const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                          glop_hit* d_hits, uint64_t hit_cap, glop_alert* d_alerts,
+                                          uint64_t alert_cap, uint64_t* d_counts, uint64_t* n_hits,
+                                          uint64_t* n_alerts) {
+  if (!c || !t || !r || !n_hits || !n_alerts || (!d_alerts && alert_cap))
+    return fail(GLOP_EINVAL, "glop_run_pfac_pipeline_device: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  return pipeline_device_impl(c, t, r, d_text, n, own, base, d_hits, hit_cap, d_alerts, alert_cap, d_counts, n_hits,
+                              n_alerts);
 }
 
 glop_status glop_line_numbers_device(glop_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t base,
@@ -1355,7 +1802,7 @@ glop_status glop_line_numbers_device(glop_ctx* c, const uint8_t* d_text, uint64_
     return fail(GLOP_EINVAL, "glop_line_numbers_device: bad argument");
   std::lock_guard<std::mutex> lk(c->mu);
   Dev g(c->device);
-  return line_numbers_impl(c, d_text, n, base, d_records, stride, count, d_lines);
+  return line_numbers_impl(c, d_text, n, base, d_records, stride, count, d_lines, nullptr, nullptr);
 }
 
 glop_status glop_line_numbers(glop_ctx* c, const uint8_t* text, uint64_t n, int text_on_device,
@@ -1371,7 +1818,7 @@ glop_status glop_line_numbers(glop_ctx* c, const uint8_t* text, uint64_t n, int 
   TRY(c->loffs.ensure(count * 16));
   uint64_t* d_offs = c->loffs.as<uint64_t>();
   CU(cudaMemcpyAsync(d_offs, offsets, count * 8, cudaMemcpyHostToDevice, c->stream));
-  TRY(line_numbers_impl(c, d_text, n, 0, d_offs, 8, count, d_offs + count));
+  TRY(line_numbers_impl(c, d_text, n, 0, d_offs, 8, count, d_offs + count, nullptr, nullptr));
   CU(cudaMemcpyAsync(lines, d_offs + count, count * 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return GLOP_OK;

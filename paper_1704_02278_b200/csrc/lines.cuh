@@ -48,12 +48,15 @@ __global__ void __launch_bounds__(256) lf_block_count_kernel(const uint8_t* A, u
   }
 }
 
-// lines[i] = 1 + LFs in text[0, offsets[i] - base) (warp per offset).
+// lines[i] = 1 + LFs in text[0, offsets[i] - base) (+ *line_base: LFs of
+// earlier streamed chunks) (warp per offset).
 __global__ void __launch_bounds__(256) lines_of_kernel(const uint8_t* A, uint32_t a, unsigned long long base,
                                                        const unsigned long long* prefix, const void* recs,
                                                        uint32_t stride, unsigned long long count,
-                                                       unsigned long long* lines) {
+                                                       unsigned long long* lines,
+                                                       const unsigned long long* line_base) {
   const uint32_t lane = threadIdx.x & 31;
+  const unsigned long long lb = line_base ? *line_base : 0;
   for (unsigned long long i = (blockIdx.x * 256ull + threadIdx.x) / 32; i < count;
        i += (unsigned long long)gridDim.x * 8) {
     const unsigned long long off =
@@ -61,8 +64,21 @@ __global__ void __launch_bounds__(256) lines_of_kernel(const uint8_t* A, uint32_
     const unsigned long long b = off / kLineBlock;
     uint32_t c = lf_count_range(A, max(b * kLineBlock, (unsigned long long)a), off, lane, 32);
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) lines[i] = prefix[b] + c + 1;
+    if (lane == 0) lines[i] = prefix[b] + c + 1 + lb;
   }
+}
+
+// *acc += LFs of the whole text (last block prefix + last block count).
+__global__ void lf_total_add_kernel(const unsigned long long* counts, const unsigned long long* prefix,
+                                    unsigned long long nblocks, unsigned long long* acc) {
+  *acc += prefix[nblocks - 1] + counts[nblocks - 1];
+}
+
+// Lines of offsets into an empty text: 1 (+ *line_base).
+__global__ void lines_fill_kernel(unsigned long long* lines, unsigned long long count,
+                                  const unsigned long long* line_base) {
+  const unsigned long long lb = line_base ? *line_base : 0;
+  for (unsigned long long i = threadIdx.x; i < count; i += blockDim.x) lines[i] = 1 + lb;
 }
 
 }  // namespace glop

@@ -194,7 +194,13 @@ __device__ __forceinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb
 
 // kL1: 0 byte d-mask buckets; 1 one-bit buckets; 2 one-bit buckets and a
 // second level-2 bitmap probe (prefix_bit2_32) for large prefix sets.
-template <bool kWalk, int kL1, typename Entry>
+// kCareful: a replayed lane always starts with an empty hit buffer.  Without
+// it a replayed lane may start with up to GLOP_P8_FLUSH_AT keys, which is
+// exact but sends a lane emitting more than kP8Hits - GLOP_P8_FLUSH_AT ids to
+// the global-key fallback; the host picks kCareful for automata where one
+// lane can emit that many (glop_trie_upload: p8_lane_emits), because its
+// extra flush site costs ~3.5% of the k=1,000 scan (measured: 2.29 -> 2.37 ms).
+template <bool kWalk, int kL1, typename Entry, bool kCareful>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
@@ -431,10 +437,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         // ---- exact check of the survivors; a pass that overflows the hit
         // buffer is dropped and replayed lane by lane (lanes hold ascending
         // candidates), flushing in between
-        const uint32_t nb0 = *s_nh;  // <= GLOP_P8_FLUSH_AT
-        uint32_t mask = runmask, redo = 0;
-        bool first = true;
-        for (;;) {
+        auto run_lanes = [&](uint32_t mask) {
           if ((mask >> lane) & 1u) {
             uint32_t sv = surv;
             while (sv) {
@@ -447,19 +450,46 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           __syncwarp();
           const uint32_t nb = *s_nh;
           __syncwarp();
+          return nb;
+        };
+        const uint32_t nb0 = *s_nh;  // <= GLOP_P8_FLUSH_AT
+        if constexpr (kCareful) {
+          const uint32_t nb = run_lanes(runmask);
           if (p.mode == 0) {
-            if (first && nb > kP8Hits) {
+            if (nb > kP8Hits) {
+              // replay: flush the earlier rounds' keys, then run each lane
+              // alone and flush after it
               if (lane == 0) *s_nh = nb0;
               __syncwarp();
-              redo = runmask;
+              if (nb0) flush(nb0);
+#pragma unroll 1
+              for (uint32_t redo = runmask; redo; redo &= redo - 1) {
+                const uint32_t nl = run_lanes(redo & (0u - redo));
+                if (nl) flush(nl);
+              }
             } else if (nb > GLOP_P8_FLUSH_AT) {
               flush(nb);
             }
           }
-          first = false;
-          if (!redo) break;
-          mask = redo & (0u - redo);
-          redo &= redo - 1;
+        } else {
+          uint32_t mask = runmask, redo = 0;
+          bool first = true;
+          for (;;) {
+            const uint32_t nb = run_lanes(mask);
+            if (p.mode == 0) {
+              if (first && nb > kP8Hits) {  // replay lane by lane from the earlier rounds' keys
+                if (lane == 0) *s_nh = nb0;
+                __syncwarp();
+                redo = runmask;
+              } else if (nb > GLOP_P8_FLUSH_AT) {
+                flush(nb);
+              }
+            }
+            first = false;
+            if (!redo) break;
+            mask = redo & (0u - redo);
+            redo &= redo - 1;
+          }
         }
       }
     }

@@ -1,0 +1,186 @@
+// pipeline.cuh -- the device half of run_engine_scan's PFAC branch
+// (pipeline.hpp:86-97) after pfac8_kernel, enqueued without host round trips:
+//
+//   pfac8_kernel        per-warp staging regions (already in text order)
+//   p8_prefix_kernel    exclusive prefix of the region hit counts; zeroes the
+//                       per-pattern counts (no separate memset)
+//   p8_keep_kernel      stage 2 only (some pattern longer than the prefix):
+//                       the suffix compare of verify_hits (verify.hpp:78-87)
+//                       per hit -> keep flags + kept count per region
+//   p8_prefix_kernel    exclusive prefix of the kept counts (stage 2 only)
+//   p8_emit_kernel      stable compaction of the kept hits into alerts in
+//                       (offset, rule_id) order (verify.hpp:100-103: the
+//                       regions are already sorted), the optional ordered hit
+//                       list, and the per-pattern alert histogram
+//
+// The host reads one 64-byte status block at the end (totals, the scan's
+// overflow flags, verify's logic_error flag); a scan that overflowed a
+// staging region or a hit buffer is redone by the general path.
+#pragma once
+#include "glop_kernels.cuh"
+
+namespace glop {
+
+// Status words in the scan's g_count block (u64 each).
+enum : uint32_t { kStTotal = 0, kStFlags = 1, kStMaxRegion = 2, kStKeys = 3, kStHits = 4, kStKept = 5,
+                  kStVerify = 6 };
+
+// Exclusive prefix of min(counts[g], region) over n regions (one CTA), the
+// sum to *total, and zeroes zero[0, nzero) (the per-pattern counts).
+__global__ void __launch_bounds__(1024) p8_prefix_kernel(const unsigned long long* counts, uint32_t n,
+                                                         unsigned long long region, unsigned long long* prefix,
+                                                         unsigned long long* total, unsigned long long* zero,
+                                                         uint32_t nzero) {
+  __shared__ unsigned long long part[1024];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < nzero; i += 1024) zero[i] = 0;
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t b = tid * per, e = min(n, b + per);
+  unsigned long long s = 0;
+  for (uint32_t i = b; i < e; ++i) s += min(counts[i], region);
+  part[tid] = s;
+  __syncthreads();
+  for (uint32_t off = 1; off < 1024; off <<= 1) {
+    const unsigned long long v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  unsigned long long run = part[tid] - s;
+  for (uint32_t i = b; i < e; ++i) {
+    prefix[i] = run;
+    run += min(counts[i], region);
+  }
+  if (tid == 1023) *total = part[1023];
+}
+
+// Stage 2 of verify_hits for hits staged per region: keep[g * region + i]
+// and the kept count of region g.  Flag 1 of *vflags: a hit past the end of
+// the text or naming an unknown pattern (the reference's logic_error /
+// rules.patterns.at(), verify.hpp:76-79).  One CTA per region, grid-stride.
+__global__ void __launch_bounds__(256) p8_keep_kernel(const DevRules r, const uint8_t* text,
+                                                      unsigned long long base, unsigned long long n,
+                                                      const unsigned long long* counts, uint32_t regions,
+                                                      unsigned long long region, const DevHit* staging,
+                                                      uint8_t* keep, unsigned long long* kcounts,
+                                                      unsigned long long* vflags) {
+  __shared__ uint32_t s_cnt;
+  for (uint32_t g = blockIdx.x; g < regions; g += gridDim.x) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const unsigned long long c = min(counts[g], region);
+    const DevHit* src = staging + (unsigned long long)g * region;
+    uint8_t* kp = keep + (unsigned long long)g * region;
+    uint32_t mine = 0, bad = 0;
+    for (unsigned long long i = threadIdx.x; i < c; i += blockDim.x) {
+      const DevHit x = src[i];
+      uint32_t ok = 0;
+      if (x.offset < base || x.offset + x.len > base + n || x.pid >= r.n_patterns) {
+        bad = 1;
+      } else {
+        const unsigned long long pb = r.off[x.pid], plen = r.off[x.pid + 1] - pb;
+        if (plen <= r.prefix_len) {
+          ok = 1;
+        } else if (x.offset + plen <= base + n) {
+          ok = 1;
+          const uint8_t* t = text + (x.offset - base);
+          for (unsigned long long k = x.len; k < plen; ++k)
+            if (t[k] != r.bytes[pb + k]) {
+              ok = 0;
+              break;
+            }
+        }
+      }
+      kp[i] = (uint8_t)ok;
+      mine += ok;
+    }
+    if (bad) atomicOr(reinterpret_cast<unsigned int*>(vflags), 1u);
+    for (uint32_t o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) kcounts[g] = s_cnt;
+    __syncthreads();
+  }
+}
+
+// Region hits -> alerts (+ optionally the ordered hit list).  kStage2:
+// compaction by the keep flags at kprefix[g]; otherwise every hit is an
+// alert at hprefix[g] + i (all patterns fit in the prefix: verify.hpp:80).
+// The per-pattern histogram lives in shared memory (hist_bins = n_patterns,
+// flushed once per CTA) when it fits, else global atomics.  Without stage 2
+// the bounds / id checks happen here (flag 1 of *vflags).
+template <bool kStage2>
+__global__ void __launch_bounds__(1024) p8_emit_kernel(const DevRules r, unsigned long long base,
+                                                       unsigned long long n, const unsigned long long* counts,
+                                                       uint32_t regions, unsigned long long region,
+                                                       const DevHit* staging, const uint8_t* keep,
+                                                       const unsigned long long* hprefix,
+                                                       const unsigned long long* kprefix, DevHit* hits_out,
+                                                       unsigned long long hit_cap, DevAlert* out,
+                                                       unsigned long long alert_cap, unsigned long long* gcounts,
+                                                       uint32_t hist_bins, unsigned long long* vflags) {
+  extern __shared__ uint32_t hist[];
+  __shared__ uint32_t warp_base[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (uint32_t i = tid; i < hist_bins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  uint32_t bad = 0;
+  for (uint32_t g = blockIdx.x; g < regions; g += gridDim.x) {
+    const unsigned long long c = min(counts[g], region), hp = hprefix[g];
+    const DevHit* src = staging + (unsigned long long)g * region;
+    unsigned long long dst0 = kStage2 ? kprefix[g] : hp;
+    for (unsigned long long i0 = 0; i0 < c; i0 += blockDim.x) {
+      const unsigned long long i = i0 + tid;
+      DevHit x{};
+      uint32_t ok = 0;
+      if (i < c) {
+        x = src[i];
+        if (hits_out && hp + i < hit_cap) hits_out[hp + i] = x;
+        if (kStage2) {
+          ok = keep[(unsigned long long)g * region + i];
+        } else {
+          ok = 1;
+          if (x.offset < base || x.offset + x.len > base + n || x.pid >= r.n_patterns) bad = 1, ok = 0;
+        }
+      }
+      unsigned long long dst = dst0 + i;
+      if (kStage2) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) warp_base[w] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+        for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+          const uint32_t v = warp_base[k];
+          before += k < w ? v : 0;
+          all += v;
+        }
+        dst = dst0 + before + __popc(bal & ((1u << lane) - 1));
+        dst0 += all;
+        __syncthreads();
+      }
+      if (ok) {
+        if (dst < alert_cap) {
+          DevAlert a;
+          a.offset = x.offset;
+          a.rule_id = x.pid;
+          a.pattern_len = (uint32_t)(r.off[x.pid + 1] - r.off[x.pid]);
+          out[dst] = a;
+        }
+        if (hist_bins) atomicAdd(&hist[x.pid], 1u);
+        else atomicAdd(gcounts + x.pid, 1ull);
+      }
+    }
+  }
+  if (bad) atomicOr(reinterpret_cast<unsigned int*>(vflags), 1u);
+  __syncthreads();
+  for (uint32_t i = tid; i < hist_bins; i += blockDim.x)
+    if (hist[i]) atomicAdd(gcounts + i, (unsigned long long)hist[i]);
+}
+
+// acc[i] += add[i] (per-pattern counts of one streamed chunk).
+__global__ void add_u64_kernel(unsigned long long* acc, const unsigned long long* add, uint32_t k) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) acc[i] += add[i];
+}
+
+}  // namespace glop

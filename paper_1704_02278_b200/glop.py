@@ -94,6 +94,10 @@ _sig("glop_run_pfac_pipeline_shard", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c
 _sig("glop_last_kernel_ms", vp, C.POINTER(C.c_float))
 _lib.glop_ctx_launch_count.argtypes = [vp]
 _lib.glop_ctx_launch_count.restype = C.c_uint64
+_lib.glop_ctx_fallback_count.argtypes = [vp]
+_lib.glop_ctx_fallback_count.restype = C.c_uint64
+_sig("glop_run_pfac_pipeline_device", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64, vp,
+     C.c_uint64, vp, u64p, u64p)
 _sig("glop_rules_upload", vp, u8p, u64p, C.c_uint32, C.c_uint64, C.POINTER(vp))
 _sig("glop_rules_destroy", vp)
 _sig("glop_verify_hits", vp, vp, vp, C.c_uint64, C.c_int, vp, C.c_uint64, C.c_int, C.POINTER(vp), u64p, u64p)
@@ -365,6 +369,22 @@ class Context:
                                                  cnt.ctypes.data_as(u64p), C.byref(s1)), "run_pfac_pipeline")
         return _take(p, na.value, ALERT_DTYPE), cnt[:rules.n_patterns], s1.value
 
+    def run_pfac_pipeline_device(self, trie: DeviceTrie, rules: DeviceRules, d_text: int, n: int, d_alerts: int,
+                                 alert_cap: int, d_counts: int | None = None, own: int | None = None, base: int = 0,
+                                 d_hits: int | None = None, hit_cap: int = 0):
+        """Device-resident scan + verify + counts (one host wait): returns
+        (n_hits, n_alerts); alerts / counts / optional hits stay on the device."""
+        nh, na = C.c_uint64(), C.c_uint64()
+        _check(_lib.glop_run_pfac_pipeline_device(self.h, trie.h, rules.h, d_text, n, n if own is None else own, base,
+                                                  d_hits, hit_cap, d_alerts, alert_cap, d_counts, C.byref(nh),
+                                                  C.byref(na)), "run_pfac_pipeline_device")
+        return nh.value, na.value
+
+    @property
+    def fallbacks(self) -> int:
+        """Scans on this context that took the exact global-key fallback."""
+        return int(_lib.glop_ctx_fallback_count(self.h))
+
     def line_numbers(self, text, offsets) -> np.ndarray:
         """LineIndex(text).line_of(o) for every o (verify.hpp:40-64), on the device."""
         t = _u8(text)
@@ -449,3 +469,51 @@ class Context:
 
     def gen_payload_device(self, d_out: int, n: int, seed: int, begin: int = 0):
         _check(_lib.glop_gen_payload_device(self.h, d_out, begin, n, seed), "gen_payload_device")
+
+
+# ---------------------------------------------------------------- drop-in engine
+class Engine:
+    """The drop-in C++ run_engine_scan (include/logtrawl/pipeline.hpp) through
+    libglop_engine.so -- the call a reference C++ caller makes, for bench.py's
+    e2e_dropin leg and FFI callers.  engine: "kmp", "pfac_dense",
+    "pfac_compact" (default), "ac_chunked"."""
+
+    ENGINES = {"kmp": 0, "pfac_dense": 1, "pfac_compact": 2, "ac_chunked": 3}
+
+    def __init__(self, patterns):
+        path = os.path.join(HERE, "libglop_engine.so")
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is not built (make -C paper_1704_02278_b200/cli)")
+        self.lib = C.CDLL(path)
+        self.lib.glop_engine_rules_create.restype = vp
+        self.lib.glop_engine_rules_create.argtypes = [u8p, u64p, C.c_uint32]
+        self.lib.glop_engine_rules_destroy.argtypes = [vp]
+        self.lib.glop_engine_last_error.restype = C.c_char_p
+        self.lib.glop_engine_run.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                             C.POINTER(vp), C.POINTER(vp), u64p, u64p]
+        pat, off = pack_patterns(list(patterns))
+        self.h = self.lib.glop_engine_rules_create(pat.ctypes.data_as(u8p), off.ctypes.data_as(u64p), len(patterns))
+
+    def run(self, text_ptr: int, n: int, engine: str = "pfac_compact", prefix_len: int = 8, chunk_size: int = 0,
+            lines: bool = False):
+        """(alerts ALERT_DTYPE, lines or None, stage1_hits) of run_engine_scan
+        over the host bytes at text_ptr (pageable or pinned)."""
+        a, ln, na, s1 = vp(), vp(), C.c_uint64(), C.c_uint64()
+        rc = self.lib.glop_engine_run(self.h, text_ptr, n, self.ENGINES[engine], prefix_len, chunk_size,
+                                      1 if lines else 0, C.byref(a), C.byref(ln), C.byref(na), C.byref(s1))
+        if rc:
+            raise _ERRORS.get({1: 1, 2: 2, 3: 3}.get(rc, 4), GlopError)(
+                "run_engine_scan: " + (self.lib.glop_engine_last_error() or b"").decode())
+        alerts = _take(a, na.value, ALERT_DTYPE)
+        return alerts, (_take(ln, na.value, np.uint64) if lines else None), s1.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.glop_engine_rules_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

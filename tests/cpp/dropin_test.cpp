@@ -164,6 +164,126 @@ int main() {
       CHECK(naive_scan(text, r) == truth);
     }
   }
+  // test_scan.cpp:90-146 / acceptance.cpp:80-93: chunked AC, the boundary
+  // problem and its overlap fix, on the device
+  {
+    RuleSet r = make_rules({"HIS", "SHE"});
+    Automaton ac = build_ac_automaton(r);
+    const std::string text = "XXHISXX";
+    auto lost = chunked_ac_scan(text, ac, {.workers = 1, .chunk_size = 4, .overlap = 0});
+    CHECK(lost.empty());
+    auto found = chunked_ac_scan(text, ac, {.workers = 1, .chunk_size = 4, .overlap = 2});
+    CHECK(found == (std::vector<Match>{{2, 0}}));
+    CHECK(found == chunked_ac_scan(text, ac, {.workers = 1, .chunk_size = text.size(), .overlap = 0}));
+    Automaton aba = build_ac_automaton(make_rules({"ABA"}));
+    auto whole = chunked_ac_scan("ABABA", aba, {.workers = 1, .chunk_size = 5, .overlap = 0});
+    CHECK(whole == (std::vector<Match>{{0, 0}, {2, 0}}));
+    for (std::size_t ov : {0u, 1u, 10u}) CHECK(chunked_ac_scan("ABABA", aba, {.chunk_size = 100, .overlap = ov}) == whole);
+    CHECK(throws<std::invalid_argument>([&] {
+      chunked_ac_scan("x", build_failureless_trie(truncate_prefixes(r, 8)), {});
+    }));
+    // random inputs, lossless (overlap >= max_len - 1) and lossy overlaps,
+    // against the ownership rule restated by brute force (scan.hpp:224-233)
+    std::mt19937 rng(13);
+    for (int trial = 0; trial < 100; ++trial) {
+      const bool full = trial % 2;
+      std::set<std::string> used;
+      std::vector<std::string> pats;
+      while (pats.size() < 8) {
+        std::string b;
+        const std::size_t len = 1 + rng() % 8;
+        for (std::size_t j = 0; j < len; ++j) b.push_back(full ? char(rng() & 0xFF) : char('A' + rng() % 4));
+        if (used.insert(b).second) pats.push_back(b);
+      }
+      std::string text;
+      for (std::size_t i = 0; i < 2048; ++i) text.push_back(full ? char(rng() & 0xFF) : char('A' + rng() % 4));
+      RuleSet rr = make_rules(pats);
+      Automaton a = build_ac_automaton(rr, trial % 3 ? Backend::dense : Backend::compact);
+      const auto truth = brute(text, rr);
+      CHECK(chunked_ac_scan(text, a, {.chunk_size = text.size(), .overlap = 0}) == truth);
+      const std::size_t chunk = 1 + rng() % 64;
+      const std::size_t overlap = trial % 4 == 3 ? rng() % rr.max_len : rr.max_len - 1 + rng() % 8;
+      std::vector<Match> expect;
+      for (const Match& m : truth) {
+        const std::size_t own = m.offset / chunk * chunk;
+        if (m.offset + rr.patterns[m.pattern_id].bytes.size() <= std::min(own + chunk + overlap, text.size()))
+          expect.push_back(m);
+      }
+      CHECK(chunked_ac_scan(text, a, {.workers = static_cast<unsigned>(1 + rng() % 8), .chunk_size = chunk, .overlap = overlap}) == expect);
+      if (overlap >= rr.max_len - 1) CHECK(expect == truth);
+    }
+  }
+  // run_engine_scan with a LineIndex: lines from the device pipeline equal the
+  // host index (pipeline.hpp:49-100, verify.hpp:40-64); stage-1 counts
+  {
+    std::string text;
+    std::mt19937 rng(77);
+    for (int i = 0; i < 20000; ++i) text += (rng() % 5 == 0) ? "Failed password for root\n" : "ok line " + std::to_string(rng()) + "\n";
+    RuleSet r = make_rules({"Failed password for root", "ok line 1", "ok line 12", "root\nok"});
+    LineIndex idx(text);
+    for (EngineKind e : {EngineKind::pfac_dense, EngineKind::pfac_compact}) {
+      EngineConfig cfg;
+      cfg.engine = e;
+      ScanReport rep = run_engine_scan(text, r, cfg, &idx);
+      CHECK(matches_of(rep.alerts) == brute(text, r));
+      bool lines_ok = !rep.alerts.empty();
+      for (const Alert& a : rep.alerts) lines_ok = lines_ok && a.line == idx.line_of(a.offset) && a.line > 0;
+      CHECK(lines_ok);
+      const PrefixSet ps = truncate_prefixes(r, cfg.prefix_len);
+      CHECK(rep.stage1_hits == pfac_scan(text, build_failureless_trie(ps)).size());
+      CHECK(rep.stage1_rejected == rep.stage1_hits - rep.total_matches && rep.bytes_scanned == text.size());
+      // a LineIndex of another text keeps its own answers
+      LineIndex other("a\nb\n");
+      for (const Alert& a : run_engine_scan(text, r, cfg, &other).alerts) lines_ok = lines_ok && a.line == other.line_of(a.offset);
+      CHECK(lines_ok);
+    }
+  }
+  // verify_hits looks patterns up by position and reports their ids
+  // (verify.hpp:78, :91): a RuleSet whose ids are not positions
+  {
+    RuleSet r;
+    r.patterns = {{7, "seven", "GETPASSWORD"}, {3, "three", "root"}};
+    r.max_len = 11;
+    PrefixSet ps = truncate_prefixes(make_rules({"GETPASSWORD", "root"}), 8);
+    auto al = verify_hits("rootGETPASSWORD", {{0, 1, 4}, {4, 0, 8}}, ps, r);
+    CHECK(al.size() == 2 && al[0].rule_id == 3 && al[0].rule_name == "three" && al[1].rule_id == 7 &&
+          al[1].pattern_len == 11);
+    auto same_off = verify_hits("rootroot", {{0, 0, 4}, {0, 1, 4}}, truncate_prefixes(make_rules({"root", "root"}), 8),
+                                RuleSet{{{9, "a", "root"}, {2, "b", "root"}}, 4});
+    CHECK(same_off.size() == 2 && same_off[0].rule_id == 2 && same_off[1].rule_id == 9);  // sorted by (offset, rule_id)
+    CHECK(throws<std::logic_error>([&] { verify_hits("rootroot", {{0, 5, 4}}, ps, r); }));  // patterns.at()
+  }
+  // kmp_search runs the given failure table as the reference does, canonical
+  // or not (kmp.hpp:41-69), and long patterns
+  {
+    auto seq = [](const std::string& t, const std::string& p, const std::vector<std::uint32_t>& tab, std::uint64_t& cmp) {
+      std::vector<std::size_t> out;
+      std::size_t j = 0;
+      for (std::size_t i = 0; i < t.size(); ++i)
+        for (;;) {
+          ++cmp;
+          if (t[i] == p[j]) {
+            if (++j == p.size()) out.push_back(i + 1 - p.size()), j = tab[p.size() - 1];
+            break;
+          }
+          if (j == 0) break;
+          j = tab[j - 1];
+        }
+      return out;
+    };
+    const std::string text = "AABAABAABAAAABAABAAB";
+    Pattern aab{0, "p", "AAB"};
+    FailureTable zero{0, {0, 0, 0}};
+    std::uint64_t c1 = 0, c2 = 0;
+    CHECK(kmp_search(text, aab, zero, &c1) == seq(text, "AAB", zero.table, c2) && c1 == c2);
+    std::string lp(9000, 'x');
+    lp.back() = 'y';
+    std::string lt = std::string(20000, 'x') + "y" + lp + "zz";
+    Pattern longp{0, "L", lp};
+    FailureTable ft = build_failure_table(longp);
+    c1 = c2 = 0;
+    CHECK(kmp_search(lt, longp, ft, &c1) == seq(lt, lp, ft.table, c2) && c1 == c2 && c1 > 0);
+  }
   std::printf("%s (%d failure%s)\n", failures ? "FAILED" : "OK", failures, failures == 1 ? "" : "s");
   return failures;
 }
