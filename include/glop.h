@@ -122,6 +122,12 @@ glop_status glop_trie_get_info(const glop_trie* trie, glop_trie_info* info);
 glop_status glop_pfac_scan(glop_ctx* ctx, const glop_trie* trie, const uint8_t* text, uint64_t n,
                            int text_on_device, glop_hit** hits, uint64_t* n_hits);
 
+/* Shard form: text covers global offsets [base, base+n); only starts in
+ * [base, base+own) are reported (the bytes past own are the halo). */
+glop_status glop_pfac_scan_shard(glop_ctx* ctx, const glop_trie* trie, const uint8_t* text, uint64_t n,
+                                 uint64_t own, uint64_t base, int text_on_device, glop_hit** hits,
+                                 uint64_t* n_hits);
+
 /* Device-resident form for shards and pipelines: reads text[0, n) (device),
  * reports only starts in [0, own) (own <= n; the bytes [own, n) are the halo),
  * adds `base` to every reported offset, and writes the sorted hits to
@@ -172,6 +178,16 @@ glop_status glop_run_pfac_pipeline_lines(glop_ctx* ctx, const glop_trie* trie, c
                                          const uint8_t* text, uint64_t n, int text_on_device, glop_alert** alerts,
                                          uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits,
                                          uint64_t** lines, uint64_t* line_count);
+
+/* Shard form of the above: lines[i] counts lines within the shard's owned
+ * bytes [0, own) (1 + LFs of text[0, alerts[i].offset - base)) and
+ * *line_count = 1 + LF bytes in text[0, own); a caller adds the LFs of the
+ * shards before this one (glop_group_run_pfac_pipeline does). */
+glop_status glop_run_pfac_pipeline_shard_lines(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules,
+                                               const uint8_t* text, uint64_t n, uint64_t own, uint64_t base,
+                                               int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                                               uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines,
+                                               uint64_t* line_count);
 
 /* Fully device-resident form (the bench step): d_text holds global offsets
  * [base, base+n); starts [base, base+own) are scanned.  Writes the sorted
@@ -249,6 +265,17 @@ glop_status glop_line_numbers_device(glop_ctx* ctx, const uint8_t* d_text, uint6
 glop_status glop_kmp_search(glop_ctx* ctx, const uint8_t* p, uint32_t m, const uint32_t* failure,
                             const uint8_t* text, uint64_t n, int text_on_device, uint64_t** offsets,
                             uint64_t* n_offsets, uint64_t* comparisons);
+/* Host-facing shard form: text = global offsets [base, base+n); starts at
+ * local positions [skip, own) are reported (as base + start) and the
+ * comparisons the sequential scan makes at positions [skip, own) are added.
+ * Exact when skip = 0 is the true text start or skip >= m - 1 (a left context
+ * from which the KMP state is recovered); shards [lo_g, hi_g) read with
+ * min(lo_g, m-1) bytes of left context and m-1 bytes of right halo sum to the
+ * whole-text result, comparisons included. */
+glop_status glop_kmp_search_shard(glop_ctx* ctx, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                  const uint8_t* text, uint64_t n, uint64_t skip, uint64_t own, uint64_t base,
+                                  int text_on_device, uint64_t** offsets, uint64_t* n_offsets,
+                                  uint64_t* comparisons);
 /* Shard form: d_text holds global offsets [base, base+n); reports the
  * starts in [0, own) (matches may end in the halo [own, own+m-1)), adds
  * `base` to each, and counts the comparisons the sequential scan makes at
@@ -257,6 +284,53 @@ glop_status glop_kmp_search_device(glop_ctx* ctx, const uint8_t* p, uint32_t m,
                                    const uint32_t* failure, const uint8_t* d_text, uint64_t n,
                                    uint64_t own, uint64_t base, uint64_t* d_out, uint64_t cap,
                                    uint64_t* n_offsets, uint64_t* comparisons);
+
+/* ---- multi-GPU group ------------------------------------------
+ * One context per member device; `devices` may repeat a device (N contexts on
+ * one GPU exercise the N-way split on a one-GPU box); devices == NULL takes
+ * the first n_devices visible devices (n_devices <= 0: all of them).  A group
+ * call splits the text into contiguous shards (member g owns starts
+ * [lo_g, lo_g + own_g) and reads a halo of max(trie depth, longest pattern)
+ * - 1 bytes past them -- scan.hpp:59-79 ranges, scan.hpp:230-232 ownership),
+ * runs each shard on its member's stream from its own host thread, and merges
+ * in rank order: results are byte-identical to one context's.  Shards are at
+ * least GLOP_GROUP_MIN_SHARD bytes (default 64 MiB), so small texts use fewer
+ * members.  Host text only (pageable or pinned); results are library-owned
+ * host arrays (glop_free). */
+typedef struct glop_group glop_group;
+typedef struct glop_group_trie glop_group_trie;
+typedef struct glop_group_rules glop_group_rules;
+glop_status glop_group_create(const int* devices, int n_devices, glop_group** out);
+glop_status glop_group_destroy(glop_group* group);
+int glop_group_size(const glop_group* group);
+glop_ctx* glop_group_ctx(glop_group* group, int member);
+glop_status glop_group_trie_upload(glop_group* group, const int32_t* dense_table, uint32_t state_count,
+                                   const uint32_t* out_offsets, const glop_output* out_flat, glop_group_trie** out);
+glop_trie* glop_group_trie_member(glop_group_trie* trie, int member);
+glop_status glop_group_trie_destroy(glop_group_trie* trie);
+glop_status glop_group_rules_upload(glop_group* group, const uint8_t* bytes, const uint64_t* off, uint32_t n_patterns,
+                                    uint64_t prefix_len, glop_group_rules** out);
+glop_rules* glop_group_rules_member(glop_group_rules* rules, int member);
+glop_status glop_group_rules_destroy(glop_group_rules* rules);
+/* pfac_scan (scan.hpp:177-202) over all members. */
+glop_status glop_group_pfac_scan(glop_group* group, const glop_group_trie* trie, const uint8_t* text, uint64_t n,
+                                 glop_hit** hits, uint64_t* n_hits);
+/* run_engine_scan's PFAC branch over all members: alerts, counts (optional,
+ * n_patterns u64), stage-1 hits, and (lines and line_count both given, or
+ * both NULL) LineIndex(text) line numbers / line count. */
+glop_status glop_group_run_pfac_pipeline(glop_group* group, const glop_group_trie* trie, const glop_group_rules* rules,
+                                         const uint8_t* text, uint64_t n, glop_alert** alerts, uint64_t* n_alerts,
+                                         uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines,
+                                         uint64_t* line_count);
+/* kmp_search (kmp.hpp:41-69) over all members; comparisons exact (each shard
+ * reads m-1 bytes of left context to recover the KMP state). */
+glop_status glop_group_kmp_search(glop_group* group, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                  const uint8_t* text, uint64_t n, uint64_t** offsets, uint64_t* n_offsets,
+                                  uint64_t* comparisons);
+/* The shard plan (host only, no device): parts contiguous ranges, the first
+ * n % parts one byte longer; read = min(own + halo, n - lo). */
+glop_status glop_plan_shards(uint64_t n, uint32_t parts, uint64_t halo, uint64_t* lo, uint64_t* own,
+                             uint64_t* read);
 
 /* ---- memory helpers -------------------------------------------------------- */
 void glop_free(void* p);

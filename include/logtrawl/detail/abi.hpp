@@ -1,7 +1,8 @@
 #pragma once
-// Glue between the drop-in C++ API and the C ABI (include/glop.h): one
-// process-wide context per device and the mapping of glop_status codes onto
-// the exception types the reference throws.
+// Glue between the drop-in C++ API and the C ABI (include/glop.h): the
+// process-wide device group, content-keyed device copies of rule sets, and
+// the mapping of glop_status codes onto the exception types the reference
+// throws.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -19,20 +20,37 @@
 
 namespace logtrawl::detail {
 
-// GLOP_DEVICE selects the CUDA device (default 0).
-inline glop_ctx* context() {
+// The process-wide device group the drop-in API runs on -- every visible
+// GPU by default, as the reference's scans use every hardware thread
+// (scan.hpp:182-195, default_workers).  GLOP_DEVICES="0,2,3" picks devices (a
+// device may repeat: N contexts on one GPU); GLOP_DEVICE=d a single one.
+inline glop_group* group() {
   static std::once_flag once;
-  static glop_ctx* ctx = nullptr;
+  static glop_group* g = nullptr;
   static glop_status st = GLOP_OK;
   static std::string err;
   std::call_once(once, [] {
-    const char* env = std::getenv("GLOP_DEVICE");
-    st = glop_ctx_create(env ? std::atoi(env) : 0, &ctx);
+    std::vector<int> devs;
+    if (const char* list = std::getenv("GLOP_DEVICES")) {
+      for (const char* c = list; *c;) {
+        char* end = nullptr;
+        const long d = std::strtol(c, &end, 10);
+        if (end == c) break;
+        devs.push_back(static_cast<int>(d));
+        c = *end == ',' ? end + 1 : end;
+      }
+    } else if (const char* one = std::getenv("GLOP_DEVICE")) {
+      devs.push_back(std::atoi(one));
+    }
+    st = glop_group_create(devs.empty() ? nullptr : devs.data(), static_cast<int>(devs.size()), &g);
     if (st != GLOP_OK) err = glop_last_error();
   });
   if (st != GLOP_OK) throw std::runtime_error("glop: no usable B200 device: " + err);
-  return ctx;
+  return g;
 }
+
+// The group's first context: single-device calls (verify_hits, chunked AC).
+inline glop_ctx* context() { return glop_group_ctx(group(), 0); }
 
 // Rethrows a failed ABI call as the reference's exception type.
 inline void check(glop_status s, const char* what) {
@@ -71,11 +89,11 @@ inline void parallel_for(std::size_t n, Fn&& fn, std::size_t grain = 1 << 16) {
 // so repeated scans with one RuleSet upload nothing.  A small LRU, process-wide.
 struct RulesEntry {
   std::string key;
-  glop_rules* rules = nullptr;
-  glop_trie* trie = nullptr;  // failureless trie over truncate_prefixes(rules, prefix_len), when built
+  glop_group_rules* rules = nullptr;
+  glop_group_trie* trie = nullptr;  // failureless trie over truncate_prefixes(rules, prefix_len), when built
   ~RulesEntry() {
-    if (trie) glop_trie_destroy(trie);
-    if (rules) glop_rules_destroy(rules);
+    if (trie) glop_group_trie_destroy(trie);
+    if (rules) glop_group_rules_destroy(rules);
   }
 };
 
@@ -108,8 +126,8 @@ inline std::shared_ptr<RulesEntry> device_rules(const RuleSet& rules, std::size_
   }
   auto e = std::make_shared<RulesEntry>();
   e->key = std::move(key);
-  check(glop_rules_upload(context(), reinterpret_cast<const std::uint8_t*>(blob.data()), off.data(),
-                          static_cast<std::uint32_t>(rules.patterns.size()), prefix_len, &e->rules),
+  check(glop_group_rules_upload(group(), reinterpret_cast<const std::uint8_t*>(blob.data()), off.data(),
+                                static_cast<std::uint32_t>(rules.patterns.size()), prefix_len, &e->rules),
         "verify_hits");
   lru.push_back(e);
   if (lru.size() > 16) lru.erase(lru.begin());
@@ -120,6 +138,6 @@ inline std::shared_ptr<RulesEntry> device_rules(const RuleSet& rules, std::size_
 
 namespace logtrawl {
 inline detail::DeviceTrieCache::~DeviceTrieCache() {
-  if (trie) glop_trie_destroy(trie);
+  if (trie) glop_group_trie_destroy(trie);
 }
 }  // namespace logtrawl

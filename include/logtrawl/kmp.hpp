@@ -46,10 +46,10 @@ inline std::vector<std::size_t> kmp_search(std::string_view text, const Pattern&
   if (ft.table.size() != m) throw std::invalid_argument("kmp_search: failure table does not match pattern");
   std::uint64_t* offs = nullptr;
   std::uint64_t no = 0;
-  detail::check(glop_kmp_search(detail::context(), reinterpret_cast<const std::uint8_t*>(p.bytes.data()),
-                                static_cast<std::uint32_t>(m), ft.table.data(),
-                                reinterpret_cast<const std::uint8_t*>(text.data()), text.size(), 0, &offs, &no,
-                                comparisons),
+  detail::check(glop_group_kmp_search(detail::group(), reinterpret_cast<const std::uint8_t*>(p.bytes.data()),
+                                      static_cast<std::uint32_t>(m), ft.table.data(),
+                                      reinterpret_cast<const std::uint8_t*>(text.data()), text.size(), &offs, &no,
+                                      comparisons),
                 "kmp_search");
   out.assign(offs, offs + no);
   glop_free(offs);

@@ -2,9 +2,10 @@
 // Drop-in for logtrawl/scan.hpp (reference: /root/reference/proj/include/
 // logtrawl/scan.hpp).  pfac_scan keeps its signature and result (every start
 // position walks the failureless trie; a Hit per output of every visited
-// state; sorted by (offset, pattern_id)) but runs on the B200 through the C
+// state; sorted by (offset, pattern_id)) but runs on the B200s of the process
+// group (detail::group(): every visible GPU, or GLOP_DEVICES) through the C
 // ABI.  ScanConfig::workers is accepted and ignored: results never depend on
-// it, and the device decides its own parallelism.
+// it, and the devices decide their own parallelism.
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
@@ -64,7 +65,7 @@ inline std::shared_ptr<DeviceTrieCache> cache_slot(const Automaton& a, bool fres
 
 // Uploads (dense goto table, CSR outputs) once per automaton value.
 template <typename Build>
-inline glop_trie* cached_trie(const Automaton& a, const char* what, Build&& build) {
+inline glop_group_trie* cached_trie(const Automaton& a, const char* what, Build&& build) {
   std::shared_ptr<DeviceTrieCache> cache = cache_slot(a);
   const void* key[4] = {a.dense_table.data(), a.cnodes.data(), a.packed.data(), a.out_flat.data()};
   const std::size_t sizes[3] = {a.state_count, a.dense_table.size() + a.packed.size(), a.out_flat.size()};
@@ -95,13 +96,13 @@ inline std::vector<std::int32_t> dense_goto(const Automaton& a) {
   return dense;
 }
 
-// Device copy of a failureless trie (pfac_scan).
-inline glop_trie* device_trie(const Automaton& a) {
+// Device copies (one per group device) of a failureless trie (pfac_scan).
+inline glop_group_trie* device_trie(const Automaton& a) {
   return cached_trie(a, "pfac_scan", [&](const char* what) {
     const std::vector<std::int32_t> dense = dense_goto(a);
-    glop_trie* t = nullptr;
-    check(glop_trie_upload(context(), dense.data(), static_cast<std::uint32_t>(a.state_count), a.out_offsets.data(),
-                           reinterpret_cast<const glop_output*>(a.out_flat.data()), &t),
+    glop_group_trie* t = nullptr;
+    check(glop_group_trie_upload(group(), dense.data(), static_cast<std::uint32_t>(a.state_count),
+                                 a.out_offsets.data(), reinterpret_cast<const glop_output*>(a.out_flat.data()), &t),
           what);
     return t;
   });
@@ -111,7 +112,7 @@ inline glop_trie* device_trie(const Automaton& a) {
 // trie (the dense table holds raw goto edges, automaton.hpp:57) with only each
 // pattern's own output (matched_len == depth; the failure-merged outputs are
 // what the device's per-start walk finds by itself).
-inline glop_trie* device_ac_trie(const Automaton& a) {
+inline glop_group_trie* device_ac_trie(const Automaton& a) {
   return cached_trie(a, "chunked_ac_scan", [&](const char* what) {
     const std::vector<std::int32_t> dense = dense_goto(a);
     std::vector<std::uint32_t> off(a.state_count + 1, 0);
@@ -122,9 +123,9 @@ inline glop_trie* device_ac_trie(const Automaton& a) {
         if (o.matched_len == a.depth[s] && o.matched_len > 0) flat.push_back(o);
     }
     off[a.state_count] = static_cast<std::uint32_t>(flat.size());
-    glop_trie* t = nullptr;
-    check(glop_trie_upload(context(), dense.data(), static_cast<std::uint32_t>(a.state_count), off.data(),
-                           reinterpret_cast<const glop_output*>(flat.data()), &t),
+    glop_group_trie* t = nullptr;
+    check(glop_group_trie_upload(group(), dense.data(), static_cast<std::uint32_t>(a.state_count), off.data(),
+                                 reinterpret_cast<const glop_output*>(flat.data()), &t),
           what);
     return t;
   });
@@ -138,11 +139,11 @@ inline std::vector<Hit> pfac_scan(std::string_view text, const Automaton& a, con
   if (a.kind != AutomatonKind::failureless) throw std::invalid_argument("pfac_scan: automaton must be failureless");
   std::vector<Hit> hits;
   if (text.empty()) return hits;
-  glop_trie* t = detail::device_trie(a);
+  glop_group_trie* t = detail::device_trie(a);
   glop_hit* h = nullptr;
   std::uint64_t nh = 0;
-  detail::check(glop_pfac_scan(detail::context(), t, reinterpret_cast<const std::uint8_t*>(text.data()),
-                               text.size(), 0, &h, &nh),
+  detail::check(glop_group_pfac_scan(detail::group(), t, reinterpret_cast<const std::uint8_t*>(text.data()),
+                                     text.size(), &h, &nh),
                 "pfac_scan");
   hits.resize(nh);
   if (nh) std::memcpy(hits.data(), h, nh * sizeof(Hit));
@@ -160,7 +161,7 @@ inline std::vector<Match> chunked_ac_scan(std::string_view text, const Automaton
   std::vector<Match> out;
   const std::size_t n = text.size();
   if (n == 0) return out;
-  glop_trie* t = detail::device_ac_trie(a);
+  glop_trie* t = glop_group_trie_member(detail::device_ac_trie(a), 0);
   glop_hit* h = nullptr;
   std::uint64_t nh = 0;
   detail::check(glop_chunked_ac_scan(detail::context(), t, reinterpret_cast<const std::uint8_t*>(text.data()), n, 0,

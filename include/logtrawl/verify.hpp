@@ -105,7 +105,8 @@ inline std::vector<Alert> verify_hits(std::string_view text, const std::vector<H
   const auto dr = detail::device_rules(rules, prefixes.prefix_len);
   glop_alert* a = nullptr;
   std::uint64_t na = 0;
-  detail::check(glop_verify_hits(detail::context(), dr->rules, reinterpret_cast<const std::uint8_t*>(text.data()),
+  detail::check(glop_verify_hits(detail::context(), glop_group_rules_member(dr->rules, 0),
+                                 reinterpret_cast<const std::uint8_t*>(text.data()),
                                  text.size(), 0, reinterpret_cast<const glop_hit*>(hits.data()), hits.size(), 0, &a,
                                  &na, nullptr),
                 "verify_hits");

@@ -459,13 +459,17 @@ void build_kmp_dfa(const uint8_t* p, uint32_t m, const uint32_t* fail_tab, std::
 glop_status kmp_seq_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab, const uint8_t* d_text,
                          uint64_t n, uint64_t* d_out, uint64_t cap, uint64_t* n_offsets, uint64_t* comparisons);
 
+// KMP over d_text = global [base, base + n): starts in [skip, own) (local) are
+// reported as base + start, and the comparisons the sequential scan makes at
+// positions [skip, own) are added -- exact when skip is 0 (the text's true
+// start) or >= m - 1 (a left context long enough to recover the state).
 glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab,
                             const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
                             uint64_t* d_out, uint64_t cap, uint64_t* n_offsets,
-                            uint64_t* comparisons) {
+                            uint64_t* comparisons, uint64_t skip = 0) {
   *n_offsets = 0;
-  if (own > n) return fail(GLOP_EINVAL, "kmp_search: own > n");
-  if (m == 0 || n < m || own == 0) return GLOP_OK;  // kmp.hpp:50
+  if (own > n || skip > own) return fail(GLOP_EINVAL, "kmp_search: own > n or skip > own");
+  if (m == 0 || n < m || own == skip) return GLOP_OK;  // kmp.hpp:50
   // chunks resynchronise from the previous m-1 bytes, which is exact for the
   // pattern's own prefix function (kmp.hpp:25-36); any other table (or a
   // pattern too long for the DFA) runs the sequential walk, whole texts only
@@ -478,7 +482,7 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
     canonical = fail_tab[i] == (i ? k : 0u);
   }
   if (!canonical) {
-    if (own != n || base != 0)
+    if (own != n || base != 0 || skip != 0)
       return fail(GLOP_EINVAL, "kmp_search: shards need the pattern's own prefix function and m < 8192");
     return kmp_seq_impl(c, pat, m, fail_tab, d_text, n, d_out, cap, n_offsets, comparisons);
   }
@@ -520,6 +524,7 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
     p.own = own;
     p.end_lim = end_lim;
     p.base = base;
+    p.skip = skip;
     p.m = m;
     p.p0 = pat[0];
     p.num_tiles = num_tiles;
@@ -1448,7 +1453,13 @@ glop_status glop_pfac_scan_device(glop_ctx* c, const glop_trie* t, const uint8_t
 
 glop_status glop_pfac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n,
                            int text_on_device, glop_hit** hits, uint64_t* n_hits) {
+  return glop_pfac_scan_shard(c, t, text, n, n, 0, text_on_device, hits, n_hits);
+}
+
+glop_status glop_pfac_scan_shard(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n, uint64_t own,
+                                 uint64_t base, int text_on_device, glop_hit** hits, uint64_t* n_hits) {
   if (!c || !t || !hits || !n_hits) return fail(GLOP_EINVAL, "glop_pfac_scan: null argument");
+  if (own > n) return fail(GLOP_EINVAL, "glop_pfac_scan: own > n");
   std::lock_guard<std::mutex> lk(c->mu);
   Dev g(c->device);
   *hits = nullptr;
@@ -1458,12 +1469,12 @@ glop_status glop_pfac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text,
   uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / sizeof(glop_hit));
   TRY(c->out.ensure(cap * sizeof(glop_hit)));
   uint64_t total = 0;
-  glop_status s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
+  glop_status s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
   if (s == GLOP_ECAPACITY && total > cap) {
     c->out.release();
     cap = total;
     TRY(c->out.ensure(cap * sizeof(glop_hit)));
-    s = pfac_scan_device_impl(c, t, d_text, n, n, 0, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
+    s = pfac_scan_device_impl(c, t, d_text, n, own, base, GLOP_PFAC_AUTO, c->out.as<glop_hit>(), cap, &total);
   }
   if (s != GLOP_OK) return s;
   glop_hit* h = static_cast<glop_hit*>(malloc(std::max<uint64_t>(total, 1) * sizeof(glop_hit)));
@@ -1587,8 +1598,16 @@ glop_status glop_kmp_search_device(glop_ctx* c, const uint8_t* p, uint32_t m, co
 glop_status glop_kmp_search(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,
                             const uint8_t* text, uint64_t n, int text_on_device, uint64_t** offsets,
                             uint64_t* n_offsets, uint64_t* comparisons) {
+  return glop_kmp_search_shard(c, p, m, failure, text, n, 0, n, 0, text_on_device, offsets, n_offsets, comparisons);
+}
+
+glop_status glop_kmp_search_shard(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                  const uint8_t* text, uint64_t n, uint64_t skip, uint64_t own, uint64_t base,
+                                  int text_on_device, uint64_t** offsets, uint64_t* n_offsets,
+                                  uint64_t* comparisons) {
   if (!c || !offsets || !n_offsets || (m && (!p || !failure)))
     return fail(GLOP_EINVAL, "glop_kmp_search: null argument");
+  if (own > n) return fail(GLOP_EINVAL, "glop_kmp_search: own > n");
   std::lock_guard<std::mutex> lk(c->mu);
   Dev g(c->device);
   *offsets = nullptr;
@@ -1598,13 +1617,14 @@ glop_status glop_kmp_search(glop_ctx* c, const uint8_t* p, uint32_t m, const uin
   uint64_t cap = std::max<uint64_t>(1 << 16, c->out.bytes / 8);
   TRY(c->out.ensure(cap * 8));
   uint64_t total = 0, cmp0 = comparisons ? *comparisons : 0;
-  glop_status s = kmp_device_impl(c, p, m, failure, d_text, n, n, 0, c->out.as<uint64_t>(), cap, &total, comparisons);
+  glop_status s =
+      kmp_device_impl(c, p, m, failure, d_text, n, own, base, c->out.as<uint64_t>(), cap, &total, comparisons, skip);
   if (s == GLOP_ECAPACITY && total > cap) {
     c->out.release();
     cap = total;
     TRY(c->out.ensure(cap * 8));
     if (comparisons) *comparisons = cmp0;
-    s = kmp_device_impl(c, p, m, failure, d_text, n, n, 0, c->out.as<uint64_t>(), cap, &total, comparisons);
+    s = kmp_device_impl(c, p, m, failure, d_text, n, own, base, c->out.as<uint64_t>(), cap, &total, comparisons, skip);
   }
   if (s != GLOP_OK) return s;
   uint64_t* o = static_cast<uint64_t*>(malloc(std::max<uint64_t>(total, 1) * 8));
@@ -1699,6 +1719,16 @@ glop_status glop_run_pfac_pipeline_lines(glop_ctx* c, const glop_trie* t, const 
                        line_count);
 }
 
+glop_status glop_run_pfac_pipeline_shard_lines(glop_ctx* c, const glop_trie* t, const glop_rules* r,
+                                               const uint8_t* text, uint64_t n, uint64_t own, uint64_t base,
+                                               int text_on_device, glop_alert** alerts, uint64_t* n_alerts,
+                                               uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines,
+                                               uint64_t* line_count) {
+  if (!lines || !line_count) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline_shard_lines: null argument");
+  return pipeline_host(c, t, r, text, n, own, base, text_on_device, alerts, n_alerts, counts, stage1_hits, lines,
+                       line_count);
+}
+
 glop_status glop_chunked_ac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n,
                                  int text_on_device, uint64_t chunk_size, uint64_t overlap, glop_hit** matches,
                                  uint64_t* n_matches) {
@@ -1767,11 +1797,11 @@ glop_status pipeline_host(glop_ctx* c, const glop_trie* t, const glop_rules* r, 
   if (s != GLOP_OK) return s;
   if (stage1_hits) *stage1_hits = nh;
   uint64_t* d_lf = nullptr;
-  if (lines || line_count) {  // LineIndex(text) on the device (own == n, base == 0 here)
+  if (lines || line_count) {  // LineIndex over the owned bytes [0, own), on the device
     TRY(c->plines.ensure(kept * 8 + 16));
     d_lf = c->plines.as<uint64_t>() + kept + 1;
     CU(cudaMemsetAsync(d_lf, 0, 8, c->stream));
-    TRY(line_numbers_impl(c, d_text, n, base, c->palerts.p, sizeof(glop_alert), kept, c->plines.as<uint64_t>(),
+    TRY(line_numbers_impl(c, d_text, own, base, c->palerts.p, sizeof(glop_alert), kept, c->plines.as<uint64_t>(),
                           nullptr, d_lf));
   }
   TRY(alerts_to_host(c, c->palerts.as<glop_alert>(), kept, d_counts, k, counts, alerts, c->plines.as<uint64_t>(),
@@ -1913,3 +1943,5 @@ glop_status glop_gen_rules(uint32_t k, uint32_t seed, uint32_t len, uint8_t* byt
 }
 
 }  // extern "C"
+
+#include "group.inl"

@@ -55,6 +55,7 @@ __host__ __device__ inline K3Layout make_k3_layout(uint32_t m, bool smem_dfa) {
 struct K3Params {
   const uint8_t* text;
   unsigned long long n, own, end_lim, base;  // starts < own; ends (last byte of a match) < end_lim
+  unsigned long long skip;                   // left context: starts and comparisons from position skip on
   uint32_t m, p0, num_tiles, per, sub;
   const uint32_t* dfa;                  // m x 256
   unsigned long long* staging;          // per-warp regions of start offsets
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
       return (y >= 0 && y < (long long)kK3Stage) ? win[y] : __ldg(A + x);
     };
     auto record = [&](unsigned long long x) {  // match ending at A coordinate x
+      if (x + 1 < a + p.skip + m) return;  // starts in the left context belong to the previous shard
       const unsigned long long start = p.base + x - a + 1 - m;
       if (p.mode == 0) {
         const uint32_t slot = atomicAdd(s_nh, 1u);
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kK3Threads, 1) kmp3_kernel(const K3Params p, c
       }
     };
     unsigned long long c0 = tT + (unsigned long long)lane * kK3Chunk;
-    if (c0 < a) c0 = a;
+    if (c0 < a + p.skip) c0 = a + p.skip;  // (left context: warm-up only)
     const unsigned long long c1 = min(tT + (unsigned long long)(lane + 1) * kK3Chunk, e_end);
     if (c0 < c1) {
       const uint32_t y0 = (uint32_t)(c0 - tT) + kK3Pre, y1 = (uint32_t)(c1 - tT) + kK3Pre;

@@ -517,3 +517,123 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- multi-GPU group
+_sig("glop_group_create", vp, C.c_int, C.POINTER(vp))
+_sig("glop_group_destroy", vp)
+_lib.glop_group_size.argtypes = [vp]
+_lib.glop_group_size.restype = C.c_int
+_sig("glop_group_trie_upload", vp, i32p, C.c_uint32, u32p, vp, C.POINTER(vp))
+_sig("glop_group_trie_destroy", vp)
+_sig("glop_group_rules_upload", vp, u8p, u64p, C.c_uint32, C.c_uint64, C.POINTER(vp))
+_sig("glop_group_rules_destroy", vp)
+_sig("glop_group_pfac_scan", vp, vp, vp, C.c_uint64, C.POINTER(vp), u64p)
+_sig("glop_group_run_pfac_pipeline", vp, vp, vp, vp, C.c_uint64, C.POINTER(vp), u64p, u64p, u64p, C.POINTER(vp), u64p)
+_sig("glop_group_kmp_search", vp, u8p, C.c_uint32, u32p, vp, C.c_uint64, C.POINTER(vp), u64p, u64p)
+_sig("glop_plan_shards", C.c_uint64, C.c_uint32, C.c_uint64, u64p, u64p, u64p)
+
+
+def plan_shards_c(n: int, parts: int, halo: int):
+    """glop_plan_shards (host only): [(lo, own, read)] per shard."""
+    lo, own, rd = (np.zeros(parts, np.uint64) for _ in range(3))
+    _check(_lib.glop_plan_shards(n, parts, halo, lo.ctypes.data_as(u64p), own.ctypes.data_as(u64p),
+                                 rd.ctypes.data_as(u64p)), "plan_shards")
+    return [(int(a), int(b), int(c)) for a, b, c in zip(lo, own, rd)]
+
+
+class Group:
+    """A glop_group: one context per member device (devices may repeat);
+    every call splits the text into halo'd shards across the members and
+    merges the results in rank order."""
+
+    def __init__(self, devices=None):
+        h = vp()
+        if devices is None:
+            _check(_lib.glop_group_create(None, 0, C.byref(h)), "glop_group_create")
+        else:
+            d = (C.c_int * len(devices))(*devices)
+            _check(_lib.glop_group_create(d, len(devices), C.byref(h)), "glop_group_create")
+        self.h = h
+
+    @property
+    def size(self) -> int:
+        return int(_lib.glop_group_size(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.glop_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, a: Automaton):
+        dense = np.ascontiguousarray(a.dense_table, dtype=np.int32)
+        offs = np.ascontiguousarray(a.out_offsets, dtype=np.uint32)
+        flat = np.ascontiguousarray(a.out_flat, dtype=np.uint32).reshape(-1)
+        if flat.size == 0:
+            flat = np.zeros(2, np.uint32)
+        h = vp()
+        _check(_lib.glop_group_trie_upload(self.h, dense.ctypes.data_as(i32p), dense.shape[0],
+                                           offs.ctypes.data_as(u32p), flat.ctypes.data_as(vp), C.byref(h)),
+               "glop_group_trie_upload")
+        return _GroupHandle(h, _lib.glop_group_trie_destroy)
+
+    def upload_rules(self, patterns, prefix_len: int):
+        pat, off = pack_patterns(list(patterns))
+        h = vp()
+        _check(_lib.glop_group_rules_upload(self.h, pat.ctypes.data_as(u8p), off.ctypes.data_as(u64p), len(patterns),
+                                            prefix_len, C.byref(h)), "glop_group_rules_upload")
+        r = _GroupHandle(h, _lib.glop_group_rules_destroy)
+        r.n_patterns = len(patterns)
+        return r
+
+    def pfac_scan(self, trie, text) -> np.ndarray:
+        t = _u8(text)
+        p, n = vp(), C.c_uint64()
+        _check(_lib.glop_group_pfac_scan(self.h, trie.h, _ptr(t), t.size, C.byref(p), C.byref(n)), "group_pfac_scan")
+        return _take(p, n.value, HIT_DTYPE)
+
+    def run_pfac_pipeline(self, trie, rules, text, lines: bool = False):
+        """(alerts, counts, stage1_hits, lines or None, line_count or None)"""
+        t = _u8(text)
+        p, na, s1, lp, lc = vp(), C.c_uint64(), C.c_uint64(), vp(), C.c_uint64()
+        cnt = np.zeros(max(rules.n_patterns, 1), dtype=np.uint64)
+        _check(_lib.glop_group_run_pfac_pipeline(self.h, trie.h, rules.h, _ptr(t), t.size, C.byref(p), C.byref(na),
+                                                 cnt.ctypes.data_as(u64p), C.byref(s1),
+                                                 C.byref(lp) if lines else None, C.byref(lc) if lines else None),
+               "group_run_pfac_pipeline")
+        alerts = _take(p, na.value, ALERT_DTYPE)
+        return (alerts, cnt[:rules.n_patterns], s1.value, _take(lp, na.value, np.uint64) if lines else None,
+                lc.value if lines else None)
+
+    def kmp_search(self, pattern: bytes, text, failure: np.ndarray | None = None):
+        t = _u8(text)
+        p = _u8(pattern)
+        f = np.ascontiguousarray(kmp_failure_table(pattern) if failure is None else failure, dtype=np.uint32)
+        o, n, cmp_ = vp(), C.c_uint64(), C.c_uint64(0)
+        pp = p if p.size else np.zeros(1, np.uint8)
+        ff = f if f.size else np.zeros(1, np.uint32)
+        _check(_lib.glop_group_kmp_search(self.h, pp.ctypes.data_as(u8p), p.size, ff.ctypes.data_as(u32p), _ptr(t),
+                                          t.size, C.byref(o), C.byref(n), C.byref(cmp_)), "group_kmp_search")
+        return _take(o, n.value, np.uint64), cmp_.value
+
+
+class _GroupHandle:
+    def __init__(self, h, destroy):
+        self.h, self._destroy = h, destroy
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -108,3 +108,13 @@ def test_gloo_world2_reduce_and_gather():
     for _, counts, rows in res:
         assert np.frombuffer(counts, np.int64).tolist() == want_counts.tolist()
         assert rows == whole.tobytes()  # rank-order concatenation is globally sorted
+
+
+def test_plan_shards_c_abi_matches_python():
+    """glop_plan_shards (the C ABI's shard plan, host only) == shards.plan_shards."""
+    from paper_1704_02278_b200 import glop
+
+    for n, world, halo in [(10, 3, 7), (8_000_000_000, 8, 7), (0, 2, 7), (5, 8, 23), (1 << 40, 7, 14)]:
+        c = glop.plan_shards_c(n, world, halo)
+        py = [(s.lo, s.own, s.read) for s in plan_shards(n, world, halo)]
+        assert c == py, (n, world, halo)
