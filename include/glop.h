@@ -137,6 +137,25 @@ glop_status glop_pfac_scan_device(glop_ctx* ctx, const glop_trie* trie, const ui
                                   uint64_t n, uint64_t own, uint64_t base, glop_pfac_kernel kernel,
                                   glop_hit* d_out, uint64_t cap, uint64_t* n_hits);
 
+/* ---- streaming ingest ----------------------------------
+ * run_engine_scan's PFAC branch over a text that arrives in pieces (a file
+ * read in windows, a log tail): the result equals glop_run_pfac_pipeline[_lines]
+ * over the concatenation of every fed piece.  Windows of 256 MiB are scanned
+ * as they fill; each reads max(trie depth, longest pattern) - 1 bytes of the
+ * next, carried across feed() calls (SPEC.md:290's max_len-1 windowing), so a
+ * match straddling two pieces is reported once, by the window owning its
+ * start.  glop_stream_end returns the results (library-owned arrays, as
+ * glop_run_pfac_pipeline_lines; lines/line_count may be NULL when the stream
+ * was begun without lines; bytes = total fed) and frees the stream, also on
+ * error.  One stream at a time per context is not required: feeds lock the
+ * context only while a window is scanned. */
+typedef struct glop_stream glop_stream;
+glop_status glop_stream_begin(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules, int with_lines,
+                              glop_stream** out);
+glop_status glop_stream_feed(glop_stream* stream, const uint8_t* data, uint64_t len);
+glop_status glop_stream_end(glop_stream* stream, glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                            uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count, uint64_t* bytes);
+
 /* ---- chunked full Aho-Corasick --------------------------------------------
  * Replaces chunked_ac_scan (scan.hpp:207-243): chunk k owns starts
  * [k*c, (k+1)*c) (c = chunk_size, 0 = the whole text) and is scanned from the

@@ -1,7 +1,9 @@
 // logtrawl -- the reference's command-line tool (tools/logtrawl.cpp:153-208)
 // over the B200 path: `scan` (JSONL / summary alerts, exit 0 = no match,
 // 1 = match, 2 = error), `bench` (throughput CSV, bench.hpp:140-157) and
-// `gen` (reference corpus + SHA-256, loggen.hpp:44-57).  Same options and
+// `gen` (reference corpus + SHA-256, loggen.hpp:44-57).  `scan` with a pfac
+// engine reads each log in 64 MiB windows through the device stream
+// (StreamScan) instead of loading the whole file.  Same options and
 // output contract (tests/cli_test.sh of the reference, restated in
 // tests/test_cli.py); CLI11 is not available here, so the option parsing is
 // a small hand-written subset of what the reference's CLI11 setup accepts.
@@ -23,27 +25,50 @@
 
 namespace {
 
-std::string read_file(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw std::runtime_error("cannot open " + path);
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return std::move(ss).str();
+// Whole file into memory (rule files; the kmp and ac_chunked engines).
+std::string slurp(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw std::runtime_error("cannot open " + path);
+  std::string data;
+  char buf[1 << 16];
+  for (size_t got; (got = std::fread(buf, 1, sizeof buf, f)) > 0;) data.append(buf, got);
+  const bool bad = std::ferror(f);
+  std::fclose(f);
+  if (bad) throw std::runtime_error("read error on " + path);
+  return data;
 }
 
-void write_file(const std::string& path, const std::string& data) {
-  std::ofstream out(path, std::ios::binary);
-  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
-  out.write(data.data(), static_cast<std::streamsize>(data.size()));
-  if (!out) throw std::runtime_error("short write to " + path);
+void spill(const std::string& path, const std::string& data) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open " + path + " for writing");
+  const size_t put = std::fwrite(data.data(), 1, data.size(), f);
+  const bool bad = std::fclose(f) != 0 || put != data.size();
+  if (bad) throw std::runtime_error("short write to " + path);
 }
 
-unsigned workers_default() {  // logtrawl.cpp:36-42
-  if (const char* env = std::getenv("LOGTRAWL_WORKERS")) {
-    const int v = std::atoi(env);
-    if (v > 0) return static_cast<unsigned>(v);
-  }
-  return 0;
+// LOGTRAWL_WORKERS (a positive count) or 0 = the library's own parallelism
+// (the reference's default_workers contract, logtrawl.cpp:36-42).
+unsigned env_workers() {
+  const char* env = std::getenv("LOGTRAWL_WORKERS");
+  const long v = env ? std::strtol(env, nullptr, 10) : 0;
+  return v > 0 ? static_cast<unsigned>(v) : 0u;
+}
+
+// A log file scanned window by window through the device stream (pfac
+// engines): the file is never held whole in memory.
+logtrawl::ScanReport scan_file_streamed(const std::string& path, const logtrawl::RuleSet& rules,
+                                        const logtrawl::EngineConfig& cfg) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw std::runtime_error("cannot open " + path);
+  logtrawl::StreamScan stream(rules, cfg, true);
+  const char* env = std::getenv("LOGTRAWL_READ_WINDOW");  // tests: small reads
+  std::vector<char> window(env && std::atol(env) > 0 ? std::atol(env) : (64l << 20));
+  for (size_t got; (got = std::fread(window.data(), 1, window.size(), f)) > 0;)
+    stream.feed(std::string_view(window.data(), got));
+  const bool bad = std::ferror(f);
+  std::fclose(f);
+  if (bad) throw std::runtime_error("read error on " + path);
+  return stream.finish();
 }
 
 // --- SHA-256 (FIPS 180-4), for the `gen` digest line -----------------------
@@ -148,7 +173,7 @@ int do_scan(const Opts& o) {  // logtrawl.cpp:54-84
   using namespace logtrawl;
   const std::string* rules_path = get(o, {"-r", "--rules"});
   if (!rules_path || o.positional.empty()) throw std::invalid_argument("scan: -r RULES and input files required");
-  RuleSet rules = parse_rules(read_file(*rules_path));
+  RuleSet rules = parse_rules(slurp(*rules_path));
   if (rules.patterns.empty()) throw std::runtime_error(*rules_path + ": rule file has no rules");
   const std::string engine_s = get(o, {"--engine"}) ? *get(o, {"--engine"}) : "pfac_compact";
   const auto engine = engine_from_name(engine_s);
@@ -156,15 +181,21 @@ int do_scan(const Opts& o) {  // logtrawl.cpp:54-84
   EngineConfig cfg;
   cfg.engine = *engine;
   if (auto* v = get(o, {"--prefix-len"})) cfg.prefix_len = to_u64(*v);
-  cfg.workers = get(o, {"--workers"}) ? (unsigned)to_u64(*get(o, {"--workers"})) : workers_default();
+  cfg.workers = get(o, {"--workers"}) ? (unsigned)to_u64(*get(o, {"--workers"})) : env_workers();
   if (auto* v = get(o, {"--chunk-size"})) cfg.chunk_size = to_u64(*v);
   const std::string format = get(o, {"--format"}) ? *get(o, {"--format"}) : "jsonl";
   if (format != "jsonl" && format != "summary") throw std::invalid_argument("--format: jsonl|summary");
   std::size_t total = 0;
+  const bool pfac = cfg.engine == EngineKind::pfac_dense || cfg.engine == EngineKind::pfac_compact;
   for (const std::string& path : o.positional) {
-    const std::string text = read_file(path);
-    LineIndex lines(text);
-    const ScanReport report = run_engine_scan(text, rules, cfg, &lines);
+    ScanReport report;
+    if (pfac) {
+      report = scan_file_streamed(path, rules, cfg);
+    } else {
+      const std::string text = slurp(path);
+      LineIndex lines(text);
+      report = run_engine_scan(text, rules, cfg, &lines);
+    }
     total += report.total_matches;
     if (format == "jsonl") {
       std::cout << render_alerts_jsonl(path, report);
@@ -181,7 +212,7 @@ int do_bench(const Opts& o) {  // logtrawl.cpp:99-129, bench.hpp:64-157
   using namespace logtrawl;
   const std::string* in = get(o, {"-i", "--input"});
   if (!in) throw std::invalid_argument("bench: -i INPUT required");
-  const std::string text = read_file(*in);
+  const std::string text = slurp(*in);
   const std::string engine_s = get(o, {"--engine"}) ? *get(o, {"--engine"}) : "pfac_compact";
   const auto engine = engine_from_name(engine_s);
   if (!engine) throw std::runtime_error("unknown engine " + engine_s);
@@ -242,7 +273,7 @@ int do_bench(const Opts& o) {  // logtrawl.cpp:99-129, bench.hpp:64-157
       csv += buf;
     }
   }
-  if (auto* out = get(o, {"-o", "--out"})) write_file(*out, csv);
+  if (auto* out = get(o, {"-o", "--out"})) spill(*out, csv);
   else std::cout << csv;
   return 0;
 }
@@ -257,7 +288,7 @@ int do_gen(const Opts& o) {  // logtrawl.cpp:138-149
   if (n == 0) throw std::invalid_argument("generate_log: size is 0");
   if (line_len < 2) throw std::invalid_argument("generate_log: line_len must be >= 2");
   const std::string bytes = glop_workload::reference_generate_log(n, (uint32_t)to_u64(*seed), line_len);
-  write_file(*out, bytes);
+  spill(*out, bytes);
   std::cout << "sha256  " << Sha256().hex(bytes) << " " << *out << " " << bytes.size() << "\n";
   return 0;
 }

@@ -83,6 +83,24 @@ struct DBuf {
   }
 };
 
+// Results of a text processed window by window (the streamed host pipeline,
+// glop_stream_*): alerts and line numbers appended in text order, per-pattern
+// counts and the LF count of the windows so far on the device.
+struct Accum {
+  DBuf alerts, lines, cnt;  // cnt: counts[k+1] | window counts[k+1] | lf
+  uint64_t total = 0, hits = 0;
+  uint32_t k = 0;
+  bool want_lines = false;
+  uint64_t* d_counts() { return cnt.as<uint64_t>(); }
+  uint64_t* d_window_counts() { return cnt.as<uint64_t>() + k + 1; }
+  uint64_t* d_lf() { return cnt.as<uint64_t>() + 2 * (k + 1); }
+  void release() {
+    alerts.release();
+    lines.release();
+    cnt.release();
+  }
+};
+
 }  // namespace
 
 struct glop_ctx {
@@ -96,6 +114,7 @@ struct glop_ctx {
   DBuf lcount, lprefix, loffs;                   // device LineIndex
   DBuf hprefix, kcounts, kprefix, keep8, counts_tmp;  // fused pipeline (pipeline.cuh)
   DBuf palerts, plines;                          // alerts (+ lines) of the host-facing pipeline calls
+  Accum acc;                                     // streamed pipeline results
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
   void* pin[2] = {nullptr, nullptr};             // pinned staging of pageable host text
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
@@ -843,6 +862,56 @@ glop_status alerts_to_host(glop_ctx* c, const glop_alert* d_alerts, uint64_t n_a
   return GLOP_OK;
 }
 
+glop_status accum_begin(glop_ctx* c, Accum& A, uint32_t k, bool want_lines) {
+  A.total = A.hits = 0;
+  A.k = k;
+  A.want_lines = want_lines;
+  TRY(A.cnt.ensure((size_t)(2 * k + 3) * 8));
+  CU(cudaMemsetAsync(A.cnt.p, 0, (size_t)(2 * k + 3) * 8, c->stream));
+  TRY(A.alerts.ensure(std::max<size_t>(A.alerts.bytes, (1 << 16) * sizeof(glop_alert))));
+  return GLOP_OK;
+}
+
+// One window: d_text = global [base, base + rd), starts [base, base + own).
+glop_status accum_window(glop_ctx* c, const glop_trie* t, const glop_rules* r, Accum& A, const uint8_t* d_text,
+                         uint64_t rd, uint64_t own, uint64_t base) {
+  uint64_t nh = 0, kept = 0;
+  for (;;) {
+    const uint64_t room = A.alerts.bytes / sizeof(glop_alert) - A.total;
+    glop_status s = pipeline_device_impl(c, t, r, d_text, rd, own, base, nullptr, 0,
+                                         A.alerts.as<glop_alert>() + A.total, room, A.d_window_counts(), &nh, &kept);
+    if (s == GLOP_ECAPACITY && kept > room) {  // grow, keeping the alerts so far; redo the window
+      TRY(grow_keep(c, A.alerts, std::max<uint64_t>(2 * A.alerts.bytes, (A.total + kept + (1 << 16)) * sizeof(glop_alert)),
+                    A.total * sizeof(glop_alert)));
+      continue;
+    }
+    if (s != GLOP_OK) return s;
+    break;
+  }
+  if (A.want_lines) {  // LineIndex over the owned bytes of this window, offset by the earlier windows' LFs
+    TRY(grow_keep(c, A.lines, (A.total + kept) * 8 + 8, A.total * 8));
+    TRY(line_numbers_impl(c, d_text, own, base, A.alerts.as<glop_alert>() + A.total, sizeof(glop_alert), kept,
+                          A.lines.as<uint64_t>() + A.total, A.d_lf(), A.d_lf()));
+  }
+  ++c->launches;
+  add_u64_kernel<<<(A.k + 255) / 256 + 1, 256, 0, c->stream>>>(
+      reinterpret_cast<unsigned long long*>(A.d_counts()),
+      reinterpret_cast<const unsigned long long*>(A.d_window_counts()), A.k);
+  CU(cudaGetLastError());
+  A.hits += nh;
+  A.total += kept;
+  return GLOP_OK;
+}
+
+glop_status accum_end(glop_ctx* c, Accum& A, glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                      uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count) {
+  if (stage1_hits) *stage1_hits = A.hits;
+  TRY(alerts_to_host(c, A.alerts.as<glop_alert>(), A.total, A.d_counts(), A.k, counts, alerts,
+                     A.lines.as<uint64_t>(), lines, A.d_lf(), line_count));
+  *n_alerts = A.total;
+  return GLOP_OK;
+}
+
 glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* h_text,
                                   uint64_t n, uint64_t own, uint64_t base, glop_alert** alerts,
                                   uint64_t* n_alerts, uint64_t* counts, uint64_t* stage1_hits,
@@ -850,16 +919,8 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   const uint64_t halo = std::max<uint64_t>(std::max<uint64_t>(t->info.max_depth, r->max_len), 1) - 1;
   const uint64_t chunks = (own + kStreamChunk - 1) / kStreamChunk;
   for (int b = 0; b < 2; ++b) TRY(c->sbuf[b].ensure(kStreamChunk + halo + 64));
-  const uint32_t k = r->view.n_patterns;
-  TRY(c->spill.ensure((size_t)(2 * k + 3) * 8));
-  uint64_t* d_counts = c->spill.as<uint64_t>();          // accumulated over chunks
-  uint64_t* d_chunk_counts = d_counts + k + 1;           // one chunk's counts
-  uint64_t* d_lf = d_chunk_counts + k + 1;               // LF bytes of the chunks so far
-  CU(cudaMemsetAsync(d_counts, 0, (size_t)(2 * k + 3) * 8, c->stream));
-  const bool want_lines = lines || line_count;
-  DBuf& acc = c->palerts;  // accumulated alerts (device); grows rarely, kept across calls
-  TRY(acc.ensure(std::max<size_t>(acc.bytes, (1 << 16) * sizeof(glop_alert))));
-  uint64_t total = 0, hits = 0;
+  Accum& A = c->acc;  // kept across calls (buffers grow rarely)
+  TRY(accum_begin(c, A, r->view.n_patterns, lines || line_count));
   // Pageable text (a std::string, a file read into memory): the driver would
   // stage it through its own pinned buffers on one thread; instead host
   // threads copy each chunk into one of two pinned staging buffers while the
@@ -892,43 +953,11 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
     if (i + 1 < chunks) TRY(copy(i + 1));
     const uint64_t lo = i * kStreamChunk, own_i = std::min<uint64_t>(kStreamChunk, own - lo);
     const uint64_t rd = std::min<uint64_t>(own_i + halo, n - lo);
-    const uint8_t* d_text = c->sbuf[i & 1].as<uint8_t>();
     CU(cudaStreamWaitEvent(c->stream, c->ev_copied[i & 1], 0));
-    uint64_t nh = 0, kept = 0;
-    for (;;) {
-      const uint64_t room = acc.bytes / sizeof(glop_alert) - total;
-      glop_status s = pipeline_device_impl(c, t, r, d_text, rd, own_i, base + lo, nullptr, 0,
-                                           acc.as<glop_alert>() + total, room, d_chunk_counts, &nh, &kept);
-      if (s == GLOP_ECAPACITY && kept > room) {  // grow, keeping the alerts so far; redo the chunk
-        DBuf bigger;
-        TRY(bigger.ensure(std::max<uint64_t>(2 * acc.bytes, (total + kept + (1 << 16)) * sizeof(glop_alert))));
-        if (total) CU(cudaMemcpyAsync(bigger.p, acc.p, total * sizeof(glop_alert), cudaMemcpyDeviceToDevice, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
-        acc.release();
-        acc = bigger;
-        bigger.p = nullptr;
-        continue;
-      }
-      if (s != GLOP_OK) return s;
-      break;
-    }
-    if (want_lines) {  // LineIndex over the owned bytes of this chunk, offset by the earlier chunks' LFs
-      TRY(grow_keep(c, c->plines, (total + kept) * 8 + 8, total * 8));
-      TRY(line_numbers_impl(c, d_text, own_i, base + lo, acc.as<glop_alert>() + total, sizeof(glop_alert), kept,
-                            c->plines.as<uint64_t>() + total, d_lf, d_lf));
-    }
-    ++c->launches;
-    add_u64_kernel<<<(k + 255) / 256 + 1, 256, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(d_counts), reinterpret_cast<const unsigned long long*>(d_chunk_counts), k);
-    CU(cudaGetLastError());
+    TRY(accum_window(c, t, r, A, c->sbuf[i & 1].as<uint8_t>(), rd, own_i, base + lo));
     CU(cudaEventRecord(c->ev_free[i & 1], c->stream));
-    hits += nh;
-    total += kept;
   }
-  if (stage1_hits) *stage1_hits = hits;
-  TRY(alerts_to_host(c, acc.as<glop_alert>(), total, d_counts, k, counts, alerts, c->plines.as<uint64_t>(), lines,
-                     d_lf, line_count));
-  *n_alerts = total;
-  return GLOP_OK;
+  return accum_end(c, A, alerts, n_alerts, counts, stage1_hits, lines, line_count);
 }
 
 // Device LineIndex (lines.cuh): lines[i] = line of record i's offset (u64
@@ -1130,6 +1159,7 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
                   &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1], &c->lcount, &c->lprefix, &c->loffs,
                   &c->hprefix, &c->kcounts, &c->kprefix, &c->keep8, &c->counts_tmp, &c->palerts, &c->plines})
     b->release();
+  c->acc.release();
   if (c->cstream) {
     cudaStreamSynchronize(c->cstream);
     cudaStreamDestroy(c->cstream);
@@ -1727,6 +1757,101 @@ glop_status glop_run_pfac_pipeline_shard_lines(glop_ctx* c, const glop_trie* t, 
   if (!lines || !line_count) return fail(GLOP_EINVAL, "glop_run_pfac_pipeline_shard_lines: null argument");
   return pipeline_host(c, t, r, text, n, own, base, text_on_device, alerts, n_alerts, counts, stage1_hits, lines,
                        line_count);
+}
+
+// ---- streaming: the text arrives in caller buffers of any size; windows of
+// W bytes are scanned as they fill, each reading max(depth, max_len) - 1 bytes
+// of the next one (carried over), so a match straddling two feed() calls or
+// two windows is found exactly once (SPEC.md:290 windowing).
+struct glop_stream {
+  glop_ctx* c = nullptr;
+  const glop_trie* t = nullptr;
+  const glop_rules* r = nullptr;
+  uint64_t halo = 0, W = 0, fill = 0, pos = 0;
+  void* pin = nullptr;  // window staging (pinned): bytes [pos, pos + fill) of the text
+  DBuf dtext;
+  Accum A;
+  glop_status err = GLOP_OK;
+};
+
+namespace {
+glop_status stream_window(glop_stream* st, uint64_t own) {
+  glop_ctx* c = st->c;
+  CU(cudaMemcpyAsync(st->dtext.p, st->pin, st->fill, cudaMemcpyHostToDevice, c->stream));
+  return accum_window(c, st->t, st->r, st->A, st->dtext.as<uint8_t>(), st->fill, own, st->pos);
+}
+}  // namespace
+
+glop_status glop_stream_begin(glop_ctx* c, const glop_trie* t, const glop_rules* r, int with_lines,
+                              glop_stream** out) {
+  if (!c || !t || !r || !out) return fail(GLOP_EINVAL, "glop_stream_begin: null argument");
+  *out = nullptr;
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  auto* st = new glop_stream();
+  st->c = c;
+  st->t = t;
+  st->r = r;
+  st->halo = std::max<uint64_t>(std::max<uint64_t>(t->info.max_depth, r->max_len), 1) - 1;
+  const char* env = getenv("GLOP_STREAM_WINDOW");  // tests: small windows
+  st->W = std::max<uint64_t>(env ? strtoull(env, nullptr, 10) : kStreamChunk, st->halo + 1);
+  glop_status s = GLOP_OK;
+  if (cudaMallocHost(&st->pin, st->W + st->halo + 64) != cudaSuccess) s = fail(GLOP_ENOMEM, "glop_stream_begin: pinned buffer");
+  if (s == GLOP_OK) s = st->dtext.ensure(st->W + st->halo + 64);
+  if (s == GLOP_OK) s = accum_begin(c, st->A, r->view.n_patterns, with_lines != 0);
+  if (s != GLOP_OK) {
+    if (st->pin) cudaFreeHost(st->pin);
+    st->dtext.release();
+    st->A.release();
+    delete st;
+    return s;
+  }
+  *out = st;
+  return GLOP_OK;
+}
+
+glop_status glop_stream_feed(glop_stream* st, const uint8_t* data, uint64_t len) {
+  if (!st || (len && !data)) return fail(GLOP_EINVAL, "glop_stream_feed: null argument");
+  if (st->err != GLOP_OK) return fail(st->err, "glop_stream_feed: the stream failed earlier");
+  std::lock_guard<std::mutex> lk(st->c->mu);
+  Dev g(st->c->device);
+  const uint64_t full = st->W + st->halo;
+  while (len) {
+    const uint64_t take = std::min<uint64_t>(len, full - st->fill);
+    parallel_memcpy(static_cast<uint8_t*>(st->pin) + st->fill, data, take);
+    st->fill += take;
+    data += take;
+    len -= take;
+    if (st->fill == full) {  // window [pos, pos + W) with its halo: scan, then carry the halo
+      const glop_status s = stream_window(st, st->W);
+      if (s != GLOP_OK) return st->err = s;
+      memmove(st->pin, static_cast<uint8_t*>(st->pin) + st->W, st->halo);  // (the copy above has completed)
+      st->fill = st->halo;
+      st->pos += st->W;
+    }
+  }
+  return GLOP_OK;
+}
+
+glop_status glop_stream_end(glop_stream* st, glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                            uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count, uint64_t* bytes) {
+  if (!st) return fail(GLOP_EINVAL, "glop_stream_end: null stream");
+  glop_status s = st->err;
+  {
+    std::lock_guard<std::mutex> lk(st->c->mu);
+    Dev g(st->c->device);
+    if (s == GLOP_OK && (!alerts || !n_alerts)) s = fail(GLOP_EINVAL, "glop_stream_end: null argument");
+    if (s == GLOP_OK && st->fill) s = stream_window(st, st->fill);  // the tail owns every remaining start
+    if (s == GLOP_OK)
+      s = accum_end(st->c, st->A, alerts, n_alerts, counts, stage1_hits, lines, line_count);
+    if (s == GLOP_OK && bytes) *bytes = st->pos + st->fill;
+    cudaStreamSynchronize(st->c->stream);
+    st->dtext.release();
+    st->A.release();
+  }
+  if (st->pin) cudaFreeHost(st->pin);
+  delete st;
+  return s;
 }
 
 glop_status glop_chunked_ac_scan(glop_ctx* c, const glop_trie* t, const uint8_t* text, uint64_t n,

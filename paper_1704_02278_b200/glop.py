@@ -637,3 +637,36 @@ class _GroupHandle:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- streaming ingest
+_sig("glop_stream_begin", vp, vp, vp, C.c_int, C.POINTER(vp))
+_sig("glop_stream_feed", vp, vp, C.c_uint64)
+_sig("glop_stream_end", vp, C.POINTER(vp), u64p, u64p, u64p, C.POINTER(vp), u64p, u64p)
+
+
+class Stream:
+    """glop_stream_*: the PFAC pipeline over a text fed in pieces of any size
+    (the result equals run_pfac_pipeline over the concatenation)."""
+
+    def __init__(self, ctx: "Context", trie: "DeviceTrie", rules: "DeviceRules", lines: bool = False):
+        h = vp()
+        _check(_lib.glop_stream_begin(ctx.h, trie.h, rules.h, 1 if lines else 0, C.byref(h)), "stream_begin")
+        self.h, self.lines, self.n_patterns = h, lines, rules.n_patterns
+        self._keep = (ctx, trie, rules)
+
+    def feed(self, data):
+        t = _u8(data)
+        _check(_lib.glop_stream_feed(self.h, _ptr(t), t.size), "stream_feed")
+
+    def end(self):
+        """(alerts, counts, stage1_hits, lines or None, line_count or None, bytes)"""
+        p, na, s1, lp, lc, nb = vp(), C.c_uint64(), C.c_uint64(), vp(), C.c_uint64(), C.c_uint64()
+        cnt = np.zeros(max(self.n_patterns, 1), dtype=np.uint64)
+        h, self.h = self.h, None
+        _check(_lib.glop_stream_end(h, C.byref(p), C.byref(na), cnt.ctypes.data_as(u64p), C.byref(s1),
+                                    C.byref(lp) if self.lines else None, C.byref(lc) if self.lines else None,
+                                    C.byref(nb)), "stream_end")
+        alerts = _take(p, na.value, ALERT_DTYPE)
+        return (alerts, cnt[:self.n_patterns], s1.value, _take(lp, na.value, np.uint64) if self.lines else None,
+                lc.value if self.lines else None, nb.value)

@@ -76,6 +76,12 @@ def test_scan_jsonl_equals_reference(cli, tmp_path):
     assert rc == 0 and b'"total_matches":0' in out
     rc, out = run([cli, "scan", "-r", "hit.rules", "--format", "summary", "hit.log"], tmp_path)
     assert rc == 1 and b"total_matches=1" in out
+    # the pfac engines read the log in windows through the device stream:
+    # small reads (feed boundaries) and small device windows give the same bytes
+    for eng in ("pfac_compact", "pfac_dense"):
+        rc, out = run([cli, "scan", "-r", "big.rules", "--engine", eng, "big.log"], tmp_path,
+                      {"LOGTRAWL_READ_WINDOW": "4093", "GLOP_STREAM_WINDOW": "997"})
+        assert rc == 1 and out == golden(f"cli_big_{eng}.jsonl"), eng
     w1 = run([cli, "scan", "-r", "big.rules", "--workers", "1", "big.log"], tmp_path)[1]
     w8 = run([cli, "scan", "-r", "big.rules", "--workers", "8", "big.log"], tmp_path)[1]
     we = run([cli, "scan", "-r", "big.rules", "big.log"], tmp_path, {"LOGTRAWL_WORKERS": "3"})[1]
