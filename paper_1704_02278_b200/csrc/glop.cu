@@ -247,11 +247,10 @@ glop_status p8_geometry(glop_ctx* c, const uint8_t* d_text, uint64_t own, P8Geom
 glop_status launch_pfac8(glop_ctx* c, const glop_trie* t, const P8Geom& G, const P8Params& p) {
   using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
 #define GLOP_P8_K(w, l, c) {pfac8_kernel<w, l, uint16_t, c>, pfac8_kernel<w, l, uint32_t, c>}
-  static const KF table[2][2][3][2] = {
-      {{GLOP_P8_K(false, 0, false), GLOP_P8_K(false, 1, false), GLOP_P8_K(false, 2, false)},
-       {GLOP_P8_K(true, 0, false), GLOP_P8_K(true, 1, false), GLOP_P8_K(true, 2, false)}},
-      {{GLOP_P8_K(false, 0, true), GLOP_P8_K(false, 1, true), GLOP_P8_K(false, 2, true)},
-       {GLOP_P8_K(true, 0, true), GLOP_P8_K(true, 1, true), GLOP_P8_K(true, 2, true)}}};
+#define GLOP_P8_L(w, c) GLOP_P8_K(w, 0, c), GLOP_P8_K(w, 1, c), GLOP_P8_K(w, 2, c), GLOP_P8_K(w, 3, c)
+  static const KF table[2][2][4][2] = {{{GLOP_P8_L(false, false)}, {GLOP_P8_L(true, false)}},
+                                       {{GLOP_P8_L(false, true)}, {GLOP_P8_L(true, true)}}};
+#undef GLOP_P8_L
 #undef GLOP_P8_K
   const P8Layout L = make_p8_layout();
   const KF k = table[t->p8_careful][t->info.max_depth > 8][t->p8_l1][t->u16 ? 0 : 1];
@@ -1301,7 +1300,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
   std::vector<unsigned long long> grams8;  // (p8_gram << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
-  bool bits8 = false, bloom2 = false;
+  bool bits8 = false, bloom2 = false, two8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -1357,11 +1356,17 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       grams8.erase(std::unique(grams8.begin(), grams8.end()), grams8.end());
       const char* env = getenv("GLOP_P8_BITS_MIN");  // experiments: override the layout threshold
       bits8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8BitsGrams);
+      const char* env2 = getenv("GLOP_P8_BITS2_MIN");  // experiments: override the two-bit threshold
+      two8 = bits8 && grams8.size() > (env2 ? (size_t)atoll(env2) : (size_t)kP8Bits2Grams);
       for (unsigned long long x : grams8) {
         const uint32_t g = (uint32_t)(x >> 2), bit = 1u << (x & 3);
         if (bits8) {
           const uint32_t h = p8_h1<true>(g);
           dmask8[h >> 3] |= (uint8_t)(1u << (h & 7));  // little-endian bit h of the u32 words
+          if (two8) {  // second bit in the same 32-bit word
+            const uint32_t h2 = (h & ~31u) | (p8_h1b(g) & 31u);
+            dmask8[h2 >> 3] |= (uint8_t)(1u << (h2 & 7));
+          }
         } else {
           dmask8[p8_h1<false>(g)] |= (uint8_t)bit;
         }
@@ -1430,7 +1435,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
-  t->p8_l1 = bloom2 ? 2 : bits8 ? 1 : 0;
+  t->p8_l1 = two8 && bloom2 ? 3 : bloom2 ? 2 : bits8 ? 1 : 0;
   t->p8_lane_emits = 4 * max_emits;
   t->p8_careful = t->p8_lane_emits > kP8Hits - GLOP_P8_FLUSH_AT || getenv("GLOP_P8_CAREFUL");
   t->view.jump_depth = J;

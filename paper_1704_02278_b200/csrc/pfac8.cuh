@@ -128,11 +128,19 @@ __host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur
   return (cur * 0x9E3779B1u) ^ (prev & 0xFF000000u);
 #endif
 }
-template <bool kBits>
+// Above kP8Bits2Grams grams (DPI: ~39K) one bit per gram passes ~7% of the
+// words on false positives alone; the "two bits in one word" layout (a
+// blocked Bloom filter: bits (g >> 13) & 31 and (g >> 8) & 31 of the word
+// g >> 18) passes ~1% for two more instructions and no extra shared-memory
+// wavefront per probe.
+constexpr uint32_t kP8Bits2Grams = 12000;
+__host__ __device__ __forceinline__ uint32_t p8_h1b(uint32_t g) { return g >> 8; }
+template <bool kBits, bool kTwo = false>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
   const uint32_t h = p8_h1<kBits>(g);
   if (kBits) {  // bit h & 31 of the word, in bit 0 (bits 1..31: don't care)
     const uint32_t w = reinterpret_cast<const uint32_t*>(dm)[h >> 5];
+    if (kTwo) return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, p8_h1b(g));
     return __funnelshift_r(w, w, h);
   }
   return dm[h];
@@ -193,7 +201,8 @@ __device__ __forceinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb
 }
 
 // kL1: 0 byte d-mask buckets; 1 one-bit buckets; 2 one-bit buckets and a
-// second level-2 bitmap probe (prefix_bit2_32) for large prefix sets.
+// second level-2 bitmap probe (prefix_bit2_32) for large prefix sets; 3 as 2
+// with two bits per gram in the level-1 word (kP8Bits2Grams).
 // kCareful: a replayed lane always starts with an empty hit buffer.  Without
 // it a replayed lane may start with up to GLOP_P8_FLUSH_AT keys, which is
 // exact but sends a lane emitting more than kP8Hits - GLOP_P8_FLUSH_AT ids to
@@ -204,7 +213,7 @@ template <bool kWalk, int kL1, typename Entry, bool kCareful>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
-  constexpr bool kBits = kL1 != 0, kB2 = kL1 == 2;
+  constexpr bool kBits = kL1 != 0, kB2 = kL1 >= 2, kTwo = kL1 == 3;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint8_t* s_dmask = smem + L.dmask;
@@ -338,14 +347,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (lane == 31) nb = wn;
         uint32_t* a = mm4[2 * hf];
         uint32_t* b = mm4[2 * hf + 1];
-        a[0] = p8_dmask<kBits>(s_dmask, p8_gram(va.x, va.y));
-        a[1] = p8_dmask<kBits>(s_dmask, p8_gram(va.y, va.z));
-        a[2] = p8_dmask<kBits>(s_dmask, p8_gram(va.z, va.w));
-        a[3] = p8_dmask<kBits>(s_dmask, p8_gram(va.w, na));
-        b[0] = p8_dmask<kBits>(s_dmask, p8_gram(vb.x, vb.y));
-        b[1] = p8_dmask<kBits>(s_dmask, p8_gram(vb.y, vb.z));
-        b[2] = p8_dmask<kBits>(s_dmask, p8_gram(vb.z, vb.w));
-        b[3] = p8_dmask<kBits>(s_dmask, p8_gram(vb.w, nb));
+        a[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.x, va.y));
+        a[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.y, va.z));
+        a[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.z, va.w));
+        a[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.w, na));
+        b[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.x, vb.y));
+        b[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.y, vb.z));
+        b[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.z, vb.w));
+        b[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.w, nb));
         if (kBits) {  // byte j = probe j's bit 0
           mq[2 * hf] = __byte_perm(__byte_perm(a[0], a[1], 0x40), __byte_perm(a[2], a[3], 0x40), 0x5410) & 0x01010101u;
           mq[2 * hf + 1] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410) & 0x01010101u;
