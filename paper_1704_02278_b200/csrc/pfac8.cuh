@@ -94,7 +94,7 @@ struct P8Params {
 };
 
 // Level-1 d-mask of an aligned text word (bit d-1: the word may be the
-// 4-gram at offset d of some 8-byte prefix), one hashed probe.  A two-hash
+// 5-gram at offset d of some 8-byte prefix), one hashed probe.  A two-hash
 // Bloom variant halved the candidate words but doubled the bank-conflicted
 // shared-memory probes, which bound the kernel (measured: 3.63 -> 3.55 ms at
 // k=1,000 and 2.46 -> 1.97 ms at k=10 without it).  Built by glop_trie_upload.
@@ -110,40 +110,59 @@ constexpr uint32_t kP8BitsGrams = 1024;
 // Above this many 8-byte prefixes the 2^18-bit level-2 bitmap passes too many
 // (word, d) pairs to the exact L2 probe: set and test a second bit per prefix.
 constexpr uint32_t kP8Bloom2Keys = 3000;
-template <bool kBits>
-__host__ __device__ __forceinline__ uint32_t p8_h1(uint32_t g) {
-  return g >> (32 - kP8DmaskLog2 - (kBits ? 3 : 0));
+// Level-1 probe of sample word i over the 5 bytes [4i-1, 4i+4) -- the
+// aligned word `cur` and the top byte of the previous word -- which for a
+// match at c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes
+// instead of four cut the candidate words by ~40% on the syslog vocabulary
+// set.  Two key schemes (kX):
+//  * false: key = cur * K ^ (prev's top byte); table word = key's top 14
+//    bits, bit = the next 5 (IMAD, LOP3, SHF, LOP3, LDS, SHF, SHF);
+//  * true (the two-bit layout, >= kP8Bits2Grams grams): key = cur ^ (prev's
+//    top byte); table word = the high half of key * K masked to a word offset
+//    (IMAD.HI + LOP3: no shift), bits = key & 31 and (key >> 8) & 31 (the
+//    funnel shift takes its amount straight from the key).  Two instructions
+//    fewer per probe (DPI 1.87 -> 1.81 ms, syslog k=10,000 3.04 -> 2.86 ms),
+//    but the XOR-merged key collides on text structure: small gram sets see
+//    more false candidates (k=10: 1.62 -> 1.76 ms), so only the large ones
+//    use it.
+constexpr uint32_t kP8HashMul = 0x9E3779B1u;
+template <bool kX>
+__host__ __device__ __forceinline__ uint32_t p8_key(uint32_t prev, uint32_t cur) {
+  return kX ? cur ^ (prev & 0xFF000000u) : (cur * kP8HashMul) ^ (prev & 0xFF000000u);
 }
-// Level-1 hash of sample word i over the 5 bytes [4i-1, 4i+4) -- the aligned
-// word `cur` and the top byte of the previous word -- which for a match at
-// c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes instead of
-// four cut the candidate words by ~40% on the syslog vocabulary set; the
-// fifth byte is XORed (LOP3, together with its mask) into the top of the
-// multiplicative hash of `cur`, so a probe is IMAD + LOP3 + SHF + LDS.
-// p8_h1 takes the top bits.  (GLOP_P8_Q4: the plain aligned 4-gram.)
-__host__ __device__ __forceinline__ uint32_t p8_gram(uint32_t prev, uint32_t cur) {
-#ifdef GLOP_P8_Q4
-  return cur * 0x9E3779B1u;
+__host__ __device__ __forceinline__ uint32_t p8_mulhi(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(x, kP8HashMul);
 #else
-  return (cur * 0x9E3779B1u) ^ (prev & 0xFF000000u);
+  return (uint32_t)(((unsigned long long)x * kP8HashMul) >> 32);
 #endif
 }
+// byte offset of the key's 32-bit word in the 64 KB bit table (kBits)
+template <bool kX>
+__host__ __device__ __forceinline__ uint32_t p8_word_off(uint32_t key) {
+  return kX ? p8_mulhi(key) & (kP8DmaskBytes - 4) : (key >> (32 - kP8DmaskLog2)) & (kP8DmaskBytes - 4);
+}
+// funnel-shift amounts (low 5 bits) of the key's bit(s) inside that word
+template <bool kX>
+__host__ __device__ __forceinline__ uint32_t p8_bit1(uint32_t key) {
+  return kX ? key : key >> (32 - kP8DmaskLog2 - 3);
+}
+__host__ __device__ __forceinline__ uint32_t p8_bit2(uint32_t key) { return key >> 8; }
+// the key's byte in the 64 KB d-mask table (!kBits)
+__host__ __device__ __forceinline__ uint32_t p8_byte_off(uint32_t key) { return key >> (32 - kP8DmaskLog2); }
 // Above kP8Bits2Grams grams (DPI: ~39K) one bit per gram passes ~7% of the
 // words on false positives alone; the "two bits in one word" layout (a
-// blocked Bloom filter: bits (g >> 13) & 31 and (g >> 8) & 31 of the word
-// g >> 18) passes ~1% for two more instructions and no extra shared-memory
-// wavefront per probe.
+// blocked Bloom filter: bits p8_bit1 and p8_bit2 of the word) passes ~1% for
+// two more instructions and no extra shared-memory wavefront per probe.
 constexpr uint32_t kP8Bits2Grams = 12000;
-__host__ __device__ __forceinline__ uint32_t p8_h1b(uint32_t g) { return g >> 8; }
 template <bool kBits, bool kTwo = false>
-__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t g) {
-  const uint32_t h = p8_h1<kBits>(g);
-  if (kBits) {  // bit h & 31 of the word, in bit 0 (bits 1..31: don't care)
-    const uint32_t w = reinterpret_cast<const uint32_t*>(dm)[h >> 5];
-    if (kTwo) return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, p8_h1b(g));
-    return __funnelshift_r(w, w, h);
+__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t key) {
+  if (kBits) {  // bit p8_bit1 of the word, in bit 0 (bits 1..31: don't care)
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_word_off<kTwo>(key));
+    if (kTwo) return __funnelshift_r(w, w, p8_bit1<kTwo>(key)) & __funnelshift_r(w, w, p8_bit2(key));
+    return __funnelshift_r(w, w, p8_bit1<kTwo>(key));
   }
-  return dm[h];
+  return dm[p8_byte_off(key)];
 }
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
@@ -347,14 +366,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (lane == 31) nb = wn;
         uint32_t* a = mm4[2 * hf];
         uint32_t* b = mm4[2 * hf + 1];
-        a[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.x, va.y));
-        a[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.y, va.z));
-        a[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.z, va.w));
-        a[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(va.w, na));
-        b[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.x, vb.y));
-        b[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.y, vb.z));
-        b[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.z, vb.w));
-        b[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_gram(vb.w, nb));
+        a[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.x, va.y));
+        a[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.y, va.z));
+        a[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.z, va.w));
+        a[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.w, na));
+        b[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.x, vb.y));
+        b[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.y, vb.z));
+        b[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.z, vb.w));
+        b[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.w, nb));
         if (kBits) {  // byte j = probe j's bit 0
           mq[2 * hf] = __byte_perm(__byte_perm(a[0], a[1], 0x40), __byte_perm(a[2], a[3], 0x40), 0x5410) & 0x01010101u;
           mq[2 * hf + 1] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410) & 0x01010101u;
