@@ -3,7 +3,10 @@
 // logtrawl/kmp.hpp).  The failure table stays a host computation; the search
 // runs on the B200 as a chunk-parallel KMP with an (m-1)-byte warm-up overlap
 // per chunk, reporting the same ascending, overlapping offsets and exactly the
-// sequential algorithm's comparison count.
+// sequential algorithm's comparison count.  A failure table that is not the
+// pattern's prefix function (the reference runs whatever table it is given),
+// or a pattern of 8,192 bytes or more, runs the reference's sequential loop on
+// one device thread instead -- same results, no parallelism.
 #include <algorithm>
 #include <cstdint>
 #include <cstring>

@@ -77,7 +77,8 @@ def gather_alerts_to_root(alerts, n: int, root: int = 0, group=None):
     sorted: owned ranges are ascending and disjoint).  One all_gather of the
     row counts, then point-to-point sends to the root (NCCL send/recv over
     NVLink on the B200 box; gloo in the CPU tests).  Returns the
-    concatenation on the root and None elsewhere."""
+    concatenation on the root and None elsewhere.  `root` is a rank of `group`
+    (the default group: a global rank)."""
     import torch
     import torch.distributed as dist
 
@@ -90,9 +91,13 @@ def gather_alerts_to_root(alerts, n: int, root: int = 0, group=None):
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     sizes = [int(c.item()) for c in cnts]
+
+    def glob(r):  # send/recv address GLOBAL ranks; `root` and the loop index are group ranks
+        return r if group is None else dist.get_global_rank(group, r)
+
     if rank != root:
         if n:
-            dist.send(alerts[:n].contiguous(), dst=root, group=group)
+            dist.send(alerts[:n].contiguous(), dst=glob(root), group=group)
         return None
     parts = []
     for r, sz in enumerate(sizes):
@@ -100,7 +105,7 @@ def gather_alerts_to_root(alerts, n: int, root: int = 0, group=None):
             parts.append(alerts[:n])
         elif sz:
             buf = torch.empty((sz,) + tuple(alerts.shape[1:]), dtype=alerts.dtype, device=alerts.device)
-            dist.recv(buf, src=r, group=group)
+            dist.recv(buf, src=glob(r), group=group)
             parts.append(buf)
     return torch.cat(parts, dim=0) if parts else alerts[:0]
 

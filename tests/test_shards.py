@@ -118,3 +118,42 @@ def test_plan_shards_c_abi_matches_python():
         c = glop.plan_shards_c(n, world, halo)
         py = [(s.lo, s.own, s.read) for s in plan_shards(n, world, halo)]
         assert c == py, (n, world, halo)
+
+
+def _subgroup_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1704_02278_b200.shards import gather_alerts_to_root
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sub = dist.new_group([1, 2])  # group ranks 0, 1 = global ranks 1, 2
+        if rank in (1, 2):
+            rows = torch.full((rank, 16), rank, dtype=torch.uint8)
+            out = gather_alerts_to_root(rows, rank, root=0, group=sub)  # root: group rank 0 = global rank 1
+            q.put((rank, None if out is None else out.numpy().tobytes()))
+        else:
+            q.put((rank, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_gather_to_root_in_a_subgroup():
+    """with a non-default group, send/recv must address global
+    ranks: root = group rank 0 (global 1) receives group rank 1's rows."""
+    import torch.multiprocessing as mp
+
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_subgroup_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] is None and res[2] is None
+    assert res[1] == bytes([1] * 16 + [2] * 32)
