@@ -342,6 +342,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.config == "pfac":
+        return bench_group(args)  # one process driving N GPUs through the C ABI's device group
     # GLOP_BENCH_ONE_GPU=1: functional check of the N>1 path on a one-GPU box
     # (all ranks on cuda:0, gloo instead of NCCL); never used for numbers.
     one_gpu = os.environ.get("GLOP_BENCH_ONE_GPU") == "1"
@@ -628,6 +630,108 @@ def run_e2e_dropin(args, glop, d_text, sh, pats):
             "d2h_bytes_per_step": int(alerts.nbytes), "ms_per_step": round(dt * 1e3, 3), "steps": steps,
             "api": "logtrawl::run_engine_scan (include/logtrawl/pipeline.hpp, pfac_compact) via libglop_engine.so, "
                    "text in pageable host memory"}
+
+
+def bench_group(args):
+    """`python bench.py --gpus N` without torchrun: one process drives N GPUs
+    through libglop's device group -- per-member contexts scanning their
+    halo'd shard (glop_run_pfac_pipeline_device) concurrently from host
+    threads, device-timed with CUDA events on each member's stream, max over
+    members; e2e through glop_group_run_pfac_pipeline on pinned host text.
+    GLOP_BENCH_DEVICES="0,0" runs the N-way split on one GPU (functional
+    check, not a number)."""
+    import threading as th
+
+    import numpy as np
+    import torch
+
+    from paper_1704_02278_b200 import glop
+    from paper_1704_02278_b200.shards import plan_shards
+
+    devs = [int(x) for x in os.environ.get("GLOP_BENCH_DEVICES", ",".join(map(str, range(args.gpus)))).split(",")]
+    N = len(devs)
+    S = int(args.bytes_per_gpu)
+    total = S * N
+    pats, _, gen_dev = workload_rules(args, glop)
+    ctxs = [glop.Context(d) for d in devs]
+    tries = [c.upload(glop.build_failureless_trie(pats, args.prefix_len)) for c in ctxs]
+    rules = [c.upload_rules(pats, args.prefix_len) for c in ctxs]
+    halo = max(tries[0].info.max_depth, max(len(p) for p in pats)) - 1
+    shards = plan_shards(total, N, halo)
+    cap = max(1 << 20, S // 256)
+    bufs = []
+    for c, d, sh in zip(ctxs, devs, shards):
+        with torch.cuda.device(d):
+            t = torch.empty(sh.read + 64, dtype=torch.uint8, device=f"cuda:{d}")
+            a = torch.empty(cap * 16, dtype=torch.uint8, device=f"cuda:{d}")
+            k = torch.zeros(len(pats), dtype=torch.int64, device=f"cuda:{d}")
+        getattr(c, gen_dev)(t.data_ptr(), sh.read, args.seed, begin=sh.lo)
+        bufs.append((t, a, k))
+    for c in ctxs:
+        c.synchronize()
+    res = [None] * N
+
+    def member(g, steps):
+        c, (t, a, k), sh = ctxs[g], bufs[g], shards[g]
+        with torch.cuda.device(devs[g]):
+            s0 = torch.cuda.ExternalStream(c.stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s0)
+            for _ in range(steps):
+                r = c.run_pfac_pipeline_device(tries[g], rules[g], t.data_ptr(), sh.read, a.data_ptr(), cap,
+                                               k.data_ptr(), own=sh.own, base=sh.lo)
+            e1.record(s0)
+            c.synchronize()
+            res[g] = (e0.elapsed_time(e1) / max(steps, 1), r)
+
+    def run(steps):
+        ts = [th.Thread(target=member, args=(g, steps)) for g in range(N)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    run(max(args.warmup, 3))
+    sampler = ClockSampler(devs[0])
+    with sampler:
+        sampler.settle(lambda: run(1))
+        run(args.steps)
+        sampler.hold(lambda: run(1))
+    ms = max(r[0] for r in res)
+    nh = sum(r[1][0] for r in res)
+    na = sum(r[1][1] for r in res)
+    peak, peak_src = peaks()
+    line = {"metric": METRIC, "value": round(8 * total / (ms / 1e3) / 1e9, 2), "unit": "Gbps", "n_gpus": N,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic RFC 5424 syslog generated on device (csrc/corpus.h), seeded",
+            "config": dict(workload_config(args, N), parallelism=f"group{N} (one process, libglop device group)",
+                           devices=devs),
+            "roofline": {"bound": "hbm", "achieved": round(total / (ms / 1e3) / 1e9, 1), "peak": peak * N,
+                         "unit": "GB/s", "frac": round(total / (ms / 1e3) / 1e9 / (peak * N), 4),
+                         "traffic": None, "peak_source": peak_src + f" x {N} GPUs", "kernel": "pfac8_kernel (step)"},
+            "clocks": sampler.summary(),
+            "results": {"stage1_hits_per_step": int(nh), "alerts_per_step": int(na)}}
+    if not args.no_e2e:
+        g = glop.Group(devs)
+        gt, gr = g.upload(glop.build_failureless_trie(pats, args.prefix_len)), g.upload_rules(pats, args.prefix_len)
+        try:
+            host = np.empty(total, dtype=np.uint8)
+            for (t, _, _), sh in zip(bufs, shards):
+                host[sh.lo:sh.lo + sh.own] = t[:sh.own].cpu().numpy()
+            g.run_pfac_pipeline(gt, gr, host)
+            t0 = time.perf_counter()
+            steps = max(1, min(args.e2e_steps or args.steps, 5))
+            for _ in range(steps):
+                alerts, counts, s1, _, _ = g.run_pfac_pipeline(gt, gr, host)
+            dt = (time.perf_counter() - t0) / steps
+            line["e2e"] = {"value": round(8 * total / dt / 1e9, 2), "unit": "Gbps", "h2d_bytes_per_step": total,
+                           "d2h_bytes_per_step": int(alerts.nbytes + counts.nbytes), "ms_per_step": round(dt * 1e3, 3),
+                           "api": "glop_group_run_pfac_pipeline (pageable host text)"}
+        except MemoryError as e:
+            line["e2e"] = {"unavailable": f"host copy of {total} bytes: {e}"}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
