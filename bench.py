@@ -408,6 +408,21 @@ def main():
                 gather_alerts_to_root(d_alerts.view(-1, 16), na, root=0)
         return nh, na
 
+    # N = 1: steps are submitted back to back (glop_run_pfac_pipeline_device_async,
+    # each step's status lands in a pinned ticket) and checked after the
+    # closing synchronize -- the host never idles the GPU between steps.
+    pipelined = world == 1 and kernel == glop.PFAC_AUTO
+    n_tickets = max(args.steps, 8)
+    tickets = ctx.host_alloc(glop.TICKET_BYTES * n_tickets) if pipelined else None
+
+    def submit(i):
+        ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), sh.read, d_alerts.data_ptr(), cap,
+                                           d_counts.data_ptr(), tickets + glop.TICKET_BYTES * (i % n_tickets),
+                                           own=sh.own, base=sh.lo)
+
+    def results(count):
+        return [glop.ticket_result(tickets + glop.TICKET_BYTES * i) for i in range(count)]
+
     for _ in range(max(args.warmup, 3)):
         nh, na = step()
     ctx.synchronize()
@@ -421,13 +436,23 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         kms = []
-        for _ in range(args.steps):
-            nh, na = step()
-            kms.append(ctx.last_kernel_ms())
+        for i in range(args.steps):
+            if pipelined:
+                submit(i)
+            else:
+                nh, na = step()
+                kms.append(ctx.last_kernel_ms())
         ev1.record(stream)
         ctx.synchronize()
         barrier()
         launches = ctx.launches - l0
+        if pipelined:  # every step's result, checked now (GLOP_EAGAIN would raise: the step needs the sync path)
+            got = results(min(args.steps, n_tickets))
+            assert len(set(got)) == 1, f"steps disagree: {set(got)}"
+            nh, na = got[-1]
+            for _ in range(args.steps):  # the dominant kernel's own device time, per launch
+                step()
+                kms.append(ctx.last_kernel_ms())
         if world == 1:
             sampler.hold(lambda: (step(), ctx.synchronize()))
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
@@ -484,6 +509,8 @@ def main():
         sample = min(sh.own, 2 << 30)
         host = d_text[:sample].cpu().numpy()
         line["cpu_baseline"] = cpu_baseline_pfac(host, pats, args.prefix_len, args.cpu_seconds)
+    if tickets:
+        ctx.host_free(tickets)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -544,15 +571,28 @@ def sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak):
     for _ in range(3):
         r = step()
     ctx.synchronize()
+    pipelined = c["kind"] != "kmp"  # as the headline: PFAC steps submitted back to back, tickets checked after
+    tickets = ctx.host_alloc(glop.TICKET_BYTES * steps) if pipelined else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     kms = []
-    for _ in range(steps):
-        r = step()
-        kms.append(ctx.last_kernel_ms())
+    for i in range(steps):
+        if pipelined:
+            ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), n, d_alerts.data_ptr(), cap,
+                                               d_counts.data_ptr(), tickets + glop.TICKET_BYTES * i)
+        else:
+            r = step()
+            kms.append(ctx.last_kernel_ms())
     ev1.record(stream)
     ctx.synchronize()
     ms = ev0.elapsed_time(ev1) / steps
+    if pipelined:
+        got = {glop.ticket_result(tickets + glop.TICKET_BYTES * i) for i in range(steps)}
+        ctx.host_free(tickets)
+        assert len(got) == 1, got
+        for _ in range(steps):
+            r = step()
+            kms.append(ctx.last_kernel_ms())
     kernel_ms = statistics.mean(kms)
     gbs = n / (kernel_ms / 1e3) / 1e9
     out = {"config": c["config"], "workload": c["workload"], "bytes": n, "steps": steps, "kernel": kname,

@@ -38,7 +38,8 @@ typedef enum {
   GLOP_ECAPACITY = 2, /* reference: logtrawl::CapacityError            */
   GLOP_ELOGIC = 3,    /* reference: std::logic_error (verify.hpp:76-77) */
   GLOP_ECUDA = 4,     /* device / driver failure (std::runtime_error)   */
-  GLOP_ENOMEM = 5     /* allocation failure (std::bad_alloc)            */
+  GLOP_ENOMEM = 5,    /* allocation failure (std::bad_alloc)            */
+  GLOP_EAGAIN = 6     /* an asynchronous call must be redone synchronously */
 } glop_status;
 
 /* Layout-identical to logtrawl::Hit (scan.hpp:31-41) on LP64: 16 bytes. */
@@ -221,6 +222,27 @@ glop_status glop_run_pfac_pipeline_device(glop_ctx* ctx, const glop_trie* trie, 
                                           glop_hit* d_hits, uint64_t hit_cap, glop_alert* d_alerts,
                                           uint64_t alert_cap, uint64_t* d_counts, uint64_t* n_hits,
                                           uint64_t* n_alerts);
+
+/* Asynchronous form for pipelined submission (a stream of shards, the bench
+ * step): enqueues the same work and returns without waiting; the status block
+ * is copied (stream-ordered) into *ticket, which must stay valid -- pinned
+ * host memory (glop_host_alloc) -- until the context stream is synchronized.
+ * Then glop_pipeline_ticket_result gives (n_hits, n_alerts) or the error; it
+ * returns GLOP_EAGAIN when this input needs the synchronous call (a hit-dense
+ * input that overflowed a warp's hit buffer or staging region: its outputs are
+ * not valid, rerun it with glop_run_pfac_pipeline_device).  Automata without
+ * the fused path run synchronously here and complete the ticket at once. */
+typedef struct {
+  uint64_t raw[8];  /* device status block */
+  uint64_t region, hit_cap, alert_cap;
+  uint32_t stage2, done;
+} glop_pipeline_ticket;
+glop_status glop_run_pfac_pipeline_device_async(glop_ctx* ctx, const glop_trie* trie, const glop_rules* rules,
+                                                const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                                glop_hit* d_hits, uint64_t hit_cap, glop_alert* d_alerts,
+                                                uint64_t alert_cap, uint64_t* d_counts,
+                                                glop_pipeline_ticket* ticket);
+glop_status glop_pipeline_ticket_result(const glop_pipeline_ticket* ticket, uint64_t* n_hits, uint64_t* n_alerts);
 
 /* ---- measurement ----------------------------------------------------------
  * Device time of the most recent PFAC / KMP scan kernel on this context,

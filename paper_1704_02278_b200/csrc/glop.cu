@@ -694,7 +694,7 @@ glop_status verify_device_impl(glop_ctx* c, const glop_rules* r, const uint8_t* 
 glop_status pipeline_device_impl(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* d_text,
                                  uint64_t n, uint64_t own, uint64_t base, glop_hit* d_hits, uint64_t hit_cap,
                                  glop_alert* d_alerts, uint64_t alert_cap, uint64_t* d_counts, uint64_t* n_hits,
-                                 uint64_t* n_alerts) {
+                                 uint64_t* n_alerts, glop_pipeline_ticket* ticket = nullptr) {
   *n_hits = *n_alerts = 0;
   if (own > n) return fail(GLOP_EINVAL, "run_pfac_pipeline: own > n");
   const uint32_t k = r->view.n_patterns;
@@ -749,6 +749,15 @@ glop_status pipeline_device_impl(glop_ctx* c, const glop_trie* t, const glop_rul
     }
     c->launches += 2;
     CU(cudaGetLastError());
+    if (ticket) {  // no host wait: the status block lands in the ticket, read after the stream syncs
+      ticket->region = G.region;
+      ticket->hit_cap = d_hits ? hit_cap : ~0ull;
+      ticket->alert_cap = alert_cap;
+      ticket->stage2 = stage2;
+      ticket->done = 0;
+      CU(cudaMemcpyAsync(ticket->raw, c->misc.p, sizeof ticket->raw, cudaMemcpyDeviceToHost, c->stream));
+      return GLOP_OK;
+    }
     TRY(sync_read(c, c->misc.p, 64));
     const unsigned long long* h = c->h_misc;
     const unsigned flags = (unsigned)(h[kStFlags] & 0xffffffffu);
@@ -1946,6 +1955,47 @@ glop_status pipeline_host(glop_ctx* c, const glop_trie* t, const glop_rules* r, 
 }  // namespace
 
 extern "C" {
+
+glop_status glop_run_pfac_pipeline_device_async(glop_ctx* c, const glop_trie* t, const glop_rules* r,
+                                                const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                                glop_hit* d_hits, uint64_t hit_cap, glop_alert* d_alerts,
+                                                uint64_t alert_cap, uint64_t* d_counts,
+                                                glop_pipeline_ticket* ticket) {
+  if (!c || !t || !r || !ticket || (!d_alerts && alert_cap))
+    return fail(GLOP_EINVAL, "glop_run_pfac_pipeline_device_async: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  uint64_t nh = 0, na = 0;
+  memset(ticket, 0, sizeof *ticket);
+  const glop_status s = pipeline_device_impl(c, t, r, d_text, n, own, base, d_hits, hit_cap, d_alerts, alert_cap,
+                                             d_counts, &nh, &na, ticket);
+  if (s != GLOP_OK || ticket->region == 0) {
+    // failed, or the general path ran synchronously: the ticket holds the outcome
+    ticket->done = s == GLOP_OK ? 1 : 2;
+    ticket->raw[0] = nh;
+    ticket->raw[5] = na;
+    ticket->raw[7] = (uint64_t)s;
+  }
+  return s;
+}
+
+glop_status glop_pipeline_ticket_result(const glop_pipeline_ticket* k, uint64_t* n_hits, uint64_t* n_alerts) {
+  if (!k || !n_hits || !n_alerts) return fail(GLOP_EINVAL, "glop_pipeline_ticket_result: null argument");
+  if (k->done == 1) {  // completed synchronously
+    *n_hits = k->raw[0];
+    *n_alerts = k->raw[5];
+    return GLOP_OK;
+  }
+  if (k->done == 2) return fail((glop_status)k->raw[7], "run_pfac_pipeline: failed");
+  const uint64_t* h = k->raw;
+  if ((h[kStFlags] & 1u) || h[kStMaxRegion] > k->region)
+    return fail(GLOP_EAGAIN, "run_pfac_pipeline: this input needs the synchronous path (hit buffer / staging overflow)");
+  if (h[kStVerify] & 1u) return fail(GLOP_ELOGIC, "verify_hits: hit extends past end of text");
+  *n_hits = h[kStTotal];
+  *n_alerts = k->stage2 ? h[kStKept] : h[kStTotal];
+  if (*n_hits > k->hit_cap || *n_alerts > k->alert_cap) return fail(GLOP_ECAPACITY, "run_pfac_pipeline: output capacity");
+  return GLOP_OK;
+}
 
 glop_status glop_run_pfac_pipeline_device(glop_ctx* c, const glop_trie* t, const glop_rules* r,
                                           const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,

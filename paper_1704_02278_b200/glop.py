@@ -48,7 +48,11 @@ class OutOfMemory(GlopError, MemoryError):
     code = 5
 
 
-_ERRORS = {c.code: c for c in (InvalidArgument, CapacityError, LogicError, CudaError, OutOfMemory)}
+class Again(GlopError):  # an asynchronous call must be redone synchronously
+    code = 6
+
+
+_ERRORS = {c.code: c for c in (InvalidArgument, CapacityError, LogicError, CudaError, OutOfMemory, Again)}
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -98,6 +102,18 @@ _lib.glop_ctx_fallback_count.argtypes = [vp]
 _lib.glop_ctx_fallback_count.restype = C.c_uint64
 _sig("glop_run_pfac_pipeline_device", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64, vp,
      C.c_uint64, vp, u64p, u64p)
+_sig("glop_run_pfac_pipeline_device_async", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64, vp,
+     C.c_uint64, vp, vp)
+_sig("glop_pipeline_ticket_result", vp, u64p, u64p)
+TICKET_BYTES = 8 * 8 + 3 * 8 + 2 * 4  # glop_pipeline_ticket
+
+
+def ticket_result(ticket_ptr: int):
+    """(n_hits, n_alerts) of an asynchronous pipeline call, once its context's
+    stream is synchronized; raises Again when it must be redone synchronously."""
+    nh, na = C.c_uint64(), C.c_uint64()
+    _check(_lib.glop_pipeline_ticket_result(ticket_ptr, C.byref(nh), C.byref(na)), "pipeline_ticket_result")
+    return nh.value, na.value
 _sig("glop_rules_upload", vp, u8p, u64p, C.c_uint32, C.c_uint64, C.POINTER(vp))
 _sig("glop_rules_destroy", vp)
 _sig("glop_verify_hits", vp, vp, vp, C.c_uint64, C.c_int, vp, C.c_uint64, C.c_int, C.POINTER(vp), u64p, u64p)
@@ -379,6 +395,17 @@ class Context:
                                                   d_hits, hit_cap, d_alerts, alert_cap, d_counts, C.byref(nh),
                                                   C.byref(na)), "run_pfac_pipeline_device")
         return nh.value, na.value
+
+    def run_pfac_pipeline_device_async(self, trie: DeviceTrie, rules: DeviceRules, d_text: int, n: int,
+                                       d_alerts: int, alert_cap: int, d_counts: int | None, ticket: int,
+                                       own: int | None = None, base: int = 0, d_hits: int | None = None,
+                                       hit_cap: int = 0):
+        """Enqueue the device pipeline without waiting; `ticket` (pinned host
+        memory, TICKET_BYTES) receives the status -- read it with
+        ticket_result() after synchronize()."""
+        _check(_lib.glop_run_pfac_pipeline_device_async(self.h, trie.h, rules.h, d_text, n, n if own is None else own,
+                                                        base, d_hits, hit_cap, d_alerts, alert_cap, d_counts, ticket),
+               "run_pfac_pipeline_device_async")
 
     @property
     def fallbacks(self) -> int:

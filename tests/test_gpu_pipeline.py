@@ -157,3 +157,49 @@ def test_dropin_engine_pageable_with_lines(engine):
         assert s1 == len(r_hits)
     else:
         assert s1 == len(r_alerts)  # ac_chunked matches full patterns: every hit is an alert
+
+
+def test_async_pipeline_tickets(ctx, torch_cuda):
+    """glop_run_pfac_pipeline_device_async: several submissions back to back,
+    each ticket read after one synchronize equals the synchronous call; a
+    hit-dense input that overflows a warp's buffer reports Again (its outputs
+    are not valid) and the synchronous call then gives the exact result."""
+    torch = torch_cuda
+    pats, text = corpus_case(11, 1000, [b"Failed password for invalid user"])
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    rules = ctx.upload_rules(pats, 8)
+    d = torch.from_numpy(np.concatenate([text, np.zeros(64, np.uint8)])).cuda()
+    cap = 1 << 20
+    d_alerts = torch.empty(cap * 16, dtype=torch.uint8, device="cuda")
+    d_counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+    r_hits, r_alerts, r_counts = oracle(pats, text)
+    tickets = ctx.host_alloc(glop.TICKET_BYTES * 4)
+    try:
+        for i in range(4):
+            ctx.run_pfac_pipeline_device_async(trie, rules, d.data_ptr(), text.size, d_alerts.data_ptr(), cap,
+                                               d_counts.data_ptr(), tickets + glop.TICKET_BYTES * i)
+        ctx.synchronize()
+        for i in range(4):
+            assert glop.ticket_result(tickets + glop.TICKET_BYTES * i) == (len(r_hits), len(r_alerts))
+        alerts = d_alerts[: len(r_alerts) * 16].cpu().numpy().view(glop.ALERT_DTYPE)
+        assert np.array_equal(alerts16(alerts), alerts16(r_alerts))
+        assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64), r_counts)
+        # hit-dense: every position of an 'A' run matches several patterns
+        dense = np.full(1 << 16, 65, np.uint8)
+        dpats = [b"AAAAAAAA" + bytes([66 + j]) for j in range(40)]
+        dt = ctx.upload(glop.build_failureless_trie(dpats, 8))
+        dr = ctx.upload_rules(dpats, 8)
+        dd = torch.from_numpy(np.concatenate([dense, np.zeros(64, np.uint8)])).cuda()
+        dcap = 1 << 23
+        da = torch.empty(dcap * 16, dtype=torch.uint8, device="cuda")
+        dc = torch.zeros(len(dpats), dtype=torch.int64, device="cuda")
+        ctx.run_pfac_pipeline_device_async(dt, dr, dd.data_ptr(), dense.size, da.data_ptr(), dcap, dc.data_ptr(),
+                                           tickets)
+        ctx.synchronize()
+        with pytest.raises(glop.Again):
+            glop.ticket_result(tickets)
+        nh, na = ctx.run_pfac_pipeline_device(dt, dr, dd.data_ptr(), dense.size, da.data_ptr(), dcap, dc.data_ptr())
+        h, a, c = oracle(dpats, dense)
+        assert (nh, na) == (len(h), len(a)) and nh > 0
+    finally:
+        ctx.host_free(tickets)
