@@ -171,6 +171,7 @@ def cpu_baseline_pfac(text_host, pats, L, target_s):
     mean = statistics.mean(secs)
     cores = int(ref.ref_default_workers()) if ref is not None else 1
     return {"value": round(8 * sample / mean / 1e9, 3), "unit": "Gbps", "cores": cores, "kind": kind,
+            "cpu_model": O.cpu_model(),
             "sample": f"first {sample} bytes of the GPU-0 shard, same {len(pats)} rules, L={L}; pfac_scan + "
                       f"verify_hits, {runs} timed runs after 1 warm-up, mean {mean:.3f} s/run, "
                       f"{'workers=hardware_concurrency' if kind == 'reference' else 'single thread'}"}
@@ -502,13 +503,13 @@ def main():
                               scope=f"rank 0's shard: starts [0, {S}) of the config's text, full size (untimed)")
     if world == 1 and args.config == "pfac" and not args.no_sweep:
         line["pattern_sweep"] = pattern_sweep(args, ctx, glop, d_text, sh, d_hits, cap, peak)
-    if world == 1 and args.config == "pfac" and not args.no_configs:
-        line["configs"] = [sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak)
-                           for c in SUB_CONFIGS]
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = min(sh.own, 2 << 30)
         host = d_text[:sample].cpu().numpy()
         line["cpu_baseline"] = cpu_baseline_pfac(host, pats, args.prefix_len, args.cpu_seconds)
+    if world == 1 and args.config == "pfac" and not args.no_configs:  # (overwrites d_text: after every use of it)
+        line["configs"] = [sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak)
+                           for c in SUB_CONFIGS]
     if tickets:
         ctx.host_free(tickets)
     if rank == 0:
@@ -830,7 +831,7 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
         if O.ref() is not None:
             secs, _ = O.ref_time_kmp(host, p, 1, 3)
             line["cpu_baseline"] = {"value": round(8 * sample / statistics.mean(secs) / 1e9, 3), "unit": "Gbps",
-                                    "cores": 1, "kind": "reference",
+                                    "cores": 1, "kind": "reference", "cpu_model": O.cpu_model(),
                                     "sample": f"kmp_multi on the first {sample} bytes, single thread by design"}
     if rank == 0:
         print(json.dumps(line), flush=True)
