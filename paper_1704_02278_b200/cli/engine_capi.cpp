@@ -3,7 +3,9 @@
 // callers that reach the reference's engine through an FFI (ctypes, cgo, JNI)
 // and for bench.py's `e2e_dropin` leg, which times exactly the call a
 // reference C++ caller makes: run_engine_scan on a pageable host buffer.
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -52,8 +54,10 @@ int glop_engine_run(void* rules, const char* text, uint64_t n, int engine, uint6
     const std::string_view tv(text, n);
     std::unique_ptr<logtrawl::LineIndex> idx;
     if (with_lines) idx = std::make_unique<logtrawl::LineIndex>(tv);
+    const auto t0 = std::chrono::steady_clock::now();
     const logtrawl::ScanReport rep =
         logtrawl::run_engine_scan(tv, *static_cast<logtrawl::RuleSet*>(rules), cfg, idx.get());
+    const auto t1 = std::chrono::steady_clock::now();
     const size_t na = rep.alerts.size();
     auto* a = static_cast<glop_alert*>(malloc(std::max<size_t>(na, 1) * sizeof(glop_alert)));
     auto* l = with_lines ? static_cast<uint64_t*>(malloc(std::max<size_t>(na, 1) * 8)) : nullptr;
@@ -63,6 +67,10 @@ int glop_engine_run(void* rules, const char* text, uint64_t n, int engine, uint6
         if (l) l[i] = rep.alerts[i].line;
       }
     });
+    if (std::getenv("GLOP_ENGINE_TIMING"))
+      std::fprintf(stderr, "engine: run_engine_scan %.1f ms, to C records %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     *alerts = a;
     if (lines) *lines = l;
     *n_alerts = na;

@@ -939,15 +939,28 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   if (pageable)
     for (int b = 0; b < 2; ++b)
       if (!c->pin[b]) CU(cudaMallocHost(&c->pin[b], kStreamChunk + halo + 64));
-  auto copy = [&](uint64_t i) -> glop_status {
-    const uint64_t lo = i * kStreamChunk;
-    const uint64_t rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - lo) + halo, n - lo);
-    const uint8_t* src = h_text + lo;
-    if (pageable) {  // the DMA out of pin[b] two chunks ago must be done
-      CU(cudaEventSynchronize(c->ev_copied[i & 1]));
-      parallel_memcpy(c->pin[i & 1], src, rd);
-      src = static_cast<const uint8_t*>(c->pin[i & 1]);
+  auto span = [&](uint64_t i, uint64_t* lo, uint64_t* rd) {
+    *lo = i * kStreamChunk;
+    *rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - *lo) + halo, n - *lo);
+  };
+  // pageable: a background thread stages chunk i + 2 into pin[i & 1] while
+  // chunk i + 1's DMA and chunk i's scan run, so the copy engine never waits
+  struct Stager {
+    std::thread th;
+    ~Stager() { join(); }
+    void join() {
+      if (th.joinable()) th.join();
     }
+  } stager;
+  auto stage = [&](uint64_t i) {  // pin[i & 1] must be free (its previous DMA done)
+    uint64_t lo, rd;
+    span(i, &lo, &rd);
+    stager.th = std::thread(parallel_memcpy, c->pin[i & 1], h_text + lo, rd);
+  };
+  auto dma = [&](uint64_t i) -> glop_status {
+    uint64_t lo, rd;
+    span(i, &lo, &rd);
+    const void* src = pageable ? c->pin[i & 1] : static_cast<const void*>(h_text + lo);
     CU(cudaStreamWaitEvent(c->cstream, c->ev_free[i & 1], 0));
     CU(cudaMemcpyAsync(c->sbuf[i & 1].p, src, rd, cudaMemcpyHostToDevice, c->cstream));
     CU(cudaEventRecord(c->ev_copied[i & 1], c->cstream));
@@ -956,9 +969,23 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   // ev_free[b]: buffer b may be overwritten (recorded after its chunk's work)
   CU(cudaEventRecord(c->ev_free[0], c->stream));
   CU(cudaEventRecord(c->ev_free[1], c->stream));
-  TRY(copy(0));
+  if (pageable) {
+    CU(cudaEventSynchronize(c->ev_copied[0]));  // (a previous call's DMA out of pin[0] / pin[1])
+    CU(cudaEventSynchronize(c->ev_copied[1]));
+    stage(0);
+    stager.join();
+  }
+  TRY(dma(0));
+  if (pageable && chunks > 1) stage(1);
   for (uint64_t i = 0; i < chunks; ++i) {
-    if (i + 1 < chunks) TRY(copy(i + 1));
+    if (i + 1 < chunks) {
+      stager.join();
+      TRY(dma(i + 1));
+    }
+    if (pageable && i + 2 < chunks) {  // pin[i & 1] is free once chunk i's DMA is done
+      CU(cudaEventSynchronize(c->ev_copied[i & 1]));
+      stage(i + 2);
+    }
     const uint64_t lo = i * kStreamChunk, own_i = std::min<uint64_t>(kStreamChunk, own - lo);
     const uint64_t rd = std::min<uint64_t>(own_i + halo, n - lo);
     CU(cudaStreamWaitEvent(c->stream, c->ev_copied[i & 1], 0));
