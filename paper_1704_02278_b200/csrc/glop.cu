@@ -1334,7 +1334,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   // pfac8 level 1 (outputs only at depth >= 8): bit d-1 of the bucket of the
   // 4-gram at offset d (1..4) of every 8-byte root path
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
-  std::vector<unsigned long long> grams8, grams8x;  // (p8_key<X> << 2 | d-1) of every 8-byte root path
+  std::vector<unsigned long long> grams8;  // ((prev top byte, cur) << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
   bool bits8 = false, bloom2 = false, two8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
@@ -1381,10 +1381,9 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       keys.push_back({key, s});
       if (p8)
         for (uint32_t d = 1; d <= 4; ++d) {
-          // (prev, cur) of the gram; the key scheme is picked below, by gram count
-          const uint32_t prev = (uint32_t)(key >> (8 * (d - 1))) << 24, cur = (uint32_t)(key >> (8 * d));
-          grams8.push_back((unsigned long long)p8_key<true>(prev, cur) << 2 | (d - 1));
-          grams8x.push_back((unsigned long long)p8_key<false>(prev, cur) << 2 | (d - 1));
+          // (prev's top byte, cur) of the gram at offset d: 40 bits, << 2 | d - 1
+          const uint32_t prev_top = (uint32_t)(key >> (8 * (d - 1))) & 0xFFu, cur = (uint32_t)(key >> (8 * d));
+          grams8.push_back(((unsigned long long)prev_top << 32 | cur) << 2 | (d - 1));
         }
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
@@ -1396,19 +1395,18 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       bits8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8BitsGrams);
       const char* env2 = getenv("GLOP_P8_BITS2_MIN");  // experiments: override the two-bit threshold
       two8 = bits8 && grams8.size() > (env2 ? (size_t)atoll(env2) : (size_t)kP8Bits2Grams);
-      if (!two8) grams8.swap(grams8x);  // the multiplicative key scheme
       for (unsigned long long x : grams8) {
-        const uint32_t g = (uint32_t)(x >> 2), bit = 1u << (x & 3);
+        const uint32_t cur = (uint32_t)(x >> 2), prev = (uint32_t)(x >> 34) << 24, bit = 1u << (x & 3);
         if (bits8) {  // little-endian bits of the u32 words
-          const uint32_t w = two8 ? p8_word_off<true>(g) : p8_word_off<false>(g);
-          const uint32_t b1 = (two8 ? p8_bit1<true>(g) : p8_bit1<false>(g)) & 31u;
+          const uint32_t w = p8_word_off(prev, cur);
+          const uint32_t b1 = p8_bit1(cur) & 31u;
           dmask8[w + (b1 >> 3)] |= (uint8_t)(1u << (b1 & 7));
           if (two8) {  // second bit in the same 32-bit word
-            const uint32_t b2 = p8_bit2(g) & 31u;
+            const uint32_t b2 = p8_bit2(cur) & 31u;
             dmask8[w + (b2 >> 3)] |= (uint8_t)(1u << (b2 & 7));
           }
         } else {
-          dmask8[p8_byte_off(g)] |= (uint8_t)bit;
+          dmask8[p8_byte_off(prev, cur)] |= (uint8_t)bit;
         }
       }
     }

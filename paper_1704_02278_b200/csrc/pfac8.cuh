@@ -114,22 +114,19 @@ constexpr uint32_t kP8Bloom2Keys = 3000;
 // aligned word `cur` and the top byte of the previous word -- which for a
 // match at c = 4i - d (d = 1..4) are pattern bytes [d-1, d+4).  Five bytes
 // instead of four cut the candidate words by ~40% on the syslog vocabulary
-// set.  Two key schemes (kX):
-//  * false: key = cur * K ^ (prev's top byte); table word = key's top 14
-//    bits, bit = the next 5 (IMAD, LOP3, SHF, LOP3, LDS, SHF, SHF);
-//  * true (the two-bit layout, >= kP8Bits2Grams grams): key = cur ^ (prev's
-//    top byte); table word = the high half of key * K masked to a word offset
-//    (IMAD.HI + LOP3: no shift), bits = key & 31 and (key >> 8) & 31 (the
-//    funnel shift takes its amount straight from the key).  Two instructions
-//    fewer per probe (DPI 1.87 -> 1.81 ms, syslog k=10,000 3.04 -> 2.86 ms),
-//    but the XOR-merged key collides on text structure: small gram sets see
-//    more false candidates (k=10: 1.62 -> 1.76 ms), so only the large ones
-//    use it.
+// set.
+//  * bit layouts: the table word is the high half of cur * K (IMAD.HI, a
+//    well-mixed hash of the 4 bytes) XORed with the previous word's top byte
+//    at bits 8..15 (one PRMT) and masked to a word offset -- one LOP3 does
+//    both -- and the bit inside it is cur & 31 (byte 4i; the funnel shift
+//    takes its amount straight from `cur`), the second bit of the two-bit
+//    layout (cur >> 8) & 31 (byte 4i+1): IMAD.HI, PRMT, LOP3, LDS, SHF per
+//    probe against IMAD, LOP3, SHF, LOP3, LDS, SHF, SHF with the top bits of
+//    one multiplicative hash, at the same or fewer false candidates
+//    (host-simulated on the bench sets: k=1,000 4.04% vs 4.10% of words, k=10,000
+//    9.7% vs 9.8%, DPI two-bit 4.3% vs 4.5%);
+//  * byte layout (small gram sets): byte (cur * K ^ prev's top byte) >> 16.
 constexpr uint32_t kP8HashMul = 0x9E3779B1u;
-template <bool kX>
-__host__ __device__ __forceinline__ uint32_t p8_key(uint32_t prev, uint32_t cur) {
-  return kX ? cur ^ (prev & 0xFF000000u) : (cur * kP8HashMul) ^ (prev & 0xFF000000u);
-}
 __host__ __device__ __forceinline__ uint32_t p8_mulhi(uint32_t x) {
 #ifdef __CUDA_ARCH__
   return __umulhi(x, kP8HashMul);
@@ -137,32 +134,35 @@ __host__ __device__ __forceinline__ uint32_t p8_mulhi(uint32_t x) {
   return (uint32_t)(((unsigned long long)x * kP8HashMul) >> 32);
 #endif
 }
-// byte offset of the key's 32-bit word in the 64 KB bit table (kBits)
-template <bool kX>
-__host__ __device__ __forceinline__ uint32_t p8_word_off(uint32_t key) {
-  return kX ? p8_mulhi(key) & (kP8DmaskBytes - 4) : (key >> (32 - kP8DmaskLog2)) & (kP8DmaskBytes - 4);
+// byte offset of the (prev, cur) gram's 32-bit word in the 64 KB bit table
+__host__ __device__ __forceinline__ uint32_t p8_word_off(uint32_t prev, uint32_t cur) {
+#ifdef __CUDA_ARCH__
+  const uint32_t pb = __byte_perm(prev, 0u, 0x4434);  // prev's top byte at bits 8..15
+#else
+  const uint32_t pb = (prev >> 16) & 0xFF00u;
+#endif
+  return (p8_mulhi(cur) ^ pb) & (kP8DmaskBytes - 4);
 }
-// funnel-shift amounts (low 5 bits) of the key's bit(s) inside that word
-template <bool kX>
-__host__ __device__ __forceinline__ uint32_t p8_bit1(uint32_t key) {
-  return kX ? key : key >> (32 - kP8DmaskLog2 - 3);
+// funnel-shift amounts (low 5 bits used) of the gram's bit(s) in that word
+__host__ __device__ __forceinline__ uint32_t p8_bit1(uint32_t cur) { return cur; }
+__host__ __device__ __forceinline__ uint32_t p8_bit2(uint32_t cur) { return cur >> 8; }
+// the gram's byte in the 64 KB d-mask table (byte layout)
+__host__ __device__ __forceinline__ uint32_t p8_byte_off(uint32_t prev, uint32_t cur) {
+  return ((cur * kP8HashMul) ^ (prev & 0xFF000000u)) >> (32 - kP8DmaskLog2);
 }
-__host__ __device__ __forceinline__ uint32_t p8_bit2(uint32_t key) { return key >> 8; }
-// the key's byte in the 64 KB d-mask table (!kBits)
-__host__ __device__ __forceinline__ uint32_t p8_byte_off(uint32_t key) { return key >> (32 - kP8DmaskLog2); }
 // Above kP8Bits2Grams grams (DPI: ~39K) one bit per gram passes ~7% of the
 // words on false positives alone; the "two bits in one word" layout (a
-// blocked Bloom filter: bits p8_bit1 and p8_bit2 of the word) passes ~1% for
-// two more instructions and no extra shared-memory wavefront per probe.
+// blocked Bloom filter: bits p8_bit1 and p8_bit2 of the word) passes ~1%
+// for two more instructions and no extra shared-memory wavefront per probe.
 constexpr uint32_t kP8Bits2Grams = 12000;
 template <bool kBits, bool kTwo = false>
-__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t key) {
+__device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t prev, uint32_t cur) {
   if (kBits) {  // bit p8_bit1 of the word, in bit 0 (bits 1..31: don't care)
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_word_off<kTwo>(key));
-    if (kTwo) return __funnelshift_r(w, w, p8_bit1<kTwo>(key)) & __funnelshift_r(w, w, p8_bit2(key));
-    return __funnelshift_r(w, w, p8_bit1<kTwo>(key));
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_word_off(prev, cur));
+    if (kTwo) return __funnelshift_r(w, w, p8_bit1(cur)) & __funnelshift_r(w, w, p8_bit2(cur));
+    return __funnelshift_r(w, w, p8_bit1(cur));
   }
-  return dm[p8_byte_off(key)];
+  return dm[p8_byte_off(prev, cur)];
 }
 
 // 1-D TMA bulk copy of aligned text A[lo, lo + kP8Stage) (clipped to the
@@ -366,14 +366,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (lane == 31) nb = wn;
         uint32_t* a = mm4[2 * hf];
         uint32_t* b = mm4[2 * hf + 1];
-        a[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.x, va.y));
-        a[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.y, va.z));
-        a[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.z, va.w));
-        a[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(va.w, na));
-        b[0] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.x, vb.y));
-        b[1] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.y, vb.z));
-        b[2] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.z, vb.w));
-        b[3] = p8_dmask<kBits, kTwo>(s_dmask, p8_key<kTwo>(vb.w, nb));
+        a[0] = p8_dmask<kBits, kTwo>(s_dmask, va.x, va.y);
+        a[1] = p8_dmask<kBits, kTwo>(s_dmask, va.y, va.z);
+        a[2] = p8_dmask<kBits, kTwo>(s_dmask, va.z, va.w);
+        a[3] = p8_dmask<kBits, kTwo>(s_dmask, va.w, na);
+        b[0] = p8_dmask<kBits, kTwo>(s_dmask, vb.x, vb.y);
+        b[1] = p8_dmask<kBits, kTwo>(s_dmask, vb.y, vb.z);
+        b[2] = p8_dmask<kBits, kTwo>(s_dmask, vb.z, vb.w);
+        b[3] = p8_dmask<kBits, kTwo>(s_dmask, vb.w, nb);
         if (kBits) {  // byte j = probe j's bit 0
           mq[2 * hf] = __byte_perm(__byte_perm(a[0], a[1], 0x40), __byte_perm(a[2], a[3], 0x40), 0x5410) & 0x01010101u;
           mq[2 * hf + 1] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410) & 0x01010101u;
