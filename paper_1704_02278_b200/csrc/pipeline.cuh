@@ -54,6 +54,29 @@ __global__ void __launch_bounds__(1024) p8_prefix_kernel(const unsigned long lon
   if (tid == 1023) *total = part[1023];
 }
 
+// 8 bytes at any alignment from two aligned loads (the caller keeps p + 15
+// inside the allocation).
+__device__ __forceinline__ unsigned long long load8_any(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const unsigned long long* q = reinterpret_cast<const unsigned long long*>(a & ~uintptr_t(7));
+  const uint32_t sh = (uint32_t)(a & 7) * 8;
+  const unsigned long long lo = __ldg(q);
+  return sh ? (lo >> sh) | (__ldg(q + 1) << (64 - sh)) : lo;
+}
+
+// text[0, len) == pat[0, len): 8 bytes per step while both reads stay
+// inside their buffers (text: [.., t_end); pattern bytes are padded to 16).
+__device__ __forceinline__ bool suffix_equal(const uint8_t* t, const uint8_t* t_end, const uint8_t* pat,
+                                             unsigned long long len) {
+  while (len >= 8 && t + 16 <= t_end) {
+    if (load8_any(t) != load8_any(pat)) return false;
+    t += 8, pat += 8, len -= 8;
+  }
+  for (unsigned long long k = 0; k < len; ++k)
+    if (t[k] != pat[k]) return false;
+  return true;
+}
+
 // Stage 2 of verify_hits for hits staged per region: keep[g * region + i]
 // and the kept count of region g.  Flag 1 of *vflags: a hit past the end of
 // the text or naming an unknown pattern (the reference's logic_error /
@@ -82,13 +105,8 @@ __global__ void __launch_bounds__(256) p8_keep_kernel(const DevRules r, const ui
         if (plen <= r.prefix_len) {
           ok = 1;
         } else if (x.offset + plen <= base + n) {
-          ok = 1;
           const uint8_t* t = text + (x.offset - base);
-          for (unsigned long long k = x.len; k < plen; ++k)
-            if (t[k] != r.bytes[pb + k]) {
-              ok = 0;
-              break;
-            }
+          ok = suffix_equal(t + x.len, text + n, r.bytes + pb + x.len, plen - x.len);
         }
       }
       kp[i] = (uint8_t)ok;
@@ -121,6 +139,7 @@ __global__ void __launch_bounds__(1024) p8_emit_kernel(const DevRules r, unsigne
                                                        uint32_t hist_bins, unsigned long long* vflags) {
   extern __shared__ uint32_t hist[];
   __shared__ uint32_t warp_base[32];
+  __shared__ uint32_t chunk_total;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (uint32_t i = tid; i < hist_bins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -144,18 +163,23 @@ __global__ void __launch_bounds__(1024) p8_emit_kernel(const DevRules r, unsigne
         }
       }
       unsigned long long dst = dst0 + i;
-      if (kStage2) {
+      if (kStage2) {  // stable compaction of this chunk: warp counts, one warp scans them
         const uint32_t bal = __ballot_sync(0xffffffffu, ok);
         if (lane == 0) warp_base[w] = __popc(bal);
         __syncthreads();
-        uint32_t before = 0, all = 0;
-        for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
-          const uint32_t v = warp_base[k];
-          before += k < w ? v : 0;
-          all += v;
+        if (w == 0) {
+          const uint32_t v = lane < blockDim.x / 32 ? warp_base[lane] : 0u;
+          uint32_t incl = v;
+          for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          warp_base[lane] = incl - v;
+          if (lane == 31) chunk_total = incl;
         }
-        dst = dst0 + before + __popc(bal & ((1u << lane) - 1));
-        dst0 += all;
+        __syncthreads();
+        dst = dst0 + warp_base[w] + __popc(bal & ((1u << lane) - 1));
+        dst0 += chunk_total;
         __syncthreads();
       }
       if (ok) {

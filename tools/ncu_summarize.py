@@ -104,7 +104,7 @@ def main():
                   "| kernel | launches | mean µs | share of listed time |", "|---|---|---|---|"]
         la = launches(tag)
         # drop the one-off corpus generator from the share (not part of a step)
-        step = {k: v for k, v in la.items() if "gen_syslog" not in k}
+        step = {k: v for k, v in la.items() if "gen_syslog" not in k and "gen_payload" not in k}
         tot = sum(sum(v) for v in step.values()) or 1
         for k, v in sorted(la.items(), key=lambda kv: -sum(kv[1])):
             share = f"{100 * sum(v) / tot:.1f}%" if k in step else "setup (untimed)"
