@@ -1330,7 +1330,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   const uint32_t stride = lmin ? std::min<uint32_t>(lmin - q + 1, 8) : 1;
   const uint32_t J = lmin ? std::min<uint32_t>(lmin, 8) : 1;
   std::vector<uint8_t> dmask(kDmaskBytes, 0);
-  std::vector<uint32_t> bm2(kBm2Bits / 32, 0);
+  std::vector<uint32_t> bm2(kBm2Bits / 32, 0), bm28((1u << kP8Bm2Log2) / 32, 0);
   // pfac8 level 1 (outputs only at depth >= 8): bit d-1 of the bucket of the
   // 4-gram at offset d (1..4) of every 8-byte root path
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
@@ -1387,6 +1387,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         }
       const uint32_t bit = prefix_bit(key);
       bm2[bit >> 5] |= 1u << (bit & 31);
+      const uint32_t bit8 = prefix_hash32((uint32_t)key, (uint32_t)(key >> 32)) >> (32 - kP8Bm2Log2);
+      bm28[bit8 >> 5] |= 1u << (bit8 & 31);
     });
     if (p8) {
       std::sort(grams8.begin(), grams8.end());
@@ -1417,6 +1419,9 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
         for (const auto& kv : keys) {
           const uint32_t bit = prefix_bit2(kv.first);
           bm2[bit >> 5] |= 1u << (bit & 31);
+          const uint32_t bit8 =
+              prefix_hash2(prefix_hash32((uint32_t)kv.first, (uint32_t)(kv.first >> 32))) >> (32 - kP8Bm2Log2);
+          bm28[bit8 >> 5] |= 1u << (bit8 & 31);
         }
     }
     while ((1ull << cap_log2) < 2 * keys.size()) ++cap_log2;
@@ -1438,7 +1443,8 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   const size_t o_plen = o_pid + up16(std::max<size_t>(pid2.size(), 1) * 4);
   const size_t o_dmask = o_plen + up16(pid_len.size() * 4);
   const size_t o_bm2 = o_dmask + kDmaskBytes;
-  const size_t o_dmask8 = o_bm2 + kBm2Bytes;
+  const size_t o_bm28 = o_bm2 + kBm2Bytes;
+  const size_t o_dmask8 = o_bm28 + kP8Bm2Bytes;
   const size_t o_jump = o_dmask8 + kP8DmaskBytes;
   const size_t total = o_jump + jump_bytes;
   std::vector<uint8_t> host(total, 0);
@@ -1449,6 +1455,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   memcpy(&host[o_plen], pid_len.data(), pid_len.size() * 4);
   memcpy(&host[o_dmask], dmask.data(), kDmaskBytes);
   memcpy(&host[o_bm2], bm2.data(), kBm2Bytes);
+  memcpy(&host[o_bm28], bm28.data(), kP8Bm2Bytes);
   memcpy(&host[o_dmask8], dmask8.data(), kP8DmaskBytes);
   memcpy(&host[o_jump], jump.data(), jump_bytes);
   Dev g(c->device);
@@ -1470,6 +1477,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.pid_len = reinterpret_cast<const uint32_t*>(m + o_plen);
   t->view.dmask = m + o_dmask;
   t->view.bm2 = reinterpret_cast<const uint32_t*>(m + o_bm2);
+  t->view.bm2_8 = reinterpret_cast<const uint32_t*>(m + o_bm28);
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;

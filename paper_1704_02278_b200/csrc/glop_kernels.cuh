@@ -40,6 +40,7 @@ struct DevTrie {
   const uint32_t* pid_len;  // pattern id -> matched_len
   const uint8_t* dmask;     // kDmaskBytes
   const uint32_t* bm2;      // kBm2Bits / 32 words
+  const uint32_t* bm2_8;    // pfac8's level-2 bitmap (kP8Bm2Log2 bits, see pfac8.cuh)
   const JumpEntry* jump;    // open-addressed J-byte jump table
   const uint8_t* dmask8;    // pfac8 level-1 d-masks (lmin >= 8), 2^15 bytes
   uint32_t Q, C, lmin, lmax, q, stride;

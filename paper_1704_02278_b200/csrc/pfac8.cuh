@@ -57,6 +57,14 @@ constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 #endif
 constexpr uint32_t kP8DmaskLog2 = GLOP_P8_DMASK_LOG2;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
+// level-2 prefix bitmap of the pfac8 kernel (shared memory): 2^18 bits by
+// default; a 2^17-bit map frees 16 KB of shared memory (for more warps) at the
+// cost of twice the level-2 false positives (each one an L2 jump-table probe)
+#ifndef GLOP_P8_BM2_LOG2
+#define GLOP_P8_BM2_LOG2 18
+#endif
+constexpr uint32_t kP8Bm2Log2 = GLOP_P8_BM2_LOG2;
+constexpr uint32_t kP8Bm2Bytes = (1u << kP8Bm2Log2) / 8;
 
 struct P8Layout {
   uint32_t bufs, bars, queue, hits, nh, dmask, bm2, cls, total;
@@ -71,7 +79,7 @@ __host__ __device__ inline P8Layout make_p8_layout() {
   L.hits = o; o += kP8Warps * kP8Hits * 8;
   L.nh = o; o += kP8Warps * 4;
   L.dmask = align16(o); o = L.dmask + kP8DmaskBytes;
-  L.bm2 = o; o += kBm2Bytes;
+  L.bm2 = o; o += kP8Bm2Bytes;
   L.cls = o; o += 256;
   L.total = o;
   return L;
@@ -250,9 +258,9 @@ __global__ void __launch_bounds__(kP8Threads, 1)
     const uint4* s = reinterpret_cast<const uint4*>(p.dmask8);
     uint4* d = reinterpret_cast<uint4*>(smem + L.dmask);
     for (uint32_t i = tid; i < kP8DmaskBytes / 16; i += kP8Threads) d[i] = s[i];
-    s = reinterpret_cast<const uint4*>(tr.bm2);
+    s = reinterpret_cast<const uint4*>(tr.bm2_8);
     d = reinterpret_cast<uint4*>(smem + L.bm2);
-    for (uint32_t i = tid; i < kBm2Bytes / 16; i += kP8Threads) d[i] = s[i];
+    for (uint32_t i = tid; i < kP8Bm2Bytes / 16; i += kP8Threads) d[i] = s[i];
     if (kWalk && tid < 16) reinterpret_cast<uint4*>(smem + L.cls)[tid] = reinterpret_cast<const uint4*>(tr.cls)[tid];
     if (lane < 2) mbar_init(&bars[lane], 1);
     if (lane == 0) *s_nh = 0;
@@ -447,16 +455,16 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           uint32_t word = x;
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.shared.b32 %0, [%1];\n}"
                        : "+r"(word)
-                       : "r"(bm2_a + ((x >> (32 - kBm2Log2 + 5)) << 2)), "r"(mm & (1u << (d - 1))));
+                       : "r"(bm2_a + ((x >> (32 - kP8Bm2Log2 + 5)) << 2)), "r"(mm & (1u << (d - 1))));
           // rotate bit (x >> 14) & 31 of the bitmap word to position d - 1
-          surv |= __funnelshift_r(word, word, (x >> (32 - kBm2Log2)) + (33 - d)) & (1u << (d - 1));
+          surv |= __funnelshift_r(word, word, (x >> (32 - kP8Bm2Log2)) + (33 - d)) & (1u << (d - 1));
           if (kB2) {  // second, independent 18-bit slice of the same key hash
             const uint32_t x2 = prefix_hash2(x);
             uint32_t word2 = x2;
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.shared.b32 %0, [%1];\n}"
                          : "+r"(word2)
-                         : "r"(bm2_a + ((x2 >> (32 - kBm2Log2 + 5)) << 2)), "r"(surv & (1u << (d - 1))));
-            surv &= ~(1u << (d - 1)) | __funnelshift_r(word2, word2, (x2 >> (32 - kBm2Log2)) + (33 - d));
+                         : "r"(bm2_a + ((x2 >> (32 - kP8Bm2Log2 + 5)) << 2)), "r"(surv & (1u << (d - 1))));
+            surv &= ~(1u << (d - 1)) | __funnelshift_r(word2, word2, (x2 >> (32 - kP8Bm2Log2)) + (33 - d));
           }
         }
         surv &= mm;
