@@ -163,6 +163,29 @@ int ref_kmp_search(const uint8_t* text, uint64_t n, const uint8_t* p, uint32_t m
 
 unsigned ref_default_workers(void) { return default_workers(); }
 
+// chunked_ac_scan (scan.hpp:207-243) over build_ac_automaton(rules): sorted
+// (offset, pattern_id) matches as 16-byte records (offset, id, 0).
+int ref_chunked_ac_scan(const uint8_t* text, uint64_t n, const uint8_t* bytes, const uint64_t* off, uint32_t k,
+                        uint64_t chunk_size, uint64_t overlap, unsigned workers, ref_hit** out, uint64_t* n_out) {
+  try {
+    RuleSet r = rules_of(bytes, off, k);
+    Automaton ac = build_ac_automaton(r);
+    ScanConfig sc;
+    sc.workers = workers;
+    sc.chunk_size = chunk_size;
+    sc.overlap = overlap;
+    auto ms = chunked_ac_scan(std::string_view((const char*)text, n), ac, sc);
+    *out = (ref_hit*)malloc(sizeof(ref_hit) * (ms.size() + 1));
+    for (size_t i = 0; i < ms.size(); ++i) (*out)[i] = {ms[i].offset, ms[i].pattern_id, 0};
+    *n_out = ms.size();
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (...) {
+    return 4;
+  }
+}
+
 // ---- synthetic workloads for the reference arm, so it never maps the
 // product library (the same header-only generators libglop exports).
 int ref_gen_syslog(uint8_t* out, uint64_t begin, uint64_t n, uint64_t seed, unsigned threads) {

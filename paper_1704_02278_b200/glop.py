@@ -105,6 +105,7 @@ _sig("glop_run_pfac_pipeline_device", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.
 _sig("glop_run_pfac_pipeline_device_async", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64, vp,
      C.c_uint64, vp, vp)
 _sig("glop_pipeline_ticket_result", vp, u64p, u64p)
+_sig("glop_chunked_ac_scan", vp, vp, vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(vp), u64p)
 TICKET_BYTES = 8 * 8 + 3 * 8 + 2 * 4  # glop_pipeline_ticket
 
 
@@ -406,6 +407,16 @@ class Context:
         _check(_lib.glop_run_pfac_pipeline_device_async(self.h, trie.h, rules.h, d_text, n, n if own is None else own,
                                                         base, d_hits, hit_cap, d_alerts, alert_cap, d_counts, ticket),
                "run_pfac_pipeline_device_async")
+
+    def chunked_ac_scan(self, ac_trie: DeviceTrie, text, chunk_size: int, overlap: int) -> np.ndarray:
+        """chunked_ac_scan (scan.hpp:207-243): `ac_trie` is the goto trie of the
+        full patterns (build_failureless_trie(patterns, max_len)); sorted
+        (offset, pattern_id, matched_len) records of the owned, reached matches."""
+        t = _u8(text)
+        p, n = vp(), C.c_uint64()
+        _check(_lib.glop_chunked_ac_scan(self.h, ac_trie.h, _ptr(t), t.size, 0, chunk_size, overlap, C.byref(p),
+                                         C.byref(n)), "chunked_ac_scan")
+        return _take(p, n.value, HIT_DTYPE)
 
     @property
     def fallbacks(self) -> int:

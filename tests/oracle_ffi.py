@@ -351,3 +351,21 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
+
+
+def ref_chunked_ac_scan(text, patterns, chunk_size, overlap, workers=0):
+    """The reference's chunked_ac_scan (scan.hpp:207-243) over
+    build_ac_automaton(patterns): HIT_DTYPE records (offset, pattern_id, 0)."""
+    r = ref()
+    if not getattr(r, "_ac_sig", False):
+        r.ref_chunked_ac_scan.argtypes = [u8p, C.c_uint64, u8p, u64p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint,
+                                          C.POINTER(C.c_void_p), u64p]
+        r._ac_sig = True
+    t, n = _text_arr(text)
+    pat, off = pack_patterns(patterns)
+    p, nm = C.c_void_p(), C.c_uint64()
+    rc = r.ref_chunked_ac_scan(t.ctypes.data_as(u8p), n, pat.ctypes.data_as(u8p), off.ctypes.data_as(u64p),
+                               len(patterns), chunk_size, overlap, workers, C.byref(p), C.byref(nm))
+    if rc:
+        raise OracleError(rc)
+    return _take(p, nm.value, HIT_DTYPE, r.ref_free)

@@ -203,3 +203,23 @@ def test_async_pipeline_tickets(ctx, torch_cuda):
         assert (nh, na) == (len(h), len(a)) and nh > 0
     finally:
         ctx.host_free(tickets)
+
+
+@pytest.mark.parametrize("chunk,overlap", [(0, 0), (1 << 16, None), (4096, 3), (997, 0), (64, 20), (1 << 20, 1)])
+def test_chunked_ac_vs_reference(ctx, chunk, overlap):
+    """glop_chunked_ac_scan against the reference's chunked_ac_scan
+    (scan.hpp:207-243, oracle/_ref) on 8 MB of syslog with patterns of 3..24
+    bytes: lossless overlaps (max_len - 1, None here) and lossy ones (the
+    reference loses the matches its chunk cannot reach; so must we)."""
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(chunk + 7)
+    text = glop.gen_syslog_host(8 << 20, seed=17)
+    pats = list(dict.fromkeys(text[o:o + int(rng.integers(3, 25))].tobytes() for o in rng.integers(0, text.size - 32, 300)))
+    max_len = max(len(p) for p in pats)
+    ov = max_len - 1 if overlap is None else overlap
+    ac = ctx.upload(glop.build_failureless_trie(pats, max_len))
+    got = ctx.chunked_ac_scan(ac, text, chunk, ov)
+    ref = O.ref_chunked_ac_scan(text, pats, chunk, ov)
+    assert len(ref) > 1000
+    assert np.array_equal(got["offset"], ref["offset"]) and np.array_equal(got["pattern_id"], ref["pattern_id"])
