@@ -20,33 +20,48 @@
 
 namespace logtrawl::detail {
 
-// The process-wide device group the drop-in API runs on -- every visible
-// GPU by default, as the reference's scans use every hardware thread
-// (scan.hpp:182-195, default_workers).  GLOP_DEVICES="0,2,3" picks devices (a
-// device may repeat: N contexts on one GPU); GLOP_DEVICE=d a single one.
-inline glop_group* group() {
-  static std::once_flag once;
-  static glop_group* g = nullptr;
-  static glop_status st = GLOP_OK;
-  static std::string err;
-  std::call_once(once, [] {
-    std::vector<int> devs;
+// The device group the drop-in API runs on -- every visible GPU by default,
+// as the reference's scans use every hardware thread (scan.hpp:182-195,
+// default_workers).  GLOP_DEVICES="0,2,3" picks devices (a device may repeat:
+// N contexts on one GPU); GLOP_DEVICE=d a single one.  Each calling thread
+// gets its own group (its own streams and scratch) on those devices, so
+// concurrent scans run concurrently, as the reference's reentrant scans do
+// (SPEC.md:163, :293); device copies of automata and rule sets are shared.
+inline const std::vector<int>& group_devices() {
+  static const std::vector<int> devs = [] {
+    std::vector<int> d;
     if (const char* list = std::getenv("GLOP_DEVICES")) {
       for (const char* c = list; *c;) {
         char* end = nullptr;
-        const long d = std::strtol(c, &end, 10);
+        const long v = std::strtol(c, &end, 10);
         if (end == c) break;
-        devs.push_back(static_cast<int>(d));
+        d.push_back(static_cast<int>(v));
         c = *end == ',' ? end + 1 : end;
       }
     } else if (const char* one = std::getenv("GLOP_DEVICE")) {
-      devs.push_back(std::atoi(one));
+      d.push_back(std::atoi(one));
     }
+    return d;
+  }();
+  return devs;
+}
+
+struct GroupHolder {
+  glop_group* g = nullptr;
+  glop_status st = GLOP_OK;
+  std::string err;
+  GroupHolder() {
+    const std::vector<int>& devs = group_devices();
     st = glop_group_create(devs.empty() ? nullptr : devs.data(), static_cast<int>(devs.size()), &g);
     if (st != GLOP_OK) err = glop_last_error();
-  });
-  if (st != GLOP_OK) throw std::runtime_error("glop: no usable B200 device: " + err);
-  return g;
+  }
+  ~GroupHolder() { glop_group_destroy(g); }
+};
+
+inline glop_group* group() {
+  thread_local GroupHolder h;
+  if (h.st != GLOP_OK) throw std::runtime_error("glop: no usable B200 device: " + h.err);
+  return h.g;
 }
 
 // The group's first context: single-device calls (verify_hits, chunked AC).

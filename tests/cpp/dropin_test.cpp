@@ -6,6 +6,7 @@
 #include <random>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "logtrawl/pipeline.hpp"
@@ -283,6 +284,39 @@ int main() {
     FailureTable ft = build_failure_table(longp);
     c1 = c2 = 0;
     CHECK(kmp_search(lt, longp, ft, &c1) == seq(lt, lp, ft.table, c2) && c1 == c2 && c1 > 0);
+  }
+  // concurrent callers (the reference is reentrant): threads
+  // scanning at once with one shared rule set and automaton get the results
+  // a single caller gets
+  {
+    std::mt19937 rng(99);
+    std::vector<std::string> texts(6);
+    for (auto& t : texts)
+      for (int i = 0; i < 40000; ++i) t += (rng() % 7 == 0) ? "Failed password for root\n" : "x" + std::to_string(rng()) + "\n";
+    RuleSet r = make_rules({"Failed password", "password for", "root\nx1", "x12", "x999"});
+    const Automaton shared = build_failureless_trie(truncate_prefixes(r, 8));
+    std::vector<std::vector<Match>> want;
+    std::vector<std::size_t> want_hits;
+    for (const auto& t : texts) {
+      want.push_back(brute(t, r));
+      want_hits.push_back(pfac_scan(t, shared).size());
+    }
+    std::vector<int> ok(texts.size() * 3, 0);
+    std::vector<std::thread> pool;
+    for (std::size_t w = 0; w < 3; ++w)
+      pool.emplace_back([&, w] {
+        for (std::size_t i = 0; i < texts.size(); ++i) {
+          EngineConfig cfg;
+          cfg.engine = (i + w) % 2 ? EngineKind::pfac_dense : EngineKind::pfac_compact;
+          const bool a = matches_of(run_engine_scan(texts[i], r, cfg).alerts) == want[i];
+          const bool b = pfac_scan(texts[i], shared).size() == want_hits[i];
+          ok[w * texts.size() + i] = a && b;
+        }
+      });
+    for (auto& t : pool) t.join();
+    bool all = true;
+    for (int v : ok) all = all && v;
+    CHECK(all);
   }
   std::printf("%s (%d failure%s)\n", failures ? "FAILED" : "OK", failures, failures == 1 ? "" : "s");
   return failures;
