@@ -424,6 +424,44 @@ def main():
     def results(count):
         return [glop.ticket_result(tickets + glop.TICKET_BYTES * i) for i in range(count)]
 
+    # N > 1: the exchange of step i (count all-reduce + alert gather to rank
+    # 0, NCCL) runs on its own stream while step i+1's scan runs on the
+    # library stream: alerts / counts double-buffered, one ticket each.
+    overlapped = world > 1 and kernel == glop.PFAC_AUTO
+    if overlapped:
+        comm = torch.cuda.Stream()
+        a_bufs = [d_alerts, torch.empty_like(d_alerts)]
+        c_bufs = [d_counts, torch.zeros_like(d_counts)]
+        ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_freed = [torch.cuda.Event(), torch.cuda.Event()]
+        xtickets = ctx.host_alloc(glop.TICKET_BYTES * 2)
+        xres = [None, None]
+
+        def exchange(i):
+            b = i & 1
+            ev_done[b].synchronize()  # step i's scan is done (step i+1's is running)
+            xres[b] = glop.ticket_result(xtickets + glop.TICKET_BYTES * b)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ev_done[b])
+                dist.all_reduce(c_bufs[b])
+                gather_alerts_to_root(a_bufs[b].view(-1, 16), xres[b][1], root=0)
+                ev_freed[b].record(comm)
+
+        def run_overlapped(nsteps):
+            for i in range(nsteps):
+                b = i & 1
+                stream.wait_event(ev_freed[b])  # buffer b's previous exchange has finished
+                ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), sh.read, a_bufs[b].data_ptr(), cap,
+                                                   c_bufs[b].data_ptr(), xtickets + glop.TICKET_BYTES * b,
+                                                   own=sh.own, base=sh.lo)
+                ev_done[b].record(stream)
+                if i:
+                    exchange(i - 1)
+            if nsteps:
+                exchange(nsteps - 1)
+                stream.wait_event(ev_freed[(nsteps - 1) & 1])
+            return xres[(nsteps - 1) & 1]
+
     for _ in range(max(args.warmup, 3)):
         nh, na = step()
     ctx.synchronize()
@@ -437,7 +475,9 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         kms = []
-        for i in range(args.steps):
+        if overlapped:
+            nh, na = run_overlapped(args.steps)
+        for i in range(args.steps if not overlapped else 0):
             if pipelined:
                 submit(i)
             else:
@@ -451,9 +491,13 @@ def main():
             got = results(min(args.steps, n_tickets))
             assert len(set(got)) == 1, f"steps disagree: {set(got)}"
             nh, na = got[-1]
+        if pipelined or overlapped:
             for _ in range(args.steps):  # the dominant kernel's own device time, per launch
-                step()
+                ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), sh.read, d_alerts.data_ptr(), cap,
+                                             d_counts.data_ptr(), own=sh.own, base=sh.lo)
                 kms.append(ctx.last_kernel_ms())
+            if overlapped:  # the counts of the last exchanged step, for the results block
+                d_counts.copy_(c_bufs[(args.steps - 1) & 1])
         if world == 1:
             sampler.hold(lambda: (step(), ctx.synchronize()))
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
@@ -512,6 +556,8 @@ def main():
                            for c in SUB_CONFIGS]
     if tickets:
         ctx.host_free(tickets)
+    if overlapped:
+        ctx.host_free(xtickets)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
