@@ -368,6 +368,19 @@ glop_status glop_group_run_pfac_pipeline(glop_group* group, const glop_group_tri
 glop_status glop_group_kmp_search(glop_group* group, const uint8_t* p, uint32_t m, const uint32_t* failure,
                                   const uint8_t* text, uint64_t n, uint64_t** offsets, uint64_t* n_offsets,
                                   uint64_t* comparisons);
+/* Streaming over the group: windows of `window` bytes (0 = 64 MiB) -- each
+ * reading the next window's first max(depth, max_len) - 1 bytes, carried
+ * across feed() calls -- go round-robin to the members, which scan them
+ * concurrently (one host thread, stream and PCIe link each); end() merges in
+ * window order: the results equal glop_run_pfac_pipeline[_lines] over the
+ * concatenation (lines / line_count as in glop_stream_end). */
+typedef struct glop_group_stream glop_group_stream;
+glop_status glop_group_stream_begin(glop_group* group, const glop_group_trie* trie, const glop_group_rules* rules,
+                                    int with_lines, uint64_t window, glop_group_stream** out);
+glop_status glop_group_stream_feed(glop_group_stream* stream, const uint8_t* data, uint64_t len);
+glop_status glop_group_stream_end(glop_group_stream* stream, glop_alert** alerts, uint64_t* n_alerts,
+                                  uint64_t* counts, uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count,
+                                  uint64_t* bytes);
 /* The shard plan (host only, no device): parts contiguous ranges, the first
  * n % parts one byte longer; read = min(own + halo, n - lo). */
 glop_status glop_plan_shards(uint64_t n, uint32_t parts, uint64_t halo, uint64_t* lo, uint64_t* own,

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <deque>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

@@ -350,3 +350,229 @@ glop_status glop_group_kmp_search(glop_group* g, const uint8_t* p, uint32_t m, c
 }
 
 }  // extern "C"
+
+// ---- streaming over the group: the text arrives in pieces; windows of W
+// bytes (+ the halo carried from the next window) are handed round-robin to
+// the members, each scanning its windows on its own thread, stream and PCIe
+// link; the results merge in window order at the end.
+struct glop_group_stream {
+  glop_group* g = nullptr;
+  const glop_group_trie* t = nullptr;
+  const glop_group_rules* r = nullptr;
+  bool lines = false;
+  uint64_t W = 0, halo = 0, pos = 0, fill = 0, windows = 0;
+  uint8_t* cur = nullptr;                  // the window being filled (pinned)
+  std::vector<uint8_t*> pool;              // free pinned window buffers
+  std::vector<uint8_t*> all;               // every buffer (freed at the end)
+  struct Result {
+    glop_alert* alerts = nullptr;
+    uint64_t* lines = nullptr;
+    uint64_t n_alerts = 0, stage1 = 0, line_count = 0;
+    uint64_t own = 0, read = 0;  // the window: starts owned, bytes read (own + halo)
+    std::vector<uint64_t> counts;
+    glop_status st = GLOP_OK;
+    std::string err;
+  };
+  std::vector<Result> results;             // by window index
+  struct Member {
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::pair<uint64_t, uint8_t*>> q;  // (window index, buffer)
+    bool stop = false;
+  };
+  std::vector<std::unique_ptr<Member>> members;
+  std::mutex pool_mu;
+  std::condition_variable pool_cv;
+  std::mutex res_mu;
+};
+
+namespace {
+void gs_worker(glop_group_stream* gs, int m) {
+  glop_group_stream::Member& mb = *gs->members[m];
+  for (;;) {
+    std::pair<uint64_t, uint8_t*> job;
+    {
+      std::unique_lock<std::mutex> lk(mb.mu);
+      mb.cv.wait(lk, [&] { return mb.stop || !mb.q.empty(); });
+      if (mb.q.empty()) return;
+      job = mb.q.front();
+      mb.q.pop_front();
+    }
+    const uint64_t w = job.first, lo = w * gs->W;
+    uint64_t own, rd;
+    {
+      std::lock_guard<std::mutex> lk(gs->res_mu);
+      own = gs->results[w].own;
+      rd = gs->results[w].read;
+    }
+    glop_group_stream::Result res;
+    res.own = own;
+    res.read = rd;
+    res.counts.assign(gs->r->member[m]->view.n_patterns, 0);
+    glop_status s;
+    if (gs->lines)
+      s = glop_run_pfac_pipeline_shard_lines(gs->g->ctx[m], gs->t->member[m], gs->r->member[m], job.second, rd, own,
+                                             lo, 0, &res.alerts, &res.n_alerts, res.counts.data(), &res.stage1,
+                                             &res.lines, &res.line_count);
+    else
+      s = glop_run_pfac_pipeline_shard(gs->g->ctx[m], gs->t->member[m], gs->r->member[m], job.second, rd, own, lo, 0,
+                                       &res.alerts, &res.n_alerts, res.counts.data(), &res.stage1);
+    res.st = s;
+    if (s != GLOP_OK) res.err = glop_last_error();
+    {
+      std::lock_guard<std::mutex> lk(gs->res_mu);
+      gs->results[w] = std::move(res);
+    }
+    {
+      std::lock_guard<std::mutex> lk(gs->pool_mu);
+      gs->pool.push_back(job.second);
+    }
+    gs->pool_cv.notify_one();
+  }
+}
+
+uint8_t* gs_take_buffer(glop_group_stream* gs) {
+  std::unique_lock<std::mutex> lk(gs->pool_mu);
+  gs->pool_cv.wait(lk, [&] { return !gs->pool.empty(); });
+  uint8_t* b = gs->pool.back();
+  gs->pool.pop_back();
+  return b;
+}
+
+// hands the filled window (own bytes owned, fill bytes read) to its member
+void gs_dispatch(glop_group_stream* gs, uint64_t own) {
+  const uint64_t w = gs->windows++;
+  {
+    std::lock_guard<std::mutex> lk(gs->res_mu);
+    gs->results.emplace_back();
+    gs->results[w].own = own;
+    gs->results[w].read = gs->fill;
+  }
+  glop_group_stream::Member& mb = *gs->members[w % gs->members.size()];
+  {
+    std::lock_guard<std::mutex> lk(mb.mu);
+    mb.q.emplace_back(w, gs->cur);
+  }
+  mb.cv.notify_one();
+}
+}  // namespace
+
+extern "C" {
+
+glop_status glop_group_stream_begin(glop_group* g, const glop_group_trie* t, const glop_group_rules* r,
+                                    int with_lines, uint64_t window, glop_group_stream** out) {
+  if (!g || !t || !r || !out) return gfail(GLOP_EINVAL, "glop_group_stream_begin: null argument");
+  *out = nullptr;
+  auto* gs = new glop_group_stream();
+  gs->g = g;
+  gs->t = t;
+  gs->r = r;
+  gs->lines = with_lines != 0;
+  gs->halo = std::max<uint64_t>(std::max<uint64_t>(t->max_depth, r->max_len), 1) - 1;
+  gs->W = std::max<uint64_t>(window ? window : (64ull << 20), gs->halo + 1);
+  const size_t nb = 2 * g->ctx.size() + 1;  // two in flight per member + the one being filled
+  for (size_t i = 0; i < nb; ++i) {
+    void* b = nullptr;
+    if (cudaMallocHost(&b, gs->W + gs->halo + 64) != cudaSuccess) {
+      cudaGetLastError();
+      for (uint8_t* x : gs->all) cudaFreeHost(x);
+      delete gs;
+      return gfail(GLOP_ENOMEM, "glop_group_stream_begin: pinned window buffers");
+    }
+    gs->all.push_back(static_cast<uint8_t*>(b));
+  }
+  gs->pool.assign(gs->all.begin() + 1, gs->all.end());
+  gs->cur = gs->all[0];
+  for (size_t m = 0; m < g->ctx.size(); ++m) gs->members.push_back(std::make_unique<glop_group_stream::Member>());
+  for (size_t m = 0; m < g->ctx.size(); ++m) gs->members[m]->th = std::thread(gs_worker, gs, (int)m);
+  *out = gs;
+  return GLOP_OK;
+}
+
+glop_status glop_group_stream_feed(glop_group_stream* gs, const uint8_t* data, uint64_t len) {
+  if (!gs || (len && !data)) return gfail(GLOP_EINVAL, "glop_group_stream_feed: null argument");
+  const uint64_t full = gs->W + gs->halo;
+  while (len) {
+    const uint64_t take = std::min<uint64_t>(len, full - gs->fill);
+    parallel_memcpy(gs->cur + gs->fill, data, take);
+    gs->fill += take;
+    data += take;
+    len -= take;
+    if (gs->fill == full) {  // window [pos, pos + W) and its halo: hand it over, carry the halo
+      uint8_t* next = gs_take_buffer(gs);
+      memcpy(next, gs->cur + gs->W, gs->halo);
+      gs_dispatch(gs, gs->W);
+      gs->cur = next;
+      gs->fill = gs->halo;
+      gs->pos += gs->W;
+    }
+  }
+  return GLOP_OK;
+}
+
+glop_status glop_group_stream_end(glop_group_stream* gs, glop_alert** alerts, uint64_t* n_alerts, uint64_t* counts,
+                                  uint64_t* stage1_hits, uint64_t** lines, uint64_t* line_count, uint64_t* bytes) {
+  if (!gs) return gfail(GLOP_EINVAL, "glop_group_stream_end: null stream");
+  const uint64_t total_bytes = gs->pos + gs->fill;
+  if (gs->fill || gs->windows == 0) gs_dispatch(gs, gs->fill);  // the tail owns every remaining start
+  for (auto& mb : gs->members) {
+    {
+      std::lock_guard<std::mutex> lk(mb->mu);
+      mb->stop = true;
+    }
+    mb->cv.notify_one();
+  }
+  for (auto& mb : gs->members) mb->th.join();
+  glop_status s = GLOP_OK;
+  std::string err;
+  for (auto& res : gs->results)
+    if (res.st != GLOP_OK && s == GLOP_OK) s = res.st, err = res.err;
+  if (s == GLOP_OK && (!alerts || !n_alerts)) s = GLOP_EINVAL, err = "glop_group_stream_end: null argument";
+  if (s == GLOP_OK) {
+    std::vector<glop_alert*> pa;
+    std::vector<uint64_t> na;
+    for (auto& res : gs->results) pa.push_back(res.alerts), na.push_back(res.n_alerts);
+    s = concat(pa, na, alerts, n_alerts);
+    if (s == GLOP_OK && gs->lines && lines) {
+      std::vector<uint64_t*> pl;
+      for (auto& res : gs->results) pl.push_back(res.lines);
+      uint64_t nl = 0;
+      s = concat(pl, na, lines, &nl);
+      uint64_t before = 0, at = 0;
+      for (size_t w = 0; w < gs->results.size() && s == GLOP_OK; ++w) {
+        for (uint64_t i = 0; i < na[w]; ++i) (*lines)[at + i] += before;
+        at += na[w];
+        before += gs->results[w].line_count - 1;
+      }
+      if (line_count) *line_count = before + 1;
+    }
+    if (s == GLOP_OK) {
+      if (counts && !gs->results.empty()) {
+        const size_t k = gs->results[0].counts.size();
+        for (size_t i = 0; i < k; ++i) {
+          uint64_t x = 0;
+          for (auto& res : gs->results) x += res.counts[i];
+          counts[i] = x;
+        }
+      }
+      if (stage1_hits) {
+        uint64_t x = 0;
+        for (auto& res : gs->results) x += res.stage1;
+        *stage1_hits = x;
+      }
+      if (bytes) *bytes = total_bytes;
+    }
+  } else {
+    gfail(s, err);
+  }
+  for (auto& res : gs->results) {
+    glop_free(res.alerts);
+    glop_free(res.lines);
+  }
+  for (uint8_t* b : gs->all) cudaFreeHost(b);
+  delete gs;
+  return s;
+}
+
+}  // extern "C"

@@ -708,3 +708,35 @@ class Stream:
         alerts = _take(p, na.value, ALERT_DTYPE)
         return (alerts, cnt[:self.n_patterns], s1.value, _take(lp, na.value, np.uint64) if self.lines else None,
                 lc.value if self.lines else None, nb.value)
+
+
+_sig("glop_group_stream_begin", vp, vp, vp, C.c_int, C.c_uint64, C.POINTER(vp))
+_sig("glop_group_stream_feed", vp, vp, C.c_uint64)
+_sig("glop_group_stream_end", vp, C.POINTER(vp), u64p, u64p, u64p, C.POINTER(vp), u64p, u64p)
+
+
+class GroupStream(Stream):
+    """glop_group_stream_*: windows handed round-robin to the group's members."""
+
+    def __init__(self, group: Group, trie, rules, lines: bool = False, window: int = 0):
+        h = vp()
+        _check(_lib.glop_group_stream_begin(group.h, trie.h, rules.h, 1 if lines else 0, window, C.byref(h)),
+               "group_stream_begin")
+        self.h, self.lines, self.n_patterns = h, lines, rules.n_patterns
+        self._keep = (group, trie, rules)
+        self._feed, self._end = _lib.glop_group_stream_feed, _lib.glop_group_stream_end
+
+    def feed(self, data):
+        t = _u8(data)
+        _check(self._feed(self.h, _ptr(t), t.size), "group_stream_feed")
+
+    def end(self):
+        p, na, s1, lp, lc, nb = vp(), C.c_uint64(), C.c_uint64(), vp(), C.c_uint64(), C.c_uint64()
+        cnt = np.zeros(max(self.n_patterns, 1), dtype=np.uint64)
+        h, self.h = self.h, None
+        _check(self._end(h, C.byref(p), C.byref(na), cnt.ctypes.data_as(u64p), C.byref(s1),
+                         C.byref(lp) if self.lines else None, C.byref(lc) if self.lines else None, C.byref(nb)),
+               "group_stream_end")
+        alerts = _take(p, na.value, ALERT_DTYPE)
+        return (alerts, cnt[:self.n_patterns], s1.value, _take(lp, na.value, np.uint64) if self.lines else None,
+                lc.value if self.lines else None, nb.value)

@@ -104,3 +104,23 @@ def test_stream_empty_and_without_lines(ctx):
     alerts, counts, s1, lines, lc, nb = st.end()
     r_hits, r_alerts = reference(text, pats, with_lines=False)
     assert np.array_equal(alerts16(alerts), alerts16(r_alerts)) and s1 == len(r_hits) and nb == text.size
+
+
+@pytest.mark.parametrize("members,window", [(1, 1 << 20), (3, 1 << 16), (4, 997)])
+def test_group_stream_vs_reference(ctx, members, window):
+    """glop_group_stream_*: windows round-robin over the group's members (on
+    one GPU here), random feed pieces; the merged result equals the reference's
+    over the concatenation, lines included."""
+    rng = np.random.default_rng(members * 7 + window)
+    text = glop.gen_syslog_host(5 << 20, 31 + members)
+    pats, _ = glop.gen_rules(1000, 606)
+    pats = list(pats) + [b"Failed password for invalid user", b"session opened for user root by (uid=0)"]
+    g = glop.Group([0] * members)
+    st = glop.GroupStream(g, g.upload(glop.build_failureless_trie(pats, 8)), g.upload_rules(pats, 8), lines=True,
+                          window=window)
+    lo = 0
+    while lo < text.size:
+        step = int(rng.integers(1, 300_000))
+        st.feed(text[lo:lo + step])
+        lo += step
+    check(st.end(), text, pats)
