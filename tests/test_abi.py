@@ -100,3 +100,20 @@ def test_kmp_failure_table():  # test_kmp.cpp:29-36
     assert list(glop.kmp_failure_table(b"AAAA")) == [0, 1, 2, 3]
     for p in (b"Failed password", b"ABABCABAB", b"x"):
         assert list(glop.kmp_failure_table(p)) == list(O.kmp_failure(p))
+
+
+def test_engine_library_exports_and_fails_loudly_without_gpu():
+    """libglop_engine.so (run_engine_scan behind a C ABI): loads, exports its
+    entry points, builds a RuleSet on the host, and -- with no sm_100 device --
+    reports the failure instead of falling back to the host."""
+    import torch
+
+    eng = glop.Engine([b"Failed password", b"root"])
+    for n in ("glop_engine_rules_create", "glop_engine_rules_destroy", "glop_engine_run", "glop_engine_last_error"):
+        assert hasattr(eng.lib, n)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    text = np.frombuffer(b"x Failed password for root\n", np.uint8).copy()
+    with pytest.raises(glop.GlopError):
+        eng.run(text.ctypes.data, text.size)
+    eng.close()
