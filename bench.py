@@ -618,28 +618,28 @@ def sub_config(args, ctx, glop, stream, c, d_text, d_hits, d_alerts, cap, peak):
     for _ in range(3):
         r = step()
     ctx.synchronize()
-    pipelined = c["kind"] != "kmp"  # as the headline: PFAC steps submitted back to back, tickets checked after
-    tickets = ctx.host_alloc(glop.TICKET_BYTES * steps) if pipelined else None
+    # as the headline: steps submitted back to back, tickets checked after
+    tickets = ctx.host_alloc(glop.TICKET_BYTES * steps)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     kms = []
     for i in range(steps):
-        if pipelined:
+        if c["kind"] == "kmp":
+            ctx.kmp_search_device_async(KMP_PATTERN, d_text.data_ptr(), n, d_hits.data_ptr(), kcap,
+                                        tickets + glop.TICKET_BYTES * i)
+        else:
             ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), n, d_alerts.data_ptr(), cap,
                                                d_counts.data_ptr(), tickets + glop.TICKET_BYTES * i)
-        else:
-            r = step()
-            kms.append(ctx.last_kernel_ms())
     ev1.record(stream)
     ctx.synchronize()
     ms = ev0.elapsed_time(ev1) / steps
-    if pipelined:
-        got = {glop.ticket_result(tickets + glop.TICKET_BYTES * i) for i in range(steps)}
-        ctx.host_free(tickets)
-        assert len(got) == 1, got
-        for _ in range(steps):
-            r = step()
-            kms.append(ctx.last_kernel_ms())
+    res = glop.kmp_ticket_result if c["kind"] == "kmp" else glop.ticket_result
+    got = {res(tickets + glop.TICKET_BYTES * i) for i in range(steps)}
+    ctx.host_free(tickets)
+    assert len(got) == 1, got
+    for _ in range(steps):
+        r = step()
+        kms.append(ctx.last_kernel_ms())
     kernel_ms = statistics.mean(kms)
     gbs = n / (kernel_ms / 1e3) / 1e9
     out = {"config": c["config"], "workload": c["workload"], "bytes": n, "steps": steps, "kernel": kname,
@@ -841,16 +841,24 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
         sampler.settle(kmp_step if world == 1 else (lambda: time.sleep(0.02)))
         barrier()
         l0 = ctx.launches
+        tickets = ctx.host_alloc(glop.TICKET_BYTES * args.steps)  # steps submitted back to back
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        kms = []
-        for _ in range(args.steps):
-            nm, cmp_ = kmp_step()
-            kms.append(ctx.last_kernel_ms())
+        for i in range(args.steps):
+            ctx.kmp_search_device_async(p, d_text.data_ptr(), S, d_out.data_ptr(), cap,
+                                        tickets + glop.TICKET_BYTES * i, base=rank * S)
         ev1.record(stream)
         ctx.synchronize()
         barrier()
         launches = ctx.launches - l0
+        got = {glop.kmp_ticket_result(tickets + glop.TICKET_BYTES * i) for i in range(args.steps)}
+        ctx.host_free(tickets)
+        assert len(got) == 1, got
+        nm, cmp_ = got.pop()
+        kms = []
+        for _ in range(args.steps):  # the kernel's own device time, per launch
+            kmp_step()
+            kms.append(ctx.last_kernel_ms())
         if world == 1:
             sampler.hold(kmp_step)
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)

@@ -386,6 +386,16 @@ glop_status glop_group_stream_end(glop_group_stream* stream, glop_alert** alerts
 glop_status glop_plan_shards(uint64_t n, uint32_t parts, uint64_t halo, uint64_t* lo, uint64_t* own,
                              uint64_t* read);
 
+/* Asynchronous device KMP (pipelined submission, as
+ * glop_run_pfac_pipeline_device_async): the status lands in *ticket (pinned);
+ * after the context stream is synchronized glop_kmp_ticket_result gives the
+ * number of offsets and ADDS the comparisons, or GLOP_EAGAIN when the input
+ * needs the synchronous call (a match-dense tile or a staging overflow). */
+glop_status glop_kmp_search_device_async(glop_ctx* ctx, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                         const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                         uint64_t* d_out, uint64_t cap, glop_pipeline_ticket* ticket);
+glop_status glop_kmp_ticket_result(const glop_pipeline_ticket* ticket, uint64_t* n_offsets, uint64_t* comparisons);
+
 /* ---- memory helpers -------------------------------------------------------- */
 void glop_free(void* p);
 glop_status glop_device_alloc(glop_ctx* ctx, uint64_t bytes, void** out);

@@ -117,6 +117,7 @@ struct glop_ctx {
   DBuf lcount, lprefix, loffs;                   // device LineIndex
   DBuf hprefix, kcounts, kprefix, keep8, counts_tmp;  // fused pipeline (pipeline.cuh)
   DBuf palerts, plines;                          // alerts (+ lines) of the host-facing pipeline calls
+  std::string kmp_key;                           // pattern + failure table of the DFA in kmp_dfa
   Accum acc;                                     // streamed pipeline results
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
   void* pin[2] = {nullptr, nullptr};             // pinned staging of pageable host text
@@ -487,7 +488,7 @@ glop_status kmp_seq_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint
 glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const uint32_t* fail_tab,
                             const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
                             uint64_t* d_out, uint64_t cap, uint64_t* n_offsets,
-                            uint64_t* comparisons, uint64_t skip = 0) {
+                            uint64_t* comparisons, uint64_t skip = 0, glop_pipeline_ticket* ticket = nullptr) {
   *n_offsets = 0;
   if (own > n || skip > own) return fail(GLOP_EINVAL, "kmp_search: own > n or skip > own");
   if (m == 0 || n < m || own == skip) return GLOP_OK;  // kmp.hpp:50
@@ -507,10 +508,18 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
       return fail(GLOP_EINVAL, "kmp_search: shards need the pattern's own prefix function and m < 8192");
     return kmp_seq_impl(c, pat, m, fail_tab, d_text, n, d_out, cap, n_offsets, comparisons);
   }
-  std::vector<uint32_t> dfa;
-  build_kmp_dfa(pat, m, fail_tab, dfa);
-  TRY(c->kmp_dfa.ensure(dfa.size() * 4));
-  CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), dfa.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  // the DFA of the context's last pattern stays on the device
+  std::string key(reinterpret_cast<const char*>(pat), m);
+  key.append(reinterpret_cast<const char*>(fail_tab), (size_t)m * 4);
+  if (key != c->kmp_key) {
+    std::vector<uint32_t> dfa;
+    build_kmp_dfa(pat, m, fail_tab, dfa);
+    TRY(c->kmp_dfa.ensure(dfa.size() * 4));
+    // (stream-ordered after the kernels reading the previous DFA; a pageable
+    // source is staged before the call returns)
+    CU(cudaMemcpyAsync(c->kmp_dfa.p, dfa.data(), dfa.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    c->kmp_key.swap(key);
+  }
   const uint64_t end_lim = std::min<uint64_t>(own + m - 1, n);  // starts < own
   const uint32_t a = (uint32_t)((uintptr_t)d_text & 15);
   const uint32_t num_tiles = (uint32_t)((end_lim + a + kK3Tile - 1) / kK3Tile);
@@ -566,6 +575,15 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
         c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
         c->staging.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), cap);
     CU(cudaGetLastError());
+    if (ticket) {  // no host wait: the status block lands in the ticket
+      ticket->region = region;
+      ticket->hit_cap = cap;
+      ticket->alert_cap = 0;
+      ticket->stage2 = 3;  // (KMP ticket)
+      ticket->done = 0;
+      CU(cudaMemcpyAsync(ticket->raw, c->misc.p, sizeof ticket->raw, cudaMemcpyDeviceToHost, c->stream));
+      return GLOP_OK;
+    }
     TRY(sync_read(c, c->misc.p, 32));
     const unsigned long long total = c->h_misc[0], maxregion = c->h_misc[3];
     const unsigned flags = (unsigned)(c->h_misc[1] & 0xffffffffu);
@@ -1677,6 +1695,36 @@ glop_status glop_kmp_search_device(glop_ctx* c, const uint8_t* p, uint32_t m, co
   std::lock_guard<std::mutex> lk(c->mu);
   Dev g(c->device);
   return kmp_device_impl(c, p, m, failure, d_text, n, own, base, d_out, cap, n_offsets, comparisons);
+}
+
+glop_status glop_kmp_search_device_async(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,
+                                         const uint8_t* d_text, uint64_t n, uint64_t own, uint64_t base,
+                                         uint64_t* d_out, uint64_t cap, glop_pipeline_ticket* ticket) {
+  if (!c || !ticket || (m && (!p || !failure))) return fail(GLOP_EINVAL, "glop_kmp_search_device_async: null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  Dev g(c->device);
+  memset(ticket, 0, sizeof *ticket);
+  uint64_t no = 0, cmp = 0;
+  const glop_status s = kmp_device_impl(c, p, m, failure, d_text, n, own, base, d_out, cap, &no, &cmp, 0, ticket);
+  if (s != GLOP_OK || ticket->region == 0) {  // failed, or ran synchronously (empty, sequential walk)
+    ticket->done = s == GLOP_OK ? 1 : 2;
+    ticket->raw[0] = no;
+    ticket->raw[2] = cmp;
+    ticket->raw[7] = (uint64_t)s;
+    ticket->stage2 = 3;
+  }
+  return s;
+}
+
+glop_status glop_kmp_ticket_result(const glop_pipeline_ticket* k, uint64_t* n_offsets, uint64_t* comparisons) {
+  if (!k || !n_offsets) return fail(GLOP_EINVAL, "glop_kmp_ticket_result: null argument");
+  if (k->done == 2) return fail((glop_status)k->raw[7], "kmp_search: failed");
+  if (k->done == 0 && ((k->raw[1] & 1u) || k->raw[3] > k->region))
+    return fail(GLOP_EAGAIN, "kmp_search: this input needs the synchronous path (match-dense tile / staging overflow)");
+  *n_offsets = k->raw[0];
+  if (comparisons) *comparisons += k->raw[2];
+  if (*n_offsets > k->hit_cap && k->done == 0) return fail(GLOP_ECAPACITY, "kmp_search: output capacity");
+  return GLOP_OK;
 }
 
 glop_status glop_kmp_search(glop_ctx* c, const uint8_t* p, uint32_t m, const uint32_t* failure,

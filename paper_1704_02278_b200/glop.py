@@ -105,6 +105,17 @@ _sig("glop_run_pfac_pipeline_device", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.
 _sig("glop_run_pfac_pipeline_device_async", vp, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64, vp,
      C.c_uint64, vp, vp)
 _sig("glop_pipeline_ticket_result", vp, u64p, u64p)
+_sig("glop_kmp_search_device_async", vp, u8p, C.c_uint32, u32p, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp,
+     C.c_uint64, vp)
+_sig("glop_kmp_ticket_result", vp, u64p, u64p)
+
+
+def kmp_ticket_result(ticket_ptr: int):
+    """(n_offsets, comparisons) of an asynchronous KMP call, once its
+    context's stream is synchronized; raises Again when it must be redone."""
+    no, cmp_ = C.c_uint64(), C.c_uint64(0)
+    _check(_lib.glop_kmp_ticket_result(ticket_ptr, C.byref(no), C.byref(cmp_)), "kmp_ticket_result")
+    return no.value, cmp_.value
 _sig("glop_chunked_ac_scan", vp, vp, vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(vp), u64p)
 TICKET_BYTES = 8 * 8 + 3 * 8 + 2 * 4  # glop_pipeline_ticket
 
@@ -487,6 +498,16 @@ class Context:
                                            n if own is None else own, base, d_out, cap, C.byref(no), C.byref(cmp_)),
                "kmp_search_device")
         return no.value, cmp_.value
+
+    def kmp_search_device_async(self, pattern: bytes, d_text: int, n: int, d_out: int, cap: int, ticket: int,
+                                own: int | None = None, base: int = 0):
+        """Enqueue the device KMP without waiting (result via kmp_ticket_result)."""
+        p = _u8(pattern)
+        f = kmp_failure_table(pattern)
+        self._kmp_keep = (p, f)  # alive until the call returns (the DFA is built from them on the host)
+        _check(_lib.glop_kmp_search_device_async(self.h, p.ctypes.data_as(u8p), p.size, f.ctypes.data_as(u32p),
+                                                 d_text, n, n if own is None else own, base, d_out, cap, ticket),
+               "kmp_search_device_async")
 
     # -- memory / workloads
     def host_alloc(self, nbytes: int) -> int:

@@ -223,3 +223,37 @@ def test_chunked_ac_vs_reference(ctx, chunk, overlap):
     ref = O.ref_chunked_ac_scan(text, pats, chunk, ov)
     assert len(ref) > 1000
     assert np.array_equal(got["offset"], ref["offset"]) and np.array_equal(got["pattern_id"], ref["pattern_id"])
+
+
+def test_async_kmp_tickets(ctx, torch_cuda):
+    """glop_kmp_search_device_async: back-to-back submissions, each ticket equal
+    to the synchronous call and the oracle; a match-dense input (every
+    position of an 'A' run) reports Again and the synchronous call is exact."""
+    torch = torch_cuda
+    text = glop.gen_syslog_host(3 << 20, 5)
+    pat = b"Failed password"
+    d = torch.from_numpy(np.concatenate([text, np.zeros(64, np.uint8)])).cuda()
+    cap = 1 << 20
+    d_out = torch.empty(cap * 8, dtype=torch.uint8, device="cuda")
+    r_offs, r_cmp = O.kmp_search(text, pat)
+    tickets = ctx.host_alloc(glop.TICKET_BYTES * 3)
+    try:
+        for i in range(3):
+            ctx.kmp_search_device_async(pat, d.data_ptr(), text.size, d_out.data_ptr(), cap,
+                                        tickets + glop.TICKET_BYTES * i)
+        ctx.synchronize()
+        for i in range(3):
+            assert glop.kmp_ticket_result(tickets + glop.TICKET_BYTES * i) == (len(r_offs), r_cmp)
+        assert np.array_equal(d_out[: len(r_offs) * 8].cpu().numpy().view("<u8"), r_offs)
+        dense = np.full(1 << 20, 65, np.uint8)
+        dd = torch.from_numpy(np.concatenate([dense, np.zeros(64, np.uint8)])).cuda()
+        ctx.kmp_search_device_async(b"AA", dd.data_ptr(), dense.size, d_out.data_ptr(), cap, tickets)
+        ctx.synchronize()
+        with pytest.raises(glop.Again):
+            glop.kmp_ticket_result(tickets)
+        nm, cmp_ = ctx.kmp_search_device(b"AA", dd.data_ptr(), dense.size, d_out.data_ptr(), cap)
+        o, c = O.kmp_search(dense, b"AA")
+        assert (nm, cmp_) == (len(o), c)
+        assert np.array_equal(d_out[: nm * 8].cpu().numpy().view("<u8"), o)
+    finally:
+        ctx.host_free(tickets)
