@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <vector>
 #include <new>
@@ -106,6 +107,7 @@ struct RulesEntry {
   std::string key;
   glop_group_rules* rules = nullptr;
   glop_group_trie* trie = nullptr;  // failureless trie over truncate_prefixes(rules, prefix_len), when built
+  std::atomic<std::uint64_t> last_alerts{0};  // alerts of the last pipeline call (Alert storage is prepared ahead)
   ~RulesEntry() {
     if (trie) glop_group_trie_destroy(trie);
     if (rules) glop_group_rules_destroy(rules);

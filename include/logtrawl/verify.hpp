@@ -12,6 +12,8 @@
 #include <string_view>
 #include <vector>
 
+#include <sys/mman.h>
+
 #include "glop.h"
 #include "logtrawl/detail/abi.hpp"
 #include "logtrawl/rules.hpp"
@@ -67,11 +69,30 @@ namespace detail {
 // verify.hpp:78); the Alert carries that pattern's id and name, sorted by
 // (offset, rule_id) (verify.hpp:100-103) -- only a RuleSet whose ids are not
 // their positions changes the device's (offset, position) order.
+// n default Alerts, the storage backed by huge pages where the kernel allows
+// it (2M alerts are 128 MB: 4 KB first-touch faults were most of the cost).
+inline std::vector<Alert> alert_storage(std::size_t n) {
+  std::vector<Alert> v;
+  v.reserve(n);
+#ifdef MADV_HUGEPAGE
+  const std::uintptr_t huge = std::uintptr_t(2) << 20;
+  const std::uintptr_t lo = (reinterpret_cast<std::uintptr_t>(v.data()) + huge - 1) & ~(huge - 1);
+  const std::uintptr_t hi = reinterpret_cast<std::uintptr_t>(v.data() + n) & ~(huge - 1);
+  if (hi > lo) (void)madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+#endif
+  v.resize(n);
+  return v;
+}
+
+// glop_alert records -> Alerts (the reference's Alert values).  `storage`:
+// default Alerts prepared while the device worked (any size; resized here).
 inline std::vector<Alert> to_alerts(const glop_alert* a, std::uint64_t na, const RuleSet& rules,
-                                    const LineIndex* lines, const std::uint64_t* dev_lines) {
+                                    const LineIndex* lines, const std::uint64_t* dev_lines,
+                                    std::vector<Alert> storage = {}) {
   for (std::uint64_t i = 0; i < na; ++i)  // rules.patterns.at() (verify.hpp:78) throws before any work
     if (a[i].rule_id >= rules.patterns.size()) (void)rules.patterns.at(a[i].rule_id);
-  std::vector<Alert> out(na);
+  std::vector<Alert> out = storage.capacity() >= na ? std::move(storage) : alert_storage(na);
+  out.resize(na);
   std::atomic<bool> dense_ids{true};
   parallel_for(na, [&](std::size_t lo, std::size_t hi) {
     bool dense = true;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <memory>
@@ -32,6 +33,10 @@
 #include "logtrawl/detail/abi.hpp"
 #include "workload.hpp"
 
+namespace glop {
+// hostcopy.cpp: pageable -> pinned staging copy on a persistent host thread pool
+void parallel_memcpy(void* dst, const void* src, size_t bytes);
+}  // namespace glop
 using namespace glop;
 
 static_assert(sizeof(glop_hit) == 16, "glop_hit must match logtrawl::Hit");
@@ -120,7 +125,8 @@ struct glop_ctx {
   std::string kmp_key;                           // pattern + failure table of the DFA in kmp_dfa
   Accum acc;                                     // streamed pipeline results
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
-  void* pin[2] = {nullptr, nullptr};             // pinned staging of pageable host text
+  void* pin[3] = {nullptr, nullptr, nullptr};    // pinned staging of pageable host text (ring)
+  cudaEvent_t ev_pin[3] = {};                    // DMA out of pin[b] done
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   unsigned long long* h_misc = nullptr;  // pinned readback
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // around the last scan kernel
@@ -834,24 +840,6 @@ glop_status line_numbers_impl(glop_ctx* c, const uint8_t* d_text, uint64_t n, ui
                               uint32_t stride, uint64_t count, uint64_t* d_lines, const uint64_t* d_line_base,
                               uint64_t* d_lf_acc);
 
-// memcpy on up to 16 host threads (pageable -> pinned staging).
-void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const unsigned T = (unsigned)std::min<size_t>(std::min(hw, 16u), std::max<size_t>(1, bytes >> 22));
-  if (T <= 1) {
-    memcpy(dst, src, bytes);
-    return;
-  }
-  std::vector<std::thread> pool;
-  const size_t per = (bytes / T + 4095) & ~size_t(4095);
-  for (unsigned t = 0; t < T; ++t) {
-    const size_t lo = std::min(bytes, t * per), hi = std::min(bytes, lo + per);
-    if (lo < hi)
-      pool.emplace_back([=] { memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo); });
-  }
-  for (auto& th : pool) th.join();
-}
-
 // Grows a device buffer to `want` bytes keeping its first `keep` bytes.
 glop_status grow_keep(glop_ctx* c, DBuf& b, size_t want, size_t keep) {
   if (want <= b.bytes) return GLOP_OK;
@@ -951,68 +939,106 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   Accum& A = c->acc;  // kept across calls (buffers grow rarely)
   TRY(accum_begin(c, A, r->view.n_patterns, lines || line_count));
   // Pageable text (a std::string, a file read into memory): the driver would
-  // stage it through its own pinned buffers on one thread; instead host
-  // threads copy each chunk into one of two pinned staging buffers while the
-  // DMA of the previous chunk runs.
+  // stage it through its own pinned buffers on one thread (~11 GB/s here);
+  // instead a stager thread copies chunks into a ring of kPinRing pinned
+  // buffers (host thread pool, non-temporal stores: hostcopy.cpp), running
+  // ahead of the DMA by up to kPinRing chunks, so the copy engine never waits
+  // for the host.
+  constexpr uint64_t kPinRing = 3;
   cudaPointerAttributes pa{};
   const bool pageable = cudaPointerGetAttributes(&pa, h_text) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered;
   cudaGetLastError();  // (older drivers report unregistered memory as an error)
   if (pageable)
-    for (int b = 0; b < 2; ++b)
+    for (uint64_t b = 0; b < kPinRing; ++b) {
       if (!c->pin[b]) CU(cudaMallocHost(&c->pin[b], kStreamChunk + halo + 64));
+      CU(cudaEventSynchronize(c->ev_pin[b]));  // (a previous call's DMA out of pin[b])
+    }
   auto span = [&](uint64_t i, uint64_t* lo, uint64_t* rd) {
     *lo = i * kStreamChunk;
     *rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - *lo) + halo, n - *lo);
   };
-  // pageable: a background thread stages chunk i + 2 into pin[i & 1] while
-  // chunk i + 1's DMA and chunk i's scan run, so the copy engine never waits
-  struct Stager {
+  // staged: chunks copied into the ring; issued: chunks whose DMA is enqueued
+  // (pin[i % kPinRing] is reusable once ev_pin of chunk i's DMA has fired)
+  struct Ring {
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t staged = 0, issued = 0;
+    bool stop = false, failed = false;
+    double copy_ms = 0, wait_ms = 0;  // GLOP_STAGE_TIMING
     std::thread th;
-    ~Stager() { join(); }
-    void join() {
+    ~Ring() {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+      }
+      cv.notify_all();
       if (th.joinable()) th.join();
     }
-  } stager;
-  auto stage = [&](uint64_t i) {  // pin[i & 1] must be free (its previous DMA done)
-    uint64_t lo, rd;
-    span(i, &lo, &rd);
-    stager.th = std::thread(parallel_memcpy, c->pin[i & 1], h_text + lo, rd);
-  };
+  } ring;
+  if (pageable)
+    ring.th = std::thread([&] {
+      for (uint64_t i = 0; i < chunks; ++i) {
+        const uint64_t b = i % kPinRing;
+        if (i >= kPinRing) {  // wait for chunk i - kPinRing's DMA to be enqueued, then done
+          std::unique_lock<std::mutex> lk(ring.mu);
+          ring.cv.wait(lk, [&] { return ring.stop || ring.issued > i - kPinRing; });
+          if (ring.stop) return;
+          lk.unlock();
+          if (cudaEventSynchronize(c->ev_pin[b]) != cudaSuccess) {
+            std::lock_guard<std::mutex> lk2(ring.mu);
+            ring.failed = true;
+            ring.cv.notify_all();
+            return;
+          }
+        }
+        uint64_t lo, rd;
+        span(i, &lo, &rd);
+        const auto t0 = std::chrono::steady_clock::now();
+        parallel_memcpy(c->pin[b], h_text + lo, rd);
+        ring.copy_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::lock_guard<std::mutex> lk(ring.mu);
+        ring.staged = i + 1;
+        ring.cv.notify_all();
+      }
+    });
   auto dma = [&](uint64_t i) -> glop_status {
     uint64_t lo, rd;
     span(i, &lo, &rd);
-    const void* src = pageable ? c->pin[i & 1] : static_cast<const void*>(h_text + lo);
+    const void* src = h_text + lo;
+    if (pageable) {
+      const auto t0 = std::chrono::steady_clock::now();
+      std::unique_lock<std::mutex> lk(ring.mu);
+      ring.cv.wait(lk, [&] { return ring.staged > i || ring.failed; });
+      ring.wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ring.staged <= i) return fail(GLOP_ECUDA, "run_pfac_pipeline: staging copy failed");
+      src = c->pin[i % kPinRing];
+    }
     CU(cudaStreamWaitEvent(c->cstream, c->ev_free[i & 1], 0));
     CU(cudaMemcpyAsync(c->sbuf[i & 1].p, src, rd, cudaMemcpyHostToDevice, c->cstream));
     CU(cudaEventRecord(c->ev_copied[i & 1], c->cstream));
+    if (pageable) {
+      CU(cudaEventRecord(c->ev_pin[i % kPinRing], c->cstream));
+      std::lock_guard<std::mutex> lk(ring.mu);
+      ring.issued = i + 1;
+      ring.cv.notify_all();
+    }
     return GLOP_OK;
   };
-  // ev_free[b]: buffer b may be overwritten (recorded after its chunk's work)
+  // ev_free[b]: device buffer b may be overwritten (recorded after its chunk's work)
   CU(cudaEventRecord(c->ev_free[0], c->stream));
   CU(cudaEventRecord(c->ev_free[1], c->stream));
-  if (pageable) {
-    CU(cudaEventSynchronize(c->ev_copied[0]));  // (a previous call's DMA out of pin[0] / pin[1])
-    CU(cudaEventSynchronize(c->ev_copied[1]));
-    stage(0);
-    stager.join();
-  }
   TRY(dma(0));
-  if (pageable && chunks > 1) stage(1);
   for (uint64_t i = 0; i < chunks; ++i) {
-    if (i + 1 < chunks) {
-      stager.join();
-      TRY(dma(i + 1));
-    }
-    if (pageable && i + 2 < chunks) {  // pin[i & 1] is free once chunk i's DMA is done
-      CU(cudaEventSynchronize(c->ev_copied[i & 1]));
-      stage(i + 2);
-    }
+    if (i + 1 < chunks) TRY(dma(i + 1));
     const uint64_t lo = i * kStreamChunk, own_i = std::min<uint64_t>(kStreamChunk, own - lo);
     const uint64_t rd = std::min<uint64_t>(own_i + halo, n - lo);
     CU(cudaStreamWaitEvent(c->stream, c->ev_copied[i & 1], 0));
     TRY(accum_window(c, t, r, A, c->sbuf[i & 1].as<uint8_t>(), rd, own_i, base + lo));
     CU(cudaEventRecord(c->ev_free[i & 1], c->stream));
   }
+  if (pageable && getenv("GLOP_STAGE_TIMING"))
+    fprintf(stderr, "staging: %llu chunks, copies %.1f ms, DMA issue waited %.1f ms\n", (unsigned long long)chunks,
+            ring.copy_ms, ring.wait_ms);
   return accum_end(c, A, alerts, n_alerts, counts, stage1_hits, lines, line_count);
 }
 
@@ -1198,6 +1224,9 @@ glop_status glop_ctx_create(int device, glop_ctx** out) {
     e = cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
   }
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&c->ev_pin[i], cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     delete c;
     return fail(GLOP_ECUDA, cudaGetErrorString(e));
@@ -1224,6 +1253,8 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
     if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
     if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
   }
+  for (cudaEvent_t e : c->ev_pin)
+    if (e) cudaEventDestroy(e);
   cudaFreeHost(c->h_misc);
   for (void* p : c->pin)
     if (p) cudaFreeHost(p);
