@@ -257,8 +257,9 @@ glop_status p8_geometry(glop_ctx* c, const uint8_t* d_text, uint64_t own, P8Geom
 glop_status launch_pfac8(glop_ctx* c, const glop_trie* t, const P8Geom& G, const P8Params& p) {
   using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
 #define GLOP_P8_K(w, l, c) {pfac8_kernel<w, l, uint16_t, c>, pfac8_kernel<w, l, uint32_t, c>}
-#define GLOP_P8_L(w, c) GLOP_P8_K(w, 0, c), GLOP_P8_K(w, 1, c), GLOP_P8_K(w, 2, c), GLOP_P8_K(w, 3, c)
-  static const KF table[2][2][4][2] = {{{GLOP_P8_L(false, false)}, {GLOP_P8_L(true, false)}},
+#define GLOP_P8_L(w, c) \
+  GLOP_P8_K(w, 0, c), GLOP_P8_K(w, 1, c), GLOP_P8_K(w, 2, c), GLOP_P8_K(w, 3, c), GLOP_P8_K(w, 4, c)
+  static const KF table[2][2][5][2] = {{{GLOP_P8_L(false, false)}, {GLOP_P8_L(true, false)}},
                                        {{GLOP_P8_L(false, true)}, {GLOP_P8_L(true, true)}}};
 #undef GLOP_P8_L
 #undef GLOP_P8_K
@@ -1388,7 +1389,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
   std::vector<unsigned long long> grams8;  // ((prev top byte, cur) << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
-  bool bits8 = false, bloom2 = false, two8 = false;
+  bool bits8 = false, bloom2 = false, two8 = false, lane8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -1447,11 +1448,18 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       grams8.erase(std::unique(grams8.begin(), grams8.end()), grams8.end());
       const char* env = getenv("GLOP_P8_BITS_MIN");  // experiments: override the layout threshold
       bits8 = grams8.size() > (env ? (size_t)atoll(env) : (size_t)kP8BitsGrams);
+      const char* env3 = getenv("GLOP_P8_LANE_MAX");  // experiments: override the lane-replicated threshold
+      const char* env4 = getenv("GLOP_P8_LANE_MIN");
+      lane8 = grams8.size() <= (env3 ? (size_t)atoll(env3) : (size_t)kP8LaneGrams) &&
+              grams8.size() > (env4 ? (size_t)atoll(env4) : (size_t)kP8LaneMinGrams);
       const char* env2 = getenv("GLOP_P8_BITS2_MIN");  // experiments: override the two-bit threshold
       two8 = bits8 && grams8.size() > (env2 ? (size_t)atoll(env2) : (size_t)kP8Bits2Grams);
       for (unsigned long long x : grams8) {
         const uint32_t cur = (uint32_t)(x >> 2), prev = (uint32_t)(x >> 34) << 24, bit = 1u << (x & 3);
-        if (bits8) {  // little-endian bits of the u32 words
+        if (lane8) {  // the gram's bit in every lane's copy of its word
+          const uint32_t w = p8_lane_off(prev, cur), b1 = p8_bit1(cur) & 31u;
+          for (uint32_t l = 0; l < 32; ++l) dmask8[w + 4 * l + (b1 >> 3)] |= (uint8_t)(1u << (b1 & 7));
+        } else if (bits8) {  // little-endian bits of the u32 words
           const uint32_t w = p8_word_off(prev, cur);
           const uint32_t b1 = p8_bit1(cur) & 31u;
           dmask8[w + (b1 >> 3)] |= (uint8_t)(1u << (b1 & 7));
@@ -1466,7 +1474,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
     }
     if (p8) {  // large prefix sets: a second level-2 bit per prefix
       const char* env = getenv("GLOP_P8_BLOOM2_MIN");  // experiments: override the threshold
-      bloom2 = bits8 && keys.size() > (env ? (size_t)atoll(env) : (size_t)kP8Bloom2Keys);
+      bloom2 = bits8 && !lane8 && keys.size() > (env ? (size_t)atoll(env) : (size_t)kP8Bloom2Keys);
       if (bloom2)
         for (const auto& kv : keys) {
           const uint32_t bit = prefix_bit2(kv.first);
@@ -1533,7 +1541,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
-  t->p8_l1 = two8 && bloom2 ? 3 : bloom2 ? 2 : bits8 ? 1 : 0;
+  t->p8_l1 = lane8 ? 4 : two8 && bloom2 ? 3 : bloom2 ? 2 : bits8 ? 1 : 0;
   t->p8_lane_emits = 4 * max_emits;
   t->p8_careful = t->p8_lane_emits > kP8Hits - GLOP_P8_FLUSH_AT || getenv("GLOP_P8_CAREFUL");
   t->view.jump_depth = J;

@@ -110,6 +110,11 @@ __device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// TMA prefetch of global [src, src + bytes) into L2 (16-byte aligned, size a
+// multiple of 16): memory-level parallelism without shared memory
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(

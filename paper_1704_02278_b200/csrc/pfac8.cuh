@@ -55,6 +55,12 @@ constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 #ifndef GLOP_P8_FLUSH_AT
 #define GLOP_P8_FLUSH_AT 16
 #endif
+// L2 prefetch distance: each warp also prefetches (TMA, into L2 only) the
+// tiles this many past the two in its shared-memory pipeline
+#ifndef GLOP_P8_L2PF
+#define GLOP_P8_L2PF 0
+#endif
+constexpr uint32_t kP8L2Pf = GLOP_P8_L2PF;
 constexpr uint32_t kP8DmaskLog2 = GLOP_P8_DMASK_LOG2;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
 // level-2 prefix bitmap of the pfac8 kernel (shared memory): 2^18 bits by
@@ -163,8 +169,32 @@ __host__ __device__ __forceinline__ uint32_t p8_byte_off(uint32_t prev, uint32_t
 // blocked Bloom filter: bits p8_bit1 and p8_bit2 of the word) passes ~1%
 // for two more instructions and no extra shared-memory wavefront per probe.
 constexpr uint32_t kP8Bits2Grams = 12000;
-template <bool kBits, bool kTwo = false>
+// Small gram sets (kP8LaneGrams): the "lane-replicated" layout -- 512 words
+// of 32 bits (16K one-bit buckets), each word stored once per bank, lane l's
+// copy in bank l (byte offset w * 128 + 4 l).  Every lane reads only its own
+// bank, so a probe instruction is ONE shared-memory wavefront instead of ~3.5
+// for 32 random banks: the level-1 probes were ~55% of the kernel's
+// wavefronts, and the LSU data pipe is what bounds it.  16K buckets keep the
+// false candidates at a few percent up to ~1,000 grams (measured, 8 GB
+// syslog: k=20 1.89 -> 1.73 ms, k=100 2.01 -> 1.79 ms, k=200 2.03 -> 1.92 ms;
+// k=300 (1,188 grams) 2.03 -> 2.11 ms, so the one-bit layout keeps those).
+// (below kP8LaneMinGrams the 64K-bucket byte layout's near-empty table lets
+// most tiles skip the candidate stage entirely, which wins)
+constexpr uint32_t kP8LaneGrams = 1000, kP8LaneMinGrams = 64;
+__host__ __device__ __forceinline__ uint32_t p8_lane_off(uint32_t prev, uint32_t cur) {
+#ifdef __CUDA_ARCH__
+  const uint32_t pb = __byte_perm(prev, 0u, 0x4434);
+#else
+  const uint32_t pb = (prev >> 16) & 0xFF00u;
+#endif
+  return (p8_mulhi(cur) ^ pb) & 0xFF80u;  // word w at bits 7..15: w * 128
+}
+template <bool kBits, bool kTwo = false, bool kLane = false>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t prev, uint32_t cur) {
+  if (kLane) {  // dm = this lane's bank column
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_lane_off(prev, cur));
+    return __funnelshift_r(w, w, p8_bit1(cur));
+  }
   if (kBits) {  // bit p8_bit1 of the word, in bit 0 (bits 1..31: don't care)
     const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_word_off(prev, cur));
     if (kTwo) return __funnelshift_r(w, w, p8_bit1(cur)) & __funnelshift_r(w, w, p8_bit2(cur));
@@ -227,7 +257,8 @@ __device__ __forceinline__ uint32_t p8_flush(unsigned long long* hk, uint32_t nb
   return nb;
 }
 
-// kL1: 0 byte d-mask buckets; 1 one-bit buckets; 2 one-bit buckets and a
+// kL1: 4 lane-replicated one-bit buckets (small gram sets);
+// 0 byte d-mask buckets; 1 one-bit buckets; 2 one-bit buckets and a
 // second level-2 bitmap probe (prefix_bit2_32) for large prefix sets; 3 as 2
 // with two bits per gram in the level-1 word (kP8Bits2Grams).
 // kCareful: a replayed lane always starts with an empty hit buffer.  Without
@@ -240,10 +271,11 @@ template <bool kWalk, int kL1, typename Entry, bool kCareful>
 __global__ void __launch_bounds__(kP8Threads, 1)
     pfac8_kernel(const DevTrie tr, const P8Params p, const P8Layout L) {
   using ET = EntryTraits<Entry>;
-  constexpr bool kBits = kL1 != 0, kB2 = kL1 >= 2, kTwo = kL1 == 3;
+  constexpr bool kBits = kL1 != 0, kB2 = kL1 == 2 || kL1 == 3, kTwo = kL1 == 3, kLane = kL1 == 4;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint8_t* s_dmask = smem + L.dmask;
+  const uint8_t* s_dm = kLane ? s_dmask + 4 * (threadIdx.x & 31) : s_dmask;  // (kLane: this lane's bank)
   const uint32_t* s_bm2 = reinterpret_cast<const uint32_t*>(smem + L.bm2);
   const uint32_t bm2_a = smem_u32(s_bm2);
   const uint8_t* s_cls = smem + L.cls;
@@ -272,11 +304,17 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   const uint32_t t0 = min(cta_lo + warp * p.sub, cta_hi), t1 = min(t0 + p.sub, cta_hi);
   const uint32_t a = (uint32_t)((uintptr_t)p.text & 15);
   const uint8_t* A = p.text - a;
-  if (lane == 0)
+  auto l2_prefetch = [&](uint32_t tt) {  // whole interior tiles only
+    const unsigned long long lo = (unsigned long long)tt * kP8Tile;
+    if (tt < t1 && lo >= a && lo + kP8Stage <= a + p.n) bulk_prefetch_l2(A + lo, kP8Stage);
+  };
+  if (lane == 0) {
     for (uint32_t b = 0; b < 2; ++b)
       if (t0 + b < t1)
         p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
                  (unsigned long long)(t0 + b) * kP8Tile);
+    for (uint32_t b = 0; b < kP8L2Pf; ++b) l2_prefetch(t0 + 2 + b);
+  }
   const unsigned long long own_end = p.own + a, n_end = p.n + a;  // aligned coordinates
   // interior tiles: t >= 1, all kP8Tile starts owned, the whole stage inside
   // the text -- no range masks
@@ -374,14 +412,14 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (lane == 31) nb = wn;
         uint32_t* a = mm4[2 * hf];
         uint32_t* b = mm4[2 * hf + 1];
-        a[0] = p8_dmask<kBits, kTwo>(s_dmask, va.x, va.y);
-        a[1] = p8_dmask<kBits, kTwo>(s_dmask, va.y, va.z);
-        a[2] = p8_dmask<kBits, kTwo>(s_dmask, va.z, va.w);
-        a[3] = p8_dmask<kBits, kTwo>(s_dmask, va.w, na);
-        b[0] = p8_dmask<kBits, kTwo>(s_dmask, vb.x, vb.y);
-        b[1] = p8_dmask<kBits, kTwo>(s_dmask, vb.y, vb.z);
-        b[2] = p8_dmask<kBits, kTwo>(s_dmask, vb.z, vb.w);
-        b[3] = p8_dmask<kBits, kTwo>(s_dmask, vb.w, nb);
+        a[0] = p8_dmask<kBits, kTwo, kLane>(s_dm, va.x, va.y);
+        a[1] = p8_dmask<kBits, kTwo, kLane>(s_dm, va.y, va.z);
+        a[2] = p8_dmask<kBits, kTwo, kLane>(s_dm, va.z, va.w);
+        a[3] = p8_dmask<kBits, kTwo, kLane>(s_dm, va.w, na);
+        b[0] = p8_dmask<kBits, kTwo, kLane>(s_dm, vb.x, vb.y);
+        b[1] = p8_dmask<kBits, kTwo, kLane>(s_dm, vb.y, vb.z);
+        b[2] = p8_dmask<kBits, kTwo, kLane>(s_dm, vb.z, vb.w);
+        b[3] = p8_dmask<kBits, kTwo, kLane>(s_dm, vb.w, nb);
         if (kBits) {  // byte j = probe j's bit 0
           mq[2 * hf] = __byte_perm(__byte_perm(a[0], a[1], 0x40), __byte_perm(a[2], a[3], 0x40), 0x5410) & 0x01010101u;
           mq[2 * hf + 1] = __byte_perm(__byte_perm(b[0], b[1], 0x40), __byte_perm(b[2], b[3], 0x40), 0x5410) & 0x01010101u;
@@ -535,6 +573,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
       fence_proxy_async();
       p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
                (unsigned long long)(t + 2) * kP8Tile);
+      if (kP8L2Pf) l2_prefetch(t + 2 + kP8L2Pf);
     }
   }
   if (p.mode == 0) {

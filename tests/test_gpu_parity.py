@@ -192,10 +192,14 @@ def test_large_syslog_vs_oracle(ctx, torch_cuda, k):
 
 
 # level-1 table layouts of the PREFIX8 kernel (pfac8.cuh): the host picks
-# one-byte d-mask buckets or one-bit buckets by gram count; force each
-P8_LAYOUTS = {"auto": {}, "bytes": {"GLOP_P8_BITS_MIN": "1000000000"},
-              "bits": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "1000000000"},
-              "bits+bloom2": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "0"}}
+# lane-replicated bits, one-byte d-mask buckets or one-bit buckets (+ a second
+# level-2 bit, + two level-1 bits) by gram count; force each
+P8_LAYOUTS = {"auto": {}, "bytes": {"GLOP_P8_BITS_MIN": "1000000000", "GLOP_P8_LANE_MAX": "0"},
+              "lane": {"GLOP_P8_LANE_MAX": "1000000000"},
+              "bits": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "1000000000", "GLOP_P8_LANE_MAX": "0"},
+              "bits+bloom2": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "0", "GLOP_P8_LANE_MAX": "0"},
+              "two-bit": {"GLOP_P8_BITS_MIN": "0", "GLOP_P8_BLOOM2_MIN": "0", "GLOP_P8_BITS2_MIN": "0",
+                          "GLOP_P8_LANE_MAX": "0"}}
 
 
 @pytest.mark.parametrize("layout", list(P8_LAYOUTS))
