@@ -120,7 +120,7 @@ struct glop_ctx {
   DBuf keep, bcounts, bprefix, alerts, kmp_dfa, spill;
   DBuf sbuf[2];                                  // streamed text chunks (host-text pipeline)
   DBuf lcount, lprefix, loffs;                   // device LineIndex
-  DBuf hprefix, kcounts, kprefix, keep8, counts_tmp;  // fused pipeline (pipeline.cuh)
+  DBuf kcounts, keep8, counts_tmp;  // fused pipeline (pipeline.cuh)
   DBuf palerts, plines;                          // alerts (+ lines) of the host-facing pipeline calls
   std::string kmp_key;                           // pattern + failure table of the DFA in kmp_dfa
   Accum acc;                                     // streamed pipeline results
@@ -244,7 +244,6 @@ glop_status p8_geometry(glop_ctx* c, const uint8_t* d_text, uint64_t own, P8Geom
   G->sub = (G->per + kP8Warps - 1) / kP8Warps;
   G->regions = (unsigned long long)G->grid * kP8Warps;
   TRY(c->bcounts.ensure(8 * G->regions));
-  TRY(c->prefix.ensure(8 * G->regions));
   TRY(c->misc.ensure(64));
   unsigned long long region =
       std::max<unsigned long long>(256, (std::max<uint64_t>(1 << 20, own / 512) + G->regions - 1) / G->regions);
@@ -304,13 +303,12 @@ glop_status pfac8_scan_impl(glop_ctx* c, const glop_trie* t, const uint8_t* d_te
     CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
     P8Params p = p8_params(c, t, G, d_text, n, own, base);
     TRY(launch_pfac8(c, t, G, p));
-    // ordered output, enqueued before the flags are known (see p8_gather_kernel)
-    c->launches += 2;
-    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)G.regions,
-                                                 c->prefix.as<unsigned long long>());
-    p8_gather_kernel<DevHit><<<(uint32_t)G.regions, 256, 0, c->stream>>>(
-        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), G.region,
-        reinterpret_cast<const DevHit*>(c->staging.p), reinterpret_cast<DevHit*>(d_out), cap);
+    // ordered output, enqueued before the flags are known (see gather_regions_kernel)
+    ++c->launches;
+    gather_regions_kernel<DevHit><<<(uint32_t)std::min<unsigned long long>(G.regions, 2ull * c->num_sms), 256, 0,
+                                    c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)G.regions, G.region,
+                                                 reinterpret_cast<const DevHit*>(c->staging.p),
+                                                 reinterpret_cast<DevHit*>(d_out), cap);
     CU(cudaGetLastError());
     TRY(sync_read(c, c->misc.p, 32));
     const unsigned long long total = c->h_misc[kStTotal], maxregion = c->h_misc[kStMaxRegion];
@@ -534,7 +532,6 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
   const uint32_t per = (num_tiles + grid - 1) / grid, sub = (per + kK3Warps - 1) / kK3Warps;
   const unsigned long long regions = (unsigned long long)grid * kK3Warps;
   TRY(c->bcounts.ensure(8 * regions));
-  TRY(c->prefix.ensure(8 * regions));
   TRY(c->misc.ensure(64));
   unsigned long long region = std::max<unsigned long long>(256, (own / 8192 + regions - 1) / regions);
   if (c->staging.bytes < region * regions * 8) TRY(c->staging.ensure(region * regions * 8));
@@ -574,13 +571,12 @@ glop_status kmp_device_impl(glop_ctx* c, const uint8_t* pat, uint32_t m, const u
     p.g_count = g;
     p.comparisons = g + 2;
     TRY(launch(p));
-    // ordered output, enqueued before the flags are known (see p8_gather_kernel)
-    c->launches += 2;
-    u64_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->bcounts.as<unsigned long long>(), (uint32_t)regions,
-                                                 c->prefix.as<unsigned long long>());
-    p8_gather_kernel<unsigned long long><<<(uint32_t)regions, 256, 0, c->stream>>>(
-        c->bcounts.as<unsigned long long>(), c->prefix.as<unsigned long long>(), region,
-        c->staging.as<unsigned long long>(), reinterpret_cast<unsigned long long*>(d_out), cap);
+    // ordered output, enqueued before the flags are known (see gather_regions_kernel)
+    ++c->launches;
+    gather_regions_kernel<unsigned long long>
+        <<<(uint32_t)std::min<unsigned long long>(regions, 2ull * c->num_sms), 256, 0, c->stream>>>(
+            c->bcounts.as<unsigned long long>(), (uint32_t)regions, region, c->staging.as<unsigned long long>(),
+            reinterpret_cast<unsigned long long*>(d_out), cap);
     CU(cudaGetLastError());
     if (ticket) {  // no host wait: the status block lands in the ticket
       ticket->region = region;
@@ -736,46 +732,40 @@ glop_status pipeline_device_impl(glop_ctx* c, const glop_trie* t, const glop_rul
     P8Geom G;
     TRY(p8_geometry(c, d_text, own, &G));
     const bool stage2 = r->max_len > r->view.prefix_len;
-    TRY(c->hprefix.ensure(8 * G.regions));
     if (stage2) {
       TRY(c->kcounts.ensure(8 * G.regions));
-      TRY(c->kprefix.ensure(8 * G.regions));
       TRY(c->keep8.ensure(G.regions * G.region));
     }
     auto* g = c->misc.as<unsigned long long>();
     CU(cudaMemsetAsync(c->misc.p, 0, 64, c->stream));
-    const P8Params p = p8_params(c, t, G, d_text, n, own, base);
+    P8Params p = p8_params(c, t, G, d_text, n, own, base);
+    p.zero = reinterpret_cast<unsigned long long*>(d_counts);  // (the scan's grid zeroes the counts)
+    p.nzero = k;
     TRY(launch_pfac8(c, t, G, p));
     const auto* cnt = c->bcounts.as<unsigned long long>();
-    p8_prefix_kernel<<<1, 1024, 0, c->stream>>>(cnt, (uint32_t)G.regions, G.region,
-                                                c->hprefix.as<unsigned long long>(), g + kStHits,
-                                                reinterpret_cast<unsigned long long*>(d_counts), k);
     const uint32_t egrid = (uint32_t)std::min<unsigned long long>(G.regions, 2ull * c->num_sms);
-    const uint32_t hist_bins = (size_t)k * 4 <= kSmemMax - 1024 ? k : 0;
+    const uint32_t hist_bins = (size_t)k * 4 <= kSmemMax - 2048 ? k : 0;
     const size_t hist_bytes = (size_t)hist_bins * 4;
     if (stage2) {
-      c->launches += 2;
+      ++c->launches;
       p8_keep_kernel<<<(uint32_t)std::min<unsigned long long>(G.regions, 8ull * c->num_sms), 256, 0, c->stream>>>(
           r->view, d_text, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
           c->keep8.as<uint8_t>(), c->kcounts.as<unsigned long long>(), g + kStVerify);
-      p8_prefix_kernel<<<1, 1024, 0, c->stream>>>(c->kcounts.as<unsigned long long>(), (uint32_t)G.regions,
-                                                  G.region, c->kprefix.as<unsigned long long>(), g + kStKept,
-                                                  nullptr, 0);
       CU(cudaFuncSetAttribute(p8_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_bytes));
       p8_emit_kernel<true><<<egrid, 1024, hist_bytes, c->stream>>>(
           r->view, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
-          c->keep8.as<uint8_t>(), c->hprefix.as<unsigned long long>(), c->kprefix.as<unsigned long long>(),
-          reinterpret_cast<DevHit*>(d_hits), d_hits ? hit_cap : 0, reinterpret_cast<DevAlert*>(d_alerts), alert_cap,
-          reinterpret_cast<unsigned long long*>(d_counts), hist_bins, g + kStVerify);
+          c->keep8.as<uint8_t>(), c->kcounts.as<unsigned long long>(), reinterpret_cast<DevHit*>(d_hits),
+          d_hits ? hit_cap : 0, reinterpret_cast<DevAlert*>(d_alerts), alert_cap,
+          reinterpret_cast<unsigned long long*>(d_counts), hist_bins, g);
     } else {
       CU(cudaFuncSetAttribute(p8_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist_bytes));
       p8_emit_kernel<false><<<egrid, 1024, hist_bytes, c->stream>>>(
           r->view, base, n, cnt, (uint32_t)G.regions, G.region, reinterpret_cast<const DevHit*>(c->staging.p),
-          nullptr, c->hprefix.as<unsigned long long>(), nullptr, reinterpret_cast<DevHit*>(d_hits),
-          d_hits ? hit_cap : 0, reinterpret_cast<DevAlert*>(d_alerts), alert_cap,
-          reinterpret_cast<unsigned long long*>(d_counts), hist_bins, g + kStVerify);
+          nullptr, nullptr, reinterpret_cast<DevHit*>(d_hits), d_hits ? hit_cap : 0,
+          reinterpret_cast<DevAlert*>(d_alerts), alert_cap, reinterpret_cast<unsigned long long*>(d_counts),
+          hist_bins, g);
     }
-    c->launches += 2;
+    ++c->launches;
     CU(cudaGetLastError());
     if (ticket) {  // no host wait: the status block lands in the ticket, read after the stream syncs
       ticket->region = G.region;
@@ -1243,7 +1233,7 @@ glop_status glop_ctx_destroy(glop_ctx* c) {
   for (DBuf* b : {&c->text, &c->staging, &c->out, &c->dir, &c->prefix, &c->misc, &c->keys,
                   &c->keys_alt, &c->cub_tmp, &c->keep, &c->bcounts, &c->bprefix, &c->alerts,
                   &c->kmp_dfa, &c->spill, &c->sbuf[0], &c->sbuf[1], &c->lcount, &c->lprefix, &c->loffs,
-                  &c->hprefix, &c->kcounts, &c->kprefix, &c->keep8, &c->counts_tmp, &c->palerts, &c->plines})
+                  &c->kcounts, &c->keep8, &c->counts_tmp, &c->palerts, &c->plines})
     b->release();
   c->acc.release();
   if (c->cstream) {

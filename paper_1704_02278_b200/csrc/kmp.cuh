@@ -17,7 +17,7 @@
 // double-buffered TMA pipeline -- no CTA barriers.  A warp's matches come out
 // in text order tile by tile (a tile's few keys are warp-sorted in shared
 // memory), so the output is the concatenation of the per-warp staging
-// regions (u64_prefix_kernel + p8_gather_kernel).  A tile with more matches
+// regions (gather_regions_kernel).  A tile with more matches
 // than the buffer flags the exact global-key fallback (CUB radix sort).
 #pragma once
 #include <type_traits>

@@ -105,6 +105,8 @@ struct P8Params {
   unsigned long long* keys;      // mode 1
   unsigned long long keys_cap;
   const uint8_t* dmask8;         // 2^16 d-masks (bits 0..3: offsets d = 1..4)
+  unsigned long long* zero;      // optional: zeroed by the grid before the scan (the pipeline's per-pattern counts)
+  uint32_t nzero;
 };
 
 // Level-1 d-mask of an aligned text word (bit d-1: the word may be the
@@ -286,6 +288,8 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   unsigned long long* hk = reinterpret_cast<unsigned long long*>(smem + L.hits) + warp * kP8Hits;
   uint32_t* s_nh = reinterpret_cast<uint32_t*>(smem + L.nh) + warp;
 
+  if (p.zero)  // (read only by kernels launched after this one)
+    for (uint32_t i = blockIdx.x * kP8Threads + tid; i < p.nzero; i += gridDim.x * kP8Threads) p.zero[i] = 0;
   {
     const uint4* s = reinterpret_cast<const uint4*>(p.dmask8);
     uint4* d = reinterpret_cast<uint4*>(smem + L.dmask);
@@ -591,43 +595,41 @@ __global__ void __launch_bounds__(kP8Threads, 1)
   }
 }
 
-// Concatenates the per-warp regions (each already in text order) in warp
-// order: region g's hits go to out[prefix[g], prefix[g] + counts[g]).
-// Launched before the host has looked at the scan's flags (saves a round
-// trip): records past `cap` or beyond a region are not copied, and a flagged
-// scan is redone anyway.
-template <typename Rec>
-__global__ void __launch_bounds__(256) p8_gather_kernel(const unsigned long long* counts,
-                                                        const unsigned long long* prefix,
-                                                        unsigned long long region, const Rec* staging,
-                                                        Rec* out, unsigned long long cap) {
-  const uint32_t g = blockIdx.x;
-  const unsigned long long c = min(counts[g], region), dst = prefix[g];
-  const Rec* src = staging + (unsigned long long)g * region;
-  for (unsigned long long h = threadIdx.x; h < c && dst + h < cap; h += blockDim.x) out[dst + h] = src[h];
+// sum over i in [0, n) of min(counts[i], cap), in every thread of the CTA
+// (s_red: 32 words of shared memory; blockDim.x a multiple of 32)
+__device__ __forceinline__ unsigned long long block_sum_counts(const unsigned long long* counts, uint32_t n,
+                                                               unsigned long long cap, unsigned long long* s_red) {
+  unsigned long long s = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s += min(counts[i], cap);
+  for (uint32_t o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();  // (s_red may still be read from a previous call)
+  if (lane == 0) s_red[w] = s;
+  __syncthreads();
+  s = lane < blockDim.x / 32 ? s_red[lane] : 0ull;
+  for (uint32_t o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
 }
 
-// Exclusive prefix of u64 counts (single CTA, any n).
-__global__ void __launch_bounds__(1024) u64_prefix_kernel(const unsigned long long* counts, uint32_t n,
-                                                          unsigned long long* prefix) {
-  __shared__ unsigned long long part[1024];
-  const uint32_t tid = threadIdx.x;
-  const uint32_t per = (n + 1023) / 1024;
-  const uint32_t b = tid * per, e = min(n, b + per);
-  unsigned long long s = 0;
-  for (uint32_t i = b; i < e; ++i) s += counts[i];
-  part[tid] = s;
-  __syncthreads();
-  for (uint32_t off = 1; off < 1024; off <<= 1) {
-    const unsigned long long v = tid >= off ? part[tid - off] : 0;
-    __syncthreads();
-    part[tid] += v;
-    __syncthreads();
-  }
-  unsigned long long run = part[tid] - s;
-  for (uint32_t i = b; i < e; ++i) {
-    prefix[i] = run;
-    run += counts[i];
+// Concatenates the per-warp regions (each already in text order) in warp
+// order, each CTA a contiguous range of regions: the range's output offset is
+// the sum of the counts before it (computed here -- no separate prefix
+// launch), region g's hits go to out[prefix(g), prefix(g) + counts[g]).
+// Launched before the host has looked at the scan's flags: records past
+// `cap` or beyond a region are not copied, and a flagged scan is redone.
+template <typename Rec>
+__global__ void __launch_bounds__(256) gather_regions_kernel(const unsigned long long* counts, uint32_t regions,
+                                                             unsigned long long region, const Rec* staging,
+                                                             Rec* out, unsigned long long cap) {
+  __shared__ unsigned long long s_red[32];
+  const uint32_t per = (regions + gridDim.x - 1) / gridDim.x;
+  const uint32_t g0 = min(blockIdx.x * per, regions), g1 = min(g0 + per, regions);
+  unsigned long long dst = block_sum_counts(counts, g0, region, s_red);
+  for (uint32_t g = g0; g < g1; ++g) {
+    const unsigned long long c = min(counts[g], region);
+    const Rec* src = staging + (unsigned long long)g * region;
+    for (unsigned long long h = threadIdx.x; h < c && dst + h < cap; h += blockDim.x) out[dst + h] = src[h];
+    dst += c;
   }
 }
 

@@ -2,13 +2,13 @@
 // (pipeline.hpp:86-97) after pfac8_kernel, enqueued without host round trips:
 //
 //   pfac8_kernel        per-warp staging regions (already in text order)
-//   p8_prefix_kernel    exclusive prefix of the region hit counts; zeroes the
-//                       per-pattern counts (no separate memset)
+//                       (its grid also zeroes the per-pattern counts)
 //   p8_keep_kernel      stage 2 only (some pattern longer than the prefix):
 //                       the suffix compare of verify_hits (verify.hpp:78-87)
 //                       per hit -> keep flags + kept count per region
-//   p8_prefix_kernel    exclusive prefix of the kept counts (stage 2 only)
-//   p8_emit_kernel      stable compaction of the kept hits into alerts in
+//   p8_emit_kernel      each CTA a contiguous range of regions, its output
+//                       offsets summed from the counts before it (no prefix
+//                       launch); stable compaction of the kept hits into alerts in
 //                       (offset, rule_id) order (verify.hpp:100-103: the
 //                       regions are already sorted), the optional ordered hit
 //                       list, and the per-pattern alert histogram
@@ -18,41 +18,13 @@
 // staging region or a hit buffer is redone by the general path.
 #pragma once
 #include "glop_kernels.cuh"
+#include "pfac8.cuh"
 
 namespace glop {
 
 // Status words in the scan's g_count block (u64 each).
 enum : uint32_t { kStTotal = 0, kStFlags = 1, kStMaxRegion = 2, kStKeys = 3, kStHits = 4, kStKept = 5,
                   kStVerify = 6 };
-
-// Exclusive prefix of min(counts[g], region) over n regions (one CTA), the
-// sum to *total, and zeroes zero[0, nzero) (the per-pattern counts).
-__global__ void __launch_bounds__(1024) p8_prefix_kernel(const unsigned long long* counts, uint32_t n,
-                                                         unsigned long long region, unsigned long long* prefix,
-                                                         unsigned long long* total, unsigned long long* zero,
-                                                         uint32_t nzero) {
-  __shared__ unsigned long long part[1024];
-  const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < nzero; i += 1024) zero[i] = 0;
-  const uint32_t per = (n + 1023) / 1024;
-  const uint32_t b = tid * per, e = min(n, b + per);
-  unsigned long long s = 0;
-  for (uint32_t i = b; i < e; ++i) s += min(counts[i], region);
-  part[tid] = s;
-  __syncthreads();
-  for (uint32_t off = 1; off < 1024; off <<= 1) {
-    const unsigned long long v = tid >= off ? part[tid - off] : 0;
-    __syncthreads();
-    part[tid] += v;
-    __syncthreads();
-  }
-  unsigned long long run = part[tid] - s;
-  for (uint32_t i = b; i < e; ++i) {
-    prefix[i] = run;
-    run += min(counts[i], region);
-  }
-  if (tid == 1023) *total = part[1023];
-}
 
 // 8 bytes at any alignment from two aligned loads (the caller keeps p + 15
 // inside the allocation).
@@ -127,27 +99,44 @@ __global__ void __launch_bounds__(256) p8_keep_kernel(const DevRules r, const ui
 // The per-pattern histogram lives in shared memory (hist_bins = n_patterns,
 // flushed once per CTA) when it fits, else global atomics.  Without stage 2
 // the bounds / id checks happen here (flag 1 of *vflags).
+// Each CTA takes a contiguous range of regions and computes the output
+// offsets of its range itself (sums of the hit / kept counts before it), so
+// no prefix kernel runs between the scan and this one; CTA 0 also writes the
+// totals to the status block (g_status[kStHits], [kStKept]).
 template <bool kStage2>
 __global__ void __launch_bounds__(1024) p8_emit_kernel(const DevRules r, unsigned long long base,
                                                        unsigned long long n, const unsigned long long* counts,
                                                        uint32_t regions, unsigned long long region,
                                                        const DevHit* staging, const uint8_t* keep,
-                                                       const unsigned long long* hprefix,
-                                                       const unsigned long long* kprefix, DevHit* hits_out,
+                                                       const unsigned long long* kcounts, DevHit* hits_out,
                                                        unsigned long long hit_cap, DevAlert* out,
                                                        unsigned long long alert_cap, unsigned long long* gcounts,
-                                                       uint32_t hist_bins, unsigned long long* vflags) {
+                                                       uint32_t hist_bins, unsigned long long* g_status) {
   extern __shared__ uint32_t hist[];
   __shared__ uint32_t warp_base[32];
   __shared__ uint32_t chunk_total;
+  __shared__ unsigned long long s_red[32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (uint32_t i = tid; i < hist_bins; i += blockDim.x) hist[i] = 0;
+  const uint32_t per = (regions + gridDim.x - 1) / gridDim.x;
+  const uint32_t g0 = min(blockIdx.x * per, regions), g1 = min(g0 + per, regions);
+  unsigned long long hp = block_sum_counts(counts, g0, region, s_red);
+  unsigned long long kp = kStage2 ? block_sum_counts(kcounts, g0, region, s_red) : 0ull;
+  if (blockIdx.x == 0) {
+    const unsigned long long th = block_sum_counts(counts, regions, region, s_red);
+    const unsigned long long tk = kStage2 ? block_sum_counts(kcounts, regions, region, s_red) : 0ull;
+    if (tid == 0) {
+      g_status[kStHits] = th;
+      if (kStage2) g_status[kStKept] = tk;
+    }
+  }
   __syncthreads();
+  unsigned long long* vflags = g_status + kStVerify;
   uint32_t bad = 0;
-  for (uint32_t g = blockIdx.x; g < regions; g += gridDim.x) {
-    const unsigned long long c = min(counts[g], region), hp = hprefix[g];
+  for (uint32_t g = g0; g < g1; ++g) {
+    const unsigned long long c = min(counts[g], region);
     const DevHit* src = staging + (unsigned long long)g * region;
-    unsigned long long dst0 = kStage2 ? kprefix[g] : hp;
+    unsigned long long dst0 = kStage2 ? kp : hp;
     for (unsigned long long i0 = 0; i0 < c; i0 += blockDim.x) {
       const unsigned long long i = i0 + tid;
       DevHit x{};
@@ -194,6 +183,8 @@ __global__ void __launch_bounds__(1024) p8_emit_kernel(const DevRules r, unsigne
         else atomicAdd(gcounts + x.pid, 1ull);
       }
     }
+    hp += c;
+    if (kStage2) kp = dst0;
   }
   if (bad) atomicOr(reinterpret_cast<unsigned int*>(vflags), 1u);
   __syncthreads();
