@@ -887,6 +887,12 @@ def bench_kmp(args, ctx, stream, rank, world, local, barrier, max_over_ranks):
             line["cpu_baseline"] = {"value": round(8 * sample / statistics.mean(secs) / 1e9, 3), "unit": "Gbps",
                                     "cores": 1, "kind": "reference", "cpu_model": O.cpu_model(),
                                     "sample": f"kmp_multi on the first {sample} bytes, single thread by design"}
+            # context: the reference's multi-core pfac_scan + verify_hits with k=1
+            psecs, _ = O.ref_time_pfac(host, [p], 8, 1, 3)
+            line["cpu_baseline"]["pfac_k1_multicore"] = {
+                "value": round(8 * sample / statistics.mean(psecs) / 1e9, 3), "unit": "Gbps",
+                "cores": int(O.ref().ref_default_workers()),
+                "sample": f"pfac_scan + verify_hits, the one pattern, L=8, same {sample} bytes"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0

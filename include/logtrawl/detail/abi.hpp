@@ -107,7 +107,9 @@ struct RulesEntry {
   std::string key;
   glop_group_rules* rules = nullptr;
   glop_group_trie* trie = nullptr;  // failureless trie over truncate_prefixes(rules, prefix_len), when built
-  std::atomic<std::uint64_t> last_alerts{0};  // alerts of the last pipeline call (Alert storage is prepared ahead)
+  // alerts and text bytes of the last pipeline call: the Alert storage of a
+  // similar-sized call is prepared while the device works
+  std::atomic<std::uint64_t> last_alerts{0}, last_bytes{0};
   ~RulesEntry() {
     if (trie) glop_group_trie_destroy(trie);
     if (rules) glop_group_rules_destroy(rules);
