@@ -126,6 +126,7 @@ struct glop_ctx {
   Accum acc;                                     // streamed pipeline results
   cudaStream_t cstream = nullptr;                // H2D copies of the streamed pipeline
   void* pin[3] = {nullptr, nullptr, nullptr};    // pinned staging of pageable host text (ring)
+  size_t pin_bytes = 0;                          // size of each pin[] buffer
   cudaEvent_t ev_pin[3] = {};                    // DMA out of pin[b] done
   cudaEvent_t ev_copied[2] = {}, ev_free[2] = {};
   unsigned long long* h_misc = nullptr;  // pinned readback
@@ -939,11 +940,17 @@ glop_status run_pipeline_streamed(glop_ctx* c, const glop_trie* t, const glop_ru
   cudaPointerAttributes pa{};
   const bool pageable = cudaPointerGetAttributes(&pa, h_text) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered;
   cudaGetLastError();  // (older drivers report unregistered memory as an error)
-  if (pageable)
-    for (uint64_t b = 0; b < kPinRing; ++b) {
-      if (!c->pin[b]) CU(cudaMallocHost(&c->pin[b], kStreamChunk + halo + 64));
-      CU(cudaEventSynchronize(c->ev_pin[b]));  // (a previous call's DMA out of pin[b])
+  if (pageable) {
+    for (uint64_t b = 0; b < kPinRing; ++b) CU(cudaEventSynchronize(c->ev_pin[b]));  // (a previous call's DMAs)
+    const size_t need = kStreamChunk + halo + 64;  // (the halo depends on the trie and rules)
+    if (c->pin_bytes < need) {
+      for (void*& q : c->pin)
+        if (q) cudaFreeHost(q), q = nullptr;
+      c->pin_bytes = 0;
+      for (void*& q : c->pin) CU(cudaMallocHost(&q, need));
+      c->pin_bytes = need;
     }
+  }
   auto span = [&](uint64_t i, uint64_t* lo, uint64_t* rd) {
     *lo = i * kStreamChunk;
     *rd = std::min<uint64_t>(std::min<uint64_t>(kStreamChunk, own - *lo) + halo, n - *lo);

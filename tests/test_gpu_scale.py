@@ -189,3 +189,23 @@ def test_streamed_pipeline_868mb_vs_reference(ctx):
                                               minlength=len(long_pats)).astype(np.uint64))
     for at in (chunk - 12, 2 * chunk - 4, 3 * chunk - 1):
         assert at in set(int(o) for o in alerts["offset"])
+
+
+def test_streamed_pipeline_long_pattern_after_short(ctx):
+    """The same context's pageable-text pipeline first with a short halo,
+    then with a 20,000-byte pattern straddling the 256 MiB chunk boundary:
+    the pinned staging ring must grow with the halo (max pattern length - 1)."""
+    chunk = 256 << 20
+    n = chunk + (1 << 20)
+    text = glop.gen_syslog_host(n, 11)
+    short, _ = glop.gen_rules(100, 606)
+    at = chunk - 10_000
+    long_pat = text[at:at + 20_000].tobytes()
+    for pats in (short, short + [long_pat]):
+        trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+        rules = ctx.upload_rules(pats, 8)
+        alerts, counts, s1 = ctx.run_pfac_pipeline(trie, rules, text.ctypes.data, n, False)
+        ref_hits, ref_alerts = reference_pfac(text, pats)
+        assert s1 == len(ref_hits)
+        assert np.array_equal(alerts16(alerts), alerts16(ref_alerts))
+    assert (at, len(pats) - 1) in set(zip(alerts["offset"].tolist(), alerts["rule_id"].tolist()))
