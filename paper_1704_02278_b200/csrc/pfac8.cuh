@@ -61,6 +61,9 @@ constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 #define GLOP_P8_L2PF 0
 #endif
 constexpr uint32_t kP8L2Pf = GLOP_P8_L2PF;
+#ifndef GLOP_P8_FASTREFILL
+#define GLOP_P8_FASTREFILL 1
+#endif
 constexpr uint32_t kP8DmaskLog2 = GLOP_P8_DMASK_LOG2;
 constexpr uint32_t kP8DmaskBytes = 1u << kP8DmaskLog2;  // level-1 d-mask table (shared memory)
 // level-2 prefix bitmap of the pfac8 kernel (shared memory): 2^18 bits by
@@ -337,16 +340,17 @@ __global__ void __launch_bounds__(kP8Threads, 1)
     __syncwarp();
   };
 
-  for (uint32_t t = t0, k = 0; t < t1; ++t, ++k) {
+  // text offset of the window's byte 0, carried across tiles
+  unsigned long long off0 = p.base + (unsigned long long)t0 * kP8Tile - a;
+  for (uint32_t t = t0, k = 0; t < t1; ++t, ++k, off0 += kP8Tile) {
     const uint32_t b = k & 1;
     mbar_wait_a(bars_a + 8 * b, (k >> 1) & 1);
     const uint8_t* sb = bufs + b * kP8Stage;
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
-    const unsigned long long tA = (unsigned long long)t * kP8Tile;
-    const unsigned long long off0 = p.base + tA - a;  // text offset of window byte 0
     const bool edge = t == 0 || t >= t_int_hi;
     uint32_t lo = 0, s_hi = kP8Tile, avail = kP8Stage;
     if (edge) {
+      const unsigned long long tA = (unsigned long long)t * kP8Tile;
       s_hi = (uint32_t)min(own_end - tA, (unsigned long long)kP8Tile);
       avail = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);
       lo = t == 0 ? a : 0;
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
           else emit(c, e.out);
         }
         if (kWalk && tr.lmax > 8) {  // deeper levels: scan.hpp:142-168
+          const unsigned long long tA = (unsigned long long)t * kP8Tile;
           const uint32_t av = (uint32_t)min(n_end - tA, 0x7FFFFFFFull);
           const Entry* T = reinterpret_cast<const Entry*>(tr.table);
           for (uint32_t j = c + 8; j < av; ++j) {
@@ -571,13 +576,23 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         }
       }
     }
-    // buffer b is free: refill it with the segment's tile t + 2
+    // buffer b is free: refill it with the segment's tile t + 2 (interior
+    // tiles, the common case, with one 32-bit test: the general p8_issue
+    // cost ~35 warp instructions per tile in 64-bit range checks)
     __syncwarp();
-    if (lane == 0 && t + 2 < t1) {
-      fence_proxy_async();
-      p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
-               (unsigned long long)(t + 2) * kP8Tile);
-      if (kP8L2Pf) l2_prefetch(t + 2 + kP8L2Pf);
+    if (t + 2 < t1) {
+      if (GLOP_P8_FASTREFILL && t + 2 < t_int_hi) {
+        if (lane == 0) {
+          fence_proxy_async();
+          mbar_arrive_tx_a(bars_a + 8 * b, kP8Stage);
+          bulk_g2s_a(bufs_a + b * kP8Stage, A + (size_t)(t + 2) * kP8Tile, kP8Stage, bars_a + 8 * b);
+        }
+      } else if (lane == 0) {
+        fence_proxy_async();
+        p8_issue(bufs + b * kP8Stage, bufs_a + b * kP8Stage, bars_a + 8 * b, A, a, p.n,
+                 (unsigned long long)(t + 2) * kP8Tile);
+      }
+      if (kP8L2Pf && lane == 0) l2_prefetch(t + 2 + kP8L2Pf);
     }
   }
   if (p.mode == 0) {
