@@ -84,3 +84,24 @@ def test_dropin_cpp_on_three_member_group():
     env = dict(os.environ, GLOP_DEVICES="0,0,0", GLOP_GROUP_MIN_SHARD="512")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_group_pipeline_pageable_shards_over_one_chunk(monkeypatch):
+    """Two members each scanning a > 256 MiB shard of PAGEABLE text: both
+    members' streamed pipelines stage their chunks through the shared host
+    copy pool at the same time; the merge equals the reference."""
+    g = group(2, monkeypatch)
+    n = (600 << 20) + 12345
+    text = glop.gen_syslog_host(n, seed=77)
+    pats, _ = glop.gen_rules(1000, 606)
+    alerts, counts, s1, lines, line_count = g.run_pfac_pipeline(
+        g.upload(glop.build_failureless_trie(pats, 8)), g.upload_rules(pats, 8), text, lines=True)
+    if O.ref() is not None:
+        r_hits, r_alerts = O.ref_pfac_verify(text, pats, 8, compact=True, workers=0, with_lines=True)
+    else:
+        r_hits, r_alerts = O.pfac_verify(text, pats, 8, with_lines=True)
+    assert s1 == len(r_hits)
+    assert np.array_equal(alerts16(alerts), alerts16(r_alerts))
+    assert np.array_equal(lines, r_alerts["line"])
+    assert np.array_equal(counts, np.bincount(r_alerts["rule_id"].astype(np.int64),
+                                              minlength=len(pats)).astype(np.uint64))
