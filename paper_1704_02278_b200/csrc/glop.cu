@@ -1488,7 +1488,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       uint32_t h = jump_slot(key, cap_log2);
       while (jump[h].state1) h = (h + 1) & mask;
       const uint32_t no = off2[s + 1] - off2[s];
-      jump[h] = JumpEntry{key, s + 1, no == 0 ? kOutNone : (no == 1 ? pid2[off2[s]] : kOutMany)};
+      jump[h] = JumpEntry{key, s + 1, jump_out(pid2.data(), off2[s], no)};
     }
   } else {
     jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});

@@ -217,13 +217,21 @@ __host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15
 // Jump-table entry: the trie state reached by a J-byte root path
 // (J = min(lmin, 8)), generalising the reference's depth-1/depth-2 RootJump
 // (scan.hpp:81-108) to J levels.  state+1 in `state1` (0 = empty slot); `out`
-// is the single output pattern id of that state, kOutNone or kOutMany.
+// is the single output pattern id of that state (< kOutList), kOutNone,
+// kOutList | (n - 1) << 24 | o for n <= 127 ids at out_pid[o, o + n) (one
+// dependent load less than the state's CSR bounds), or kOutMany (the CSR
+// list of the state: lists that do not fit the encoding).
 struct JumpEntry {
   unsigned long long key;
   uint32_t state1;
   uint32_t out;
 };
-constexpr uint32_t kOutNone = 0xFFFFFFFFu, kOutMany = 0xFFFFFFFEu;
+constexpr uint32_t kOutNone = 0xFFFFFFFFu, kOutMany = 0xFFFFFFFEu, kOutList = 0x80000000u;
+__host__ __device__ __forceinline__ uint32_t jump_out(const uint32_t* pid, uint32_t o, uint32_t n) {
+  if (n == 0) return kOutNone;
+  if (n == 1) return pid[o] < kOutList ? pid[o] : kOutMany;
+  return n <= 127 && o < (1u << 24) ? kOutList | (n - 1) << 24 | o : kOutMany;
+}
 
 __host__ __device__ __forceinline__ uint32_t jump_slot(unsigned long long key, uint32_t cap_log2) {
   return (uint32_t)((key * 0xD6E8FEB86659FD93ull) >> (64 - cap_log2));
@@ -480,8 +488,11 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
           if (e.key != key) continue;
           const uint32_t st = e.state1 - 1;
           if (e.out != kOutNone) {
-            if (e.out == kOutMany) emit_state(y, st);
-            else emit(y, e.out);
+            if (e.out < kOutList) emit(y, e.out);
+            else if (e.out == kOutMany) emit_state(y, st);
+            else
+              for (uint32_t o = e.out & 0xFFFFFFu, oe = o + ((e.out >> 24) & 0x7Fu) + 1; o < oe; ++o)
+                emit(y, __ldg(tr.out_pid + o));
           }
           if (lmax > J) walk(y, st, y + J);
           return;

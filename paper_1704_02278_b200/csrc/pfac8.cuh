@@ -380,8 +380,11 @@ __global__ void __launch_bounds__(kP8Threads, 1)
         if (e.key != key) continue;
         uint32_t st = e.state1 - 1;
         if (e.out != kOutNone) {
-          if (e.out == kOutMany) emit_state(c, st);
-          else emit(c, e.out);
+          if (e.out < kOutList) emit(c, e.out);
+          else if (e.out == kOutMany) emit_state(c, st);
+          else
+            for (uint32_t o = e.out & 0xFFFFFFu, oe = o + ((e.out >> 24) & 0x7Fu) + 1; o < oe; ++o)
+              emit(c, __ldg(tr.out_pid + o));
         }
         if (kWalk && tr.lmax > 8) {  // deeper levels: scan.hpp:142-168
           const unsigned long long tA = (unsigned long long)t * kP8Tile;
