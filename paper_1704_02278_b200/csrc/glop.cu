@@ -258,8 +258,9 @@ glop_status launch_pfac8(glop_ctx* c, const glop_trie* t, const P8Geom& G, const
   using KF = void (*)(const DevTrie, const P8Params, const P8Layout);
 #define GLOP_P8_K(w, l, c) {pfac8_kernel<w, l, uint16_t, c>, pfac8_kernel<w, l, uint32_t, c>}
 #define GLOP_P8_L(w, c) \
-  GLOP_P8_K(w, 0, c), GLOP_P8_K(w, 1, c), GLOP_P8_K(w, 2, c), GLOP_P8_K(w, 3, c), GLOP_P8_K(w, 4, c)
-  static const KF table[2][2][5][2] = {{{GLOP_P8_L(false, false)}, {GLOP_P8_L(true, false)}},
+  GLOP_P8_K(w, 0, c), GLOP_P8_K(w, 1, c), GLOP_P8_K(w, 2, c), GLOP_P8_K(w, 3, c), GLOP_P8_K(w, 4, c), \
+      GLOP_P8_K(w, 5, c)
+  static const KF table[2][2][6][2] = {{{GLOP_P8_L(false, false)}, {GLOP_P8_L(true, false)}},
                                        {{GLOP_P8_L(false, true)}, {GLOP_P8_L(true, true)}}};
 #undef GLOP_P8_L
 #undef GLOP_P8_K
@@ -1386,7 +1387,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   std::vector<uint8_t> dmask8(kP8DmaskBytes, 0);
   std::vector<unsigned long long> grams8;  // ((prev top byte, cur) << 2 | d-1) of every 8-byte root path
   const bool p8 = lmin >= 8;
-  bool bits8 = false, bloom2 = false, two8 = false, lane8 = false;
+  bool bits8 = false, bloom2 = false, two8 = false, lane8 = false, lists8 = false;
   // visits every root path of length `depth`: cb(path bytes, end state)
   auto for_paths = [&](uint32_t depth, auto&& cb) {
     std::vector<uint8_t> path(depth + 1);
@@ -1489,6 +1490,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
       while (jump[h].state1) h = (h + 1) & mask;
       const uint32_t no = off2[s + 1] - off2[s];
       jump[h] = JumpEntry{key, s + 1, jump_out(pid2.data(), off2[s], no)};
+      lists8 = lists8 || (jump[h].out >= kOutList && jump[h].out != kOutNone && jump[h].out != kOutMany);
     }
   } else {
     jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
@@ -1538,7 +1540,7 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
   t->view.jump = reinterpret_cast<const JumpEntry*>(m + o_jump);
   t->view.dmask8 = m + o_dmask8;
   t->p8 = p8;
-  t->p8_l1 = lane8 ? 4 : two8 && bloom2 ? 3 : bloom2 ? 2 : bits8 ? 1 : 0;
+  t->p8_l1 = lane8 ? 4 : two8 && bloom2 ? (lists8 ? 5 : 3) : bloom2 ? 2 : bits8 ? 1 : 0;
   t->p8_lane_emits = 4 * max_emits;
   t->p8_careful = t->p8_lane_emits > kP8Hits - GLOP_P8_FLUSH_AT || getenv("GLOP_P8_CAREFUL");
   t->view.jump_depth = J;
