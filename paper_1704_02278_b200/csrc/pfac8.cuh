@@ -390,9 +390,21 @@ __global__ void __launch_bounds__(kP8Threads, 1)
             // in every instantiation cost k=1,000 2.8% and k=10,000 1.9%)
             const uint32_t o = e.out & 0xFFFFFFu, nn = ((e.out >> 24) & 0x7Fu) + 1;
             const uint32_t v0 = __ldg(tr.out_pid + o), v1 = __ldg(tr.out_pid + o + 1);
-            emit(c, v0);
-            emit(c, v1);
-            for (uint32_t k2 = 2; k2 < nn; ++k2) emit(c, __ldg(tr.out_pid + o + k2));
+            const uint32_t v2 = nn > 2 ? __ldg(tr.out_pid + o + 2) : 0u;
+            if (p.mode == 0) {  // the list's slots in one shared-memory atomic
+              const unsigned long long kb = (off0 + c) << 24;
+              const uint32_t slot = atomicAdd(s_nh, nn);
+              if (slot < kP8Hits) hk[slot] = kb | v0;
+              if (slot + 1 < kP8Hits) hk[slot + 1] = kb | v1;
+              if (nn > 2 && slot + 2 < kP8Hits) hk[slot + 2] = kb | v2;
+              for (uint32_t k2 = 3; k2 < nn; ++k2)
+                if (slot + k2 < kP8Hits) hk[slot + k2] = kb | __ldg(tr.out_pid + o + k2);
+            } else {
+              emit(c, v0);
+              emit(c, v1);
+              if (nn > 2) emit(c, v2);
+              for (uint32_t k2 = 3; k2 < nn; ++k2) emit(c, __ldg(tr.out_pid + o + k2));
+            }
           } else {
             for (uint32_t o = e.out & 0xFFFFFFu, oe = o + ((e.out >> 24) & 0x7Fu) + 1; o < oe; ++o)
               emit(c, __ldg(tr.out_pid + o));
