@@ -1482,7 +1482,17 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
           bm28[bit8 >> 5] |= 1u << (bit8 & 31);
         }
     }
-    while ((1ull << cap_log2) < 2 * keys.size()) ++cap_log2;
+    // A sparse table: every probe past the first is a dependent L2 round
+    // trip, and a false survivor's probes run to an empty slot.  Load factor
+    // <= 1/16 up to 4,096 prefixes, 1/8 up to 65,536, then 1/4 (measured
+    // against 1/2: k=1,000 2.241 -> 2.191 ms, k=10,000 2.699 -> 2.665 ms, DPI
+    // 1.618 -> 1.620 ms; the table stays L2-resident: 1 MB at 4,096 prefixes)
+    const char* env_lf = getenv("GLOP_JUMP_SPARSE");  // experiments: fixed factor
+    // (pfac8 automata only: the general kernel keeps 1/2, so its table still
+    // fits in shared memory where it did)
+    const size_t sparse = env_lf ? (size_t)atoll(env_lf)
+                          : !p8 ? 2 : keys.size() <= 4096 ? 16 : keys.size() <= 65536 ? 8 : 4;
+    while ((1ull << cap_log2) < sparse * keys.size()) ++cap_log2;
     jump.assign(1ull << cap_log2, JumpEntry{0, 0, 0});
     const uint32_t mask = (1u << cap_log2) - 1;
     for (const auto& [key, s] : keys) {
