@@ -192,7 +192,7 @@ __host__ __device__ __forceinline__ uint32_t p8_lane_off(uint32_t prev, uint32_t
 #else
   const uint32_t pb = (prev >> 16) & 0xFF00u;
 #endif
-  return (p8_mulhi(cur) ^ pb) & 0xFF80u;  // word w at bits 7..15: w * 128
+  return (p8_mulhi(cur) ^ pb) & (kP8DmaskBytes - 128u);  // word w at bits 7..15: w * 128
 }
 template <bool kBits, bool kTwo = false, bool kLane = false>
 __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t prev, uint32_t cur) {
