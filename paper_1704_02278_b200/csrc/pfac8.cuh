@@ -61,6 +61,9 @@ constexpr uint32_t kP8Hits = 32;                   // hit keys per warp in smem
 #define GLOP_P8_L2PF 0
 #endif
 constexpr uint32_t kP8L2Pf = GLOP_P8_L2PF;
+#ifndef GLOP_P8_CARRY
+#define GLOP_P8_CARRY 1
+#endif
 #ifndef GLOP_P8_FASTREFILL
 #define GLOP_P8_FASTREFILL 1
 #endif
@@ -344,6 +347,17 @@ __global__ void __launch_bounds__(kP8Threads, 1)
 
   // text offset of the window's byte 0, carried across tiles
   unsigned long long off0 = p.base + (unsigned long long)t0 * kP8Tile - a;
+  // A tile's last, partial drain round is carried into the next tile's first
+  // round (kCarry): its candidates' words, offset mask, word index and window
+  // offset stay in registers, so the few candidates of small rule sets share
+  // rounds across tiles (k=10: 1.63 -> 1.57 ms).  Only the byte layout (small
+  // gram sets): with the other layouts' ~20 candidates per tile the extra
+  // live registers cost more than the saved rounds (k=1,000 2.20 -> 2.31 ms,
+  // k=100 1.76 -> 1.84 ms).  Not for kWalk automata: their deeper walk reads
+  // the tile's shared-memory window.
+  constexpr bool kCarry = !kWalk && kL1 == 0 && GLOP_P8_CARRY;
+  uint32_t cw0 = 0, cw1 = 0, cw2 = 0, cmm = 0, ci = 1, cL = 0;  // cL: carried lanes (warp-uniform)
+  unsigned long long cbase = 0;
   for (uint32_t t = t0, k = 0; t < t1; ++t, ++k, off0 += kP8Tile) {
     const uint32_t b = k & 1;
     mbar_wait_a(bars_a + 8 * b, (k >> 1) & 1);
@@ -358,8 +372,9 @@ __global__ void __launch_bounds__(kP8Threads, 1)
       lo = t == 0 ? a : 0;
     }
 
+    unsigned long long ebase = off0;  // window offset of the candidate being checked (carried: its own tile's)
     auto emit = [&](uint32_t c, uint32_t pid) {
-      const unsigned long long key = ((off0 + c) << 24) | pid;
+      const unsigned long long key = ((ebase + c) << 24) | pid;
       if (p.mode == 0) {
         const uint32_t slot = atomicAdd(s_nh, 1u);
         if (slot < kP8Hits) hk[slot] = key;
@@ -392,7 +407,7 @@ __global__ void __launch_bounds__(kP8Threads, 1)
             const uint32_t v0 = __ldg(tr.out_pid + o), v1 = __ldg(tr.out_pid + o + 1);
             const uint32_t v2 = nn > 2 ? __ldg(tr.out_pid + o + 2) : 0u;
             if (p.mode == 0) {  // the list's slots in one shared-memory atomic
-              const unsigned long long kb = (off0 + c) << 24;
+              const unsigned long long kb = (ebase + c) << 24;
               const uint32_t slot = atomicAdd(s_nh, nn);
               if (slot < kP8Hits) hk[slot] = kb | v0;
               if (slot + 1 < kP8Hits) hk[slot + 1] = kb | v1;
@@ -505,20 +520,36 @@ __global__ void __launch_bounds__(kP8Threads, 1)
       }
     }
     {
+      // rounds over the virtual list [carried lanes (cL), this tile's queue (qt)]
+      const uint32_t total = (kCarry ? cL : 0u) + qt;
+      if (kCarry) cL = 0;
 #pragma unroll 1
-      for (uint32_t qh = 0; qh < qt; qh += 32) {
-        const uint32_t pend = qt - qh;
+      for (uint32_t qh = 0; qh < total; qh += 32) {
+        const uint32_t pend = total - qh;
         // ---- 8-byte keys of up to 32 candidate words -> prefix bitmap
-        const uint32_t e = lane < pend ? q[qh + lane] : 16u;  // idle lanes: word 1, no bits
-        const uint32_t i = e >> 4;
-        uint32_t mm = kBits ? (e & 1u) * 15u : e & 15u;  // bit layout: all four offsets
-        const uint32_t w0 = sw[i - 1], w1 = sw[i], w2 = sw[i + 1];
-        if (edge) {
+        const uint32_t v = qh + lane, ncar = kCarry ? total - qt : 0u;
+        uint32_t i, mm, w0, w1, w2;
+        if (kCarry && v < ncar) {  // carried from an earlier tile (first round only)
+          i = ci, mm = cmm, w0 = cw0, w1 = cw1, w2 = cw2;
+          ebase = cbase;
+        } else {
+          const uint32_t e = v < total ? q[v - ncar] : 16u;  // idle lanes: word 1, no bits
+          i = e >> 4;
+          mm = kBits ? (e & 1u) * 15u : e & 15u;  // bit layout: all four offsets
+          w0 = sw[i - 1], w1 = sw[i], w2 = sw[i + 1];
+          ebase = off0;
+          if (edge) {
 #pragma unroll
-          for (uint32_t d = 1; d <= 4; ++d) {
-            const uint32_t c = 4 * i - d;
-            if (c < lo || c >= s_hi || c + 8 > avail) mm &= ~(1u << (d - 1));
+            for (uint32_t d = 1; d <= 4; ++d) {
+              const uint32_t c = 4 * i - d;
+              if (c < lo || c >= s_hi || c + 8 > avail) mm &= ~(1u << (d - 1));
+            }
           }
+        }
+        if (kCarry && pend < 32 && t + 1 < t1) {  // partial round: carry it into the next tile
+          cw0 = w0, cw1 = w1, cw2 = w2, cmm = lane < pend ? mm : 0u, ci = i, cbase = ebase;
+          cL = pend;
+          break;
         }
         uint32_t surv = 0;
 #pragma unroll
