@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(kWarpKernelThreads, 1)
 #ifdef GLOP_EXP_NODRAIN
         qn = 0;
 #endif
+        __syncwarp();  // the queue entries other lanes pushed are visible (racecheck)
         for (uint32_t e0 = 0; e0 < qn; e0 += 32) {
           const uint32_t v = e0 + lane < qn ? q[e0 + lane] : 0u;
           const uint32_t c = __popc(v & 0xFFu);
