@@ -535,3 +535,30 @@ def test_prefix8_hit_density_sweep(ctx, torch_cuda, layout, monkeypatch):
         ref = O.pfac_scan(text, O.Trie(pats, 8))
         got = dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_PREFIX8)
         assert got.tobytes() == ref.tobytes(), (layout, trial, len(got), len(ref))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_prefix8_byte_layout_carried_rounds(ctx, torch_cuda, seed):
+    """Small rule sets (<= 64 grams: the byte layout, whose partial drain
+    rounds are carried in registers from tile to tile): random texts with
+    the patterns spliced at random places (every tile edge, the halo, the
+    last bytes), random shards (own / base / misaligned start) == oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 600_000))
+    text = (rng.integers(0, 4, n) + 65).astype(np.uint8) if seed % 2 else glop.gen_syslog_host(n, seed)
+    k = int(rng.integers(1, 15))
+    pats = [bytes((rng.integers(0, 4, int(rng.integers(8, 13))) + 65).astype(np.uint8)) for _ in range(k)]
+    for _ in range(int(rng.integers(0, 400))):  # occurrences, several per 2 KB tile
+        p = pats[int(rng.integers(0, k))]
+        at = int(rng.integers(0, max(1, n - len(p))))
+        text[at:at + len(p)] = np.frombuffer(p, np.uint8)[: n - at]
+    trie = ctx.upload(glop.build_failureless_trie(pats, 8))
+    ref = O.pfac_scan(text, O.Trie(pats, 8))
+    assert dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_PREFIX8).tobytes() == ref.tobytes()
+    off = int(rng.integers(0, 16))
+    if n > off + 64:
+        own = int(rng.integers(1, n - off))
+        r = ref[(ref["offset"] >= off) & (ref["offset"] < off + own)].copy()
+        r["offset"] -= off
+        got = dev_scan(ctx, torch_cuda, trie, text, glop.PFAC_PREFIX8, own=own, offset=off)
+        assert got.tobytes() == r.tobytes()
