@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the Gbps-vs-pattern-count sweep (pfac, N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline work")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size result digests")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: the alert gather / count exchange over CUDA IPC + copy engines (p2p, peer.py) "
+                         "or NCCL collectives")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the configs[0]/[1]/[4] sub-blocks of the default line")
     a = ap.parse_args()
@@ -428,19 +431,33 @@ def main():
     # 0, NCCL) runs on its own stream while step i+1's scan runs on the
     # library stream: alerts / counts double-buffered, one ticket each.
     overlapped = world > 1 and kernel == glop.PFAC_AUTO
+    p2p = None
     if overlapped:
         comm = torch.cuda.Stream()
-        a_bufs = [d_alerts, torch.empty_like(d_alerts)]
-        c_bufs = [d_counts, torch.zeros_like(d_counts)]
         ev_done = [torch.cuda.Event(), torch.cuda.Event()]
         ev_freed = [torch.cuda.Event(), torch.cuda.Event()]
         xtickets = ctx.host_alloc(glop.TICKET_BYTES * 2)
         xres = [None, None]
+        if args.exchange == "p2p":
+            # CUDA IPC + copy engines (peer.py): the pipeline writes straight into
+            # the exchange buffers; the root pulls them beside the next scan
+            from paper_1704_02278_b200.peer import PeerExchange
+
+            gloo = None if dist.get_backend() == "gloo" else dist.new_group(backend="gloo")
+            p2p = PeerExchange(ctx, rank, world, args.patterns, cap, group=gloo)
+            a_ptrs, c_ptrs = p2p.alerts, p2p.counts_buf
+        else:
+            a_bufs = [d_alerts, torch.empty_like(d_alerts)]
+            c_bufs = [d_counts, torch.zeros_like(d_counts)]
+            a_ptrs, c_ptrs = [t.data_ptr() for t in a_bufs], [t.data_ptr() for t in c_bufs]
 
         def exchange(i):
             b = i & 1
             ev_done[b].synchronize()  # step i's scan is done (step i+1's is running)
             xres[b] = glop.ticket_result(xtickets + glop.TICKET_BYTES * b)
+            if p2p is not None:
+                p2p.exchange(b, xres[b][1], ctx.stream, ev_done[b])
+                return
             with torch.cuda.stream(comm):
                 comm.wait_event(ev_done[b])
                 dist.all_reduce(c_bufs[b])
@@ -450,16 +467,19 @@ def main():
         def run_overlapped(nsteps):
             for i in range(nsteps):
                 b = i & 1
-                stream.wait_event(ev_freed[b])  # buffer b's previous exchange has finished
-                ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), sh.read, a_bufs[b].data_ptr(), cap,
-                                                   c_bufs[b].data_ptr(), xtickets + glop.TICKET_BYTES * b,
-                                                   own=sh.own, base=sh.lo)
+                if p2p is None:
+                    stream.wait_event(ev_freed[b])  # buffer b's previous exchange has finished
+                ctx.run_pfac_pipeline_device_async(trie, rules, d_text.data_ptr(), sh.read, a_ptrs[b], cap, c_ptrs[b],
+                                                   xtickets + glop.TICKET_BYTES * b, own=sh.own, base=sh.lo)
                 ev_done[b].record(stream)
                 if i:
                     exchange(i - 1)
             if nsteps:
                 exchange(nsteps - 1)
-                stream.wait_event(ev_freed[(nsteps - 1) & 1])
+                if p2p is None:
+                    stream.wait_event(ev_freed[(nsteps - 1) & 1])
+                elif rank == 0:  # the last exchange's copies are inside the timed region
+                    stream.wait_stream(p2p.comm)
             return xres[(nsteps - 1) & 1]
 
     for _ in range(max(args.warmup, 3)):
@@ -496,13 +516,28 @@ def main():
                 ctx.run_pfac_pipeline_device(trie, rules, d_text.data_ptr(), sh.read, d_alerts.data_ptr(), cap,
                                              d_counts.data_ptr(), own=sh.own, base=sh.lo)
                 kms.append(ctx.last_kernel_ms())
-            if overlapped:  # the counts of the last exchanged step, for the results block
+            if overlapped and p2p is None:  # the counts of the last exchanged step, for the results block
                 d_counts.copy_(c_bufs[(args.steps - 1) & 1])
         if world == 1:
             sampler.hold(lambda: (step(), ctx.synchronize()))
         ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
         kernel_ms = max_over_ranks(statistics.mean(kms))
         total_alerts = int(d_counts.sum().item())
+        gathered = None
+        if p2p is not None:  # the root's gathered result of the last exchanged step (rank order)
+            got = p2p.gathered((args.steps - 1) & 1)
+            if got is not None:
+                from paper_1704_02278_b200.parity import alerts16
+
+                import hashlib
+
+                g_alerts, g_counts = got
+                total_alerts = int(g_counts.sum())
+                gathered = {"alerts": int(len(g_alerts)), "alerts16_sha": hashlib.sha256(
+                    np.ascontiguousarray(alerts16(g_alerts)).tobytes()).hexdigest(),
+                            "counts_sha": hashlib.sha256(g_counts.astype("<u8").tobytes()).hexdigest()}
+            dist.barrier(group=p2p.group)
+            p2p.close()
 
         e2e = None
         if not args.no_e2e:
@@ -530,6 +565,7 @@ def main():
                          "step_share": round(kernel_ms / ms, 3)},
             "gpu_launches": launches, "clocks": clocks,
             "results": {"stage1_hits_per_gpu_step": int(nh), "alerts_per_step": total_alerts,
+                        **({"exchange": args.exchange, "gathered": gathered} if world > 1 else {}),
                         "trie": {"states": info.state_count, "classes": info.classes, "q": info.q,
                                  "stride": info.stride, "table_bytes": int(info.table_bytes),
                                  "table_in_smem": bool(info.table_in_smem)}}}

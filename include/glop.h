@@ -446,6 +446,31 @@ glop_status glop_gen_reference_log(uint8_t* out, uint64_t size, uint32_t seed, u
 glop_status glop_gen_rules(uint32_t k, uint32_t seed, uint32_t len, uint8_t* bytes,
                            uint8_t* is_vocab);
 
+/* ---- peer exchange between processes (one process per GPU) --------------
+ * The one exchange of the sharded path (per-rank alert lists
+ * to the root, per-pattern counts) done with CUDA IPC and copy-engine
+ * copies over NVLink instead of NCCL kernels: a persistent scan kernel holds
+ * every SM, so an SM-based collective on another stream could not start
+ * until it ends, while copy engines run beside it.  Handles are 64 opaque
+ * bytes the caller moves between processes (e.g. torch.distributed object
+ * collectives); streams are cudaStream_t as void* (glop_ctx_stream).
+ *   glop_peer_alloc       device buffer on ctx's device + its IPC handle
+ *   glop_peer_open        map another process's buffer (any device)
+ *   glop_peer_event       interprocess event + its handle;
+ *   glop_peer_event_open  the other process's event
+ *   glop_peer_record / glop_peer_wait   event record on / wait by a stream
+ *   glop_peer_copy        async device-to-device copy on a stream (copy engine) */
+glop_status glop_peer_alloc(glop_ctx* ctx, uint64_t bytes, void** d_ptr, void* handle64);
+glop_status glop_peer_free(glop_ctx* ctx, void* d_ptr);
+glop_status glop_peer_open(glop_ctx* ctx, const void* handle64, void** d_ptr);
+glop_status glop_peer_close(glop_ctx* ctx, void* d_ptr);
+glop_status glop_peer_event(glop_ctx* ctx, void** event, void* handle64);
+glop_status glop_peer_event_open(glop_ctx* ctx, const void* handle64, void** event);
+glop_status glop_peer_event_destroy(glop_ctx* ctx, void* event);
+glop_status glop_peer_record(glop_ctx* ctx, void* event, void* stream);
+glop_status glop_peer_wait(glop_ctx* ctx, void* stream, void* event);
+glop_status glop_peer_copy(glop_ctx* ctx, void* dst, const void* src, uint64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1873,6 +1873,107 @@ glop_status glop_last_kernel_ms(glop_ctx* c, float* ms) {
 }
 
 uint64_t glop_ctx_launch_count(glop_ctx* c) { return c ? c->launches : 0; }
+
+// ---- peer exchange (CUDA IPC + copy engines), glop.h
+static_assert(sizeof(cudaIpcMemHandle_t) == 64 && sizeof(cudaIpcEventHandle_t) == 64, "64-byte IPC handles");
+
+glop_status glop_peer_alloc(glop_ctx* c, uint64_t bytes, void** d_ptr, void* handle64) {
+  if (!c || !d_ptr || !handle64) return fail(GLOP_EINVAL, "glop_peer_alloc: null argument");
+  Dev g(c->device);
+  *d_ptr = nullptr;
+  if (cudaMalloc(d_ptr, std::max<uint64_t>(bytes, 16)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GLOP_ENOMEM, "glop_peer_alloc: cudaMalloc");
+  }
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *d_ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*d_ptr);
+    *d_ptr = nullptr;
+    return fail(GLOP_ECUDA, std::string("glop_peer_alloc: ") + cudaGetErrorString(e));
+  }
+  memcpy(handle64, &h, 64);
+  return GLOP_OK;
+}
+
+glop_status glop_peer_free(glop_ctx* c, void* d_ptr) {
+  if (!c) return fail(GLOP_EINVAL, "glop_peer_free: null context");
+  Dev g(c->device);
+  if (d_ptr) CU(cudaFree(d_ptr));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_open(glop_ctx* c, const void* handle64, void** d_ptr) {
+  if (!c || !handle64 || !d_ptr) return fail(GLOP_EINVAL, "glop_peer_open: null argument");
+  Dev g(c->device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  CU(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_close(glop_ctx* c, void* d_ptr) {
+  if (!c) return fail(GLOP_EINVAL, "glop_peer_close: null context");
+  Dev g(c->device);
+  if (d_ptr) CU(cudaIpcCloseMemHandle(d_ptr));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_event(glop_ctx* c, void** event, void* handle64) {
+  if (!c || !event || !handle64) return fail(GLOP_EINVAL, "glop_peer_event: null argument");
+  Dev g(c->device);
+  cudaEvent_t ev;
+  CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
+  cudaIpcEventHandle_t h;
+  const cudaError_t e = cudaIpcGetEventHandle(&h, ev);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    return fail(GLOP_ECUDA, std::string("glop_peer_event: ") + cudaGetErrorString(e));
+  }
+  memcpy(handle64, &h, 64);
+  *event = ev;
+  return GLOP_OK;
+}
+
+glop_status glop_peer_event_open(glop_ctx* c, const void* handle64, void** event) {
+  if (!c || !handle64 || !event) return fail(GLOP_EINVAL, "glop_peer_event_open: null argument");
+  Dev g(c->device);
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle64, 64);
+  cudaEvent_t ev;
+  CU(cudaIpcOpenEventHandle(&ev, h));
+  *event = ev;
+  return GLOP_OK;
+}
+
+glop_status glop_peer_event_destroy(glop_ctx* c, void* event) {
+  if (!c) return fail(GLOP_EINVAL, "glop_peer_event_destroy: null context");
+  Dev g(c->device);
+  if (event) CU(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_record(glop_ctx* c, void* event, void* stream) {
+  if (!c || !event) return fail(GLOP_EINVAL, "glop_peer_record: null argument");
+  Dev g(c->device);
+  CU(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_wait(glop_ctx* c, void* stream, void* event) {
+  if (!c || !event) return fail(GLOP_EINVAL, "glop_peer_wait: null argument");
+  Dev g(c->device);
+  CU(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0));
+  return GLOP_OK;
+}
+
+glop_status glop_peer_copy(glop_ctx* c, void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (!c || (bytes && (!dst || !src))) return fail(GLOP_EINVAL, "glop_peer_copy: null argument");
+  if (!bytes) return GLOP_OK;
+  Dev g(c->device);
+  CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return GLOP_OK;
+}
 uint64_t glop_ctx_fallback_count(glop_ctx* c) { return c ? c->fallbacks : 0; }
 
 glop_status glop_run_pfac_pipeline(glop_ctx* c, const glop_trie* t, const glop_rules* r, const uint8_t* text,

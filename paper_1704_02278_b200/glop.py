@@ -118,6 +118,17 @@ def kmp_ticket_result(ticket_ptr: int):
     return no.value, cmp_.value
 _sig("glop_chunked_ac_scan", vp, vp, vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(vp), u64p)
 TICKET_BYTES = 8 * 8 + 3 * 8 + 2 * 4  # glop_pipeline_ticket
+# peer exchange (CUDA IPC + copy engines; glop.h "peer exchange", peer.py)
+_sig("glop_peer_alloc", vp, C.c_uint64, C.POINTER(vp), vp)
+_sig("glop_peer_free", vp, vp)
+_sig("glop_peer_open", vp, vp, C.POINTER(vp))
+_sig("glop_peer_close", vp, vp)
+_sig("glop_peer_event", vp, C.POINTER(vp), vp)
+_sig("glop_peer_event_open", vp, vp, C.POINTER(vp))
+_sig("glop_peer_event_destroy", vp, vp)
+_sig("glop_peer_record", vp, vp, vp)
+_sig("glop_peer_wait", vp, vp, vp)
+_sig("glop_peer_copy", vp, vp, vp, C.c_uint64, vp)
 
 
 def ticket_result(ticket_ptr: int):
