@@ -684,25 +684,63 @@ __device__ __forceinline__ unsigned long long block_sum_counts(const unsigned lo
   return s;
 }
 
+// Exclusive prefix of min(counts[g0 + j], cap) over j in [0, n] into
+// s_pre[0..n] (n <= kRangeMax), computed by warp 0 32 entries at a time;
+// the caller synchronizes the CTA before reading it.
+constexpr uint32_t kRangeMax = 64;
+__device__ __forceinline__ void range_prefix(const unsigned long long* counts, uint32_t g0, uint32_t n,
+                                             unsigned long long cap, unsigned long long* s_pre) {
+  if (threadIdx.x >= 32) return;
+  const uint32_t lane = threadIdx.x;
+  unsigned long long run = 0;
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    const unsigned long long c = j < n ? min(counts[g0 + j], cap) : 0ull;
+    unsigned long long incl = c;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (j < n) s_pre[j] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) s_pre[n] = run;
+}
+
 // Concatenates the per-warp regions (each already in text order) in warp
 // order, each CTA a contiguous range of regions: the range's output offset is
 // the sum of the counts before it (computed here -- no separate prefix
-// launch), region g's hits go to out[prefix(g), prefix(g) + counts[g]).
+// launch), the regions' offsets inside the range a prefix in shared memory,
+// and each warp copies whole regions (round robin), so the regions' count
+// loads and copies overlap instead of running one region after another.
 // Launched before the host has looked at the scan's flags: records past
 // `cap` or beyond a region are not copied, and a flagged scan is redone.
 template <typename Rec>
 __global__ void __launch_bounds__(256) gather_regions_kernel(const unsigned long long* counts, uint32_t regions,
                                                              unsigned long long region, const Rec* staging,
                                                              Rec* out, unsigned long long cap) {
-  __shared__ unsigned long long s_red[32];
+  __shared__ unsigned long long s_red[32], s_pre[kRangeMax + 1];
   const uint32_t per = (regions + gridDim.x - 1) / gridDim.x;
   const uint32_t g0 = min(blockIdx.x * per, regions), g1 = min(g0 + per, regions);
-  unsigned long long dst = block_sum_counts(counts, g0, region, s_red);
-  for (uint32_t g = g0; g < g1; ++g) {
-    const unsigned long long c = min(counts[g], region);
-    const Rec* src = staging + (unsigned long long)g * region;
-    for (unsigned long long h = threadIdx.x; h < c && dst + h < cap; h += blockDim.x) out[dst + h] = src[h];
-    dst += c;
+  const unsigned long long base = block_sum_counts(counts, g0, region, s_red);
+  if (per > kRangeMax) {  // (not with the launch geometries used; kept exact)
+    unsigned long long dst = base;
+    for (uint32_t g = g0; g < g1; ++g) {
+      const unsigned long long c = min(counts[g], region);
+      const Rec* src = staging + (unsigned long long)g * region;
+      for (unsigned long long h = threadIdx.x; h < c && dst + h < cap; h += blockDim.x) out[dst + h] = src[h];
+      dst += c;
+    }
+    return;
+  }
+  range_prefix(counts, g0, g1 - g0, region, s_pre);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (uint32_t j = threadIdx.x >> 5; j < g1 - g0; j += nw) {
+    const unsigned long long d0 = base + s_pre[j], c = s_pre[j + 1] - s_pre[j];
+    const Rec* src = staging + (unsigned long long)(g0 + j) * region;
+    for (unsigned long long h = lane; h < c && d0 + h < cap; h += 32) out[d0 + h] = src[h];
   }
 }
 
