@@ -1458,11 +1458,12 @@ glop_status glop_trie_upload(glop_ctx* c, const int32_t* dense, uint32_t Q, cons
           const uint32_t w = p8_lane_off(prev, cur), b1 = p8_bit1(cur) & 31u;
           for (uint32_t l = 0; l < 32; ++l) dmask8[w + 4 * l + (b1 >> 3)] |= (uint8_t)(1u << (b1 & 7));
         } else if (bits8) {  // little-endian bits of the u32 words
-          const uint32_t w = p8_word_off(prev, cur);
+          const bool pv = two8 && GLOP_P8_BIT2_PRMT;  // (must match p8_dmask)
+          const uint32_t w = pv ? p8_word_off2(prev, cur) : p8_word_off(prev, cur);
           const uint32_t b1 = p8_bit1(cur) & 31u;
           dmask8[w + (b1 >> 3)] |= (uint8_t)(1u << (b1 & 7));
           if (two8) {  // second bit in the same 32-bit word
-            const uint32_t b2 = p8_bit2(cur) & 31u;
+            const uint32_t b2 = (pv ? p8_pb2(prev, cur) : p8_bit2(cur)) & 31u;
             dmask8[w + (b2 >> 3)] |= (uint8_t)(1u << (b2 & 7));
           }
         } else {

@@ -168,6 +168,23 @@ __host__ __device__ __forceinline__ uint32_t p8_word_off(uint32_t prev, uint32_t
 // funnel-shift amounts (low 5 bits used) of the gram's bit(s) in that word
 __host__ __device__ __forceinline__ uint32_t p8_bit1(uint32_t cur) { return cur; }
 __host__ __device__ __forceinline__ uint32_t p8_bit2(uint32_t cur) { return cur >> 8; }
+#ifndef GLOP_P8_BIT2_PRMT
+#define GLOP_P8_BIT2_PRMT 1
+#endif
+// two-bit layout, GLOP_P8_BIT2_PRMT: one PRMT puts cur's byte 1 at bits 0..7
+// and prev's top byte at bits 8..15 (bits 16..31 are masked off); XORed into
+// the word offset it also supplies the second bit's funnel amount, the same
+// (cur >> 8) & 31 as p8_bit2, without the shift
+__host__ __device__ __forceinline__ uint32_t p8_pb2(uint32_t prev, uint32_t cur) {
+#ifdef __CUDA_ARCH__
+  return __byte_perm(prev, cur, 0x4435);
+#else
+  return ((cur >> 8) & 0xFFu) | ((prev >> 16) & 0xFF00u) | ((cur & 0xFFu) * 0x01010000u);
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t p8_word_off2(uint32_t prev, uint32_t cur) {
+  return (p8_mulhi(cur) ^ p8_pb2(prev, cur)) & (kP8DmaskBytes - 4);
+}
 // the gram's byte in the 64 KB d-mask table (byte layout)
 __host__ __device__ __forceinline__ uint32_t p8_byte_off(uint32_t prev, uint32_t cur) {
   return ((cur * kP8HashMul) ^ (prev & 0xFF000000u)) >> (32 - kP8DmaskLog2);
@@ -204,6 +221,11 @@ __device__ __forceinline__ uint32_t p8_dmask(const uint8_t* dm, uint32_t prev, u
     return __funnelshift_r(w, w, p8_bit1(cur));
   }
   if (kBits) {  // bit p8_bit1 of the word, in bit 0 (bits 1..31: don't care)
+    if (kTwo && GLOP_P8_BIT2_PRMT) {
+      const uint32_t pb = p8_pb2(prev, cur);
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + ((p8_mulhi(cur) ^ pb) & (kP8DmaskBytes - 4)));
+      return __funnelshift_r(w, w, p8_bit1(cur)) & __funnelshift_r(w, w, pb);
+    }
     const uint32_t w = *reinterpret_cast<const uint32_t*>(dm + p8_word_off(prev, cur));
     if (kTwo) return __funnelshift_r(w, w, p8_bit1(cur)) & __funnelshift_r(w, w, p8_bit2(cur));
     return __funnelshift_r(w, w, p8_bit1(cur));
